@@ -1,0 +1,174 @@
+/*
+ * srt.h -- C ABI of libsrt, the sm_100a stochastic Gaussian ray tracer.
+ *
+ * Plain pointers and sizes only; every entry point returns an srt_status and
+ * never throws.  Host-pointer entry points are synchronous and mirror the
+ * reference operator boundary (/root/reference/pkg/src/splatray/kernels.py);
+ * *_device entry points take device pointers plus a cudaStream_t (passed as
+ * void*) and are asynchronous on that stream.
+ *
+ * Interface map (reference file:line -> entry point):
+ *   SplatAsset.packed          assets.py:145-171   -> srt_scene_create
+ *   scene_bvh / bvh.build      render.py:97-100,
+ *                              bvh.py:87-193       -> srt_bvh_build (GPU LBVH)
+ *   bvh= argument of render()  render.py:129,164   -> srt_bvh_upload
+ *   kernels.trace_batch        kernels.py:527-540  -> srt_trace_rays
+ *   kernels.render_stochastic  kernels.py:622-673  -> srt_render
+ *                                                     (= srt_trace_pass_device
+ *                                                      + srt_shade_pass_device
+ *                                                      per pass)
+ *   kernels.transmittance_batch kernels.py:544-557 -> srt_transmittance_rays
+ *   (new) multi-GPU tile gather                    -> srt_unpack_tiles_device
+ */
+#ifndef SRT_H
+#define SRT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t srt_status;
+#define SRT_OK 0
+#define SRT_ERR_INVALID_ARG 1
+#define SRT_ERR_CUDA 2
+#define SRT_ERR_OOM 3
+#define SRT_ERR_NO_BVH 4
+#define SRT_ERR_STACK_OVERFLOW 5
+#define SRT_ERR_UNSUPPORTED 6
+
+/* acceptance-draw generators (kernels.py:354 is the reference's trig hash) */
+#define SRT_RNG_COUNTER 1 /* u = U24(mix(seed, ray_id, sample, prim)) */
+#define SRT_RNG_TABLE 2   /* u = table[prim * table_slots + slot] (scripted tests) */
+
+typedef struct SrtScene SrtScene;
+
+/* Inputs of SplatAsset.packed (assets.py:188-195): C-contiguous float64. */
+typedef struct {
+    int64_t n;               /* primitives (>= 0) */
+    const double *means;     /* (n, 3) */
+    const double *cov_inv6;  /* (n, 6): a00 a01 a02 a11 a12 a22 (assets.py:156-162) */
+    const double *opacities; /* (n,) */
+    const double *sh;        /* (n, 3, K), K = (sh_degree + 1)^2, channel major; may be NULL */
+    int32_t sh_degree;       /* 0..3 */
+} SrtSceneDesc;
+
+/* The 14 camera scalars of render.py:144-150, in that order. */
+typedef struct {
+    double position[3];
+    double right[3];
+    double up[3];
+    double forward[3];
+    double half_w, half_h;
+} SrtCamera;
+
+typedef struct {
+    int32_t width, height;
+    int32_t passes;     /* ceil(spp / multisample)  (config.py:87-89) */
+    int32_t nslots;     /* multisample N, 1..256    (config.py:79-80) */
+    int32_t mode;       /* 0 = mean depth, 1 = center depth (render.py:153) */
+    int32_t clip;       /* far-bound clipping (render() always passes 1) */
+    double s2;          /* cutoff_s^2 (render.py:154) */
+    uint32_t seed;      /* jitter + counter RNG seed */
+    int32_t pass0;      /* global index of the first pass (sample sharding) */
+    double background[3];
+    int32_t shard_index; /* image-tile sharding: this rank renders 16x16 tiles */
+    int32_t shard_count; /* t with t % shard_count == shard_index (1 = all)   */
+} SrtRenderParams;
+
+typedef struct {
+    double t_min, t_max;
+    int32_t mode;
+    int32_t clip;
+    double s2;
+    int32_t rng;             /* SRT_RNG_COUNTER or SRT_RNG_TABLE */
+    uint32_t seed;
+    uint32_t ray_id0;        /* ray i uses ray_id = ray_id0 + i */
+    uint32_t sample0;        /* slot k uses sample = sample0 + k */
+    const double *table;     /* SRT_RNG_TABLE: host (n, table_slots) uniforms */
+    int64_t table_slots;
+} SrtTraceParams;
+
+/* ---- library ----------------------------------------------------------- */
+const char *srt_last_error(void);      /* thread-local message of the last failure */
+const char *srt_version(void);
+int32_t srt_device_count(void);
+
+/* ---- scene ------------------------------------------------------------- */
+/* Upload a packed scene to `device` (fp32 SoA records in HBM). */
+srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene **out);
+srt_status srt_scene_destroy(SrtScene *scene);
+/* Build the GPU LBVH over each primitive's cutoff-ellipsoid AABB
+ * (Mahalanobis radius cutoff_s; Morton codes, radix sort, Karras hierarchy,
+ * atomic bottom-up refit).  Replaces bvh.build (bvh.py:87-193). */
+srt_status srt_bvh_build(SrtScene *scene, double cutoff_s);
+/* Upload a reference-layout BVH (bvh.py:29-47): node_lo/node_hi (M,3) f64,
+ * node_left/node_right/node_count (M,) i64, prim_order (n,) i64,
+ * prim_lo/prim_hi (n,3) f64. */
+srt_status srt_bvh_upload(SrtScene *scene, int64_t num_nodes, const double *node_lo,
+                          const double *node_hi, const int64_t *node_left,
+                          const int64_t *node_right, const int64_t *node_count,
+                          const int64_t *prim_order, const double *prim_lo,
+                          const double *prim_hi);
+/* Introspection: node count, tree depth, primitive count, device bytes. */
+srt_status srt_bvh_info(const SrtScene *scene, int64_t *num_nodes, int32_t *depth,
+                        int64_t *num_prims, int64_t *device_bytes);
+/* Copy the built BVH back in the reference layout (for invariant tests).
+ * Arrays sized by srt_bvh_info: nodes M = 2n-1 (or 0), prims n. */
+srt_status srt_bvh_download(const SrtScene *scene, float *node_lo, float *node_hi,
+                            int64_t *node_left, int64_t *node_right, int64_t *node_count,
+                            int64_t *prim_order, float *prim_lo, float *prim_hi);
+
+/* ---- explicit rays (kernels.trace_batch) --------------------------------- */
+/* origins/dirs: host (R,3) f64.  out_t (R,nslots) f64 (+inf on miss),
+ * out_id (R,nslots) i64 (-1 on miss). */
+srt_status srt_trace_rays(const SrtScene *scene, const SrtTraceParams *params,
+                          const double *origins, const double *dirs, int64_t num_rays,
+                          int32_t nslots, double *out_t, int64_t *out_id);
+/* Device variant: d_rays is (R, 6) f64 [ox oy oz dx dy dz]; out_t f32, out_id i32. */
+srt_status srt_trace_rays_device(const SrtScene *scene, const SrtTraceParams *params,
+                                 const double *d_rays, int64_t num_rays, int32_t nslots,
+                                 float *d_out_t, int32_t *d_out_id, void *stream);
+/* kernels.transmittance_batch: prod(1 - alpha) over every valid candidate. */
+srt_status srt_transmittance_rays(const SrtScene *scene, const double *origins,
+                                  const double *dirs, int64_t num_rays, double t_min,
+                                  double t_max, int32_t mode, double s2, double *out);
+
+/* ---- full frames (kernels.render_stochastic) ----------------------------- */
+/* Host outputs out_rgb (H,W,3) f64 and out_op (H,W) f64 = per-pixel means.
+ * out_ids (optional, may be NULL): (H,W,nslots) i64 slot ids of pass pass0. */
+srt_status srt_render(const SrtScene *scene, const SrtCamera *camera,
+                      const SrtRenderParams *params, double *out_rgb, double *out_op,
+                      int64_t *out_ids);
+/* One pass, device buffers.  d_hits: (H*W*nslots) i32 scratch written by the
+ * trace stage and read by the shade stage.  d_accum: (H*W) float4 running
+ * sums (rgb, hits); pass `pass` (absolute) is traced, and the shade stage
+ * adds it, zeroing the accumulator first when `first` is set.  When `last`
+ * is set the shade stage also resolves accum / (passes * nslots) into d_out
+ * ((H*W) float4 rgba, rgba = (r, g, b, opacity)).  With shard_count > 1 the
+ * buffers are tile-compact: local tile j occupies pixels [256 j, 256 j + 256). */
+srt_status srt_trace_pass_device(const SrtScene *scene, const SrtCamera *camera,
+                                 const SrtRenderParams *params, int32_t pass, int32_t *d_hits,
+                                 void *stream);
+srt_status srt_shade_pass_device(const SrtScene *scene, const SrtCamera *camera,
+                                 const SrtRenderParams *params, int32_t pass,
+                                 const int32_t *d_hits, float *d_accum, int32_t first,
+                                 int32_t last, float *d_out, void *stream);
+/* Whole frame on device: all passes, d_out (H*W) float4 rgba means. */
+srt_status srt_render_device(const SrtScene *scene, const SrtCamera *camera,
+                             const SrtRenderParams *params, int32_t *d_hits, float *d_accum,
+                             float *d_out, void *stream);
+/* Number of 16x16 tiles a shard owns (buffer sizing for tile-compact layout). */
+int64_t srt_shard_tiles(int32_t width, int32_t height, int32_t shard_index,
+                        int32_t shard_count);
+/* Scatter gathered tile-compact shards [shard_count][max_tiles*256] float4
+ * into a full (H*W) float4 frame. */
+srt_status srt_unpack_tiles_device(const float *d_gathered, int32_t width, int32_t height,
+                                   int32_t shard_count, int64_t max_tiles, float *d_frame,
+                                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRT_H */

@@ -1,0 +1,117 @@
+"""Generate tests/golden/*.npz from the UNMODIFIED reference (run in the build
+container, where /root/reference exists; the fixtures travel, the reference
+does not).  TEST INFRASTRUCTURE.
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python oracle/gen_golden.py
+
+Every fixture is produced by the reference's own public functions:
+sampling.hash_position / pixel_jitter, synthetic.random_cloud, assets.packed
+/ aabb_arrays, bvh.build, kernels.trace_batch / transmittance_batch /
+render_stochastic (via render.render).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import importlib
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+
+
+def _digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def main() -> None:
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, REF)
+    from splatray import kernels, sampling, synthetic
+    from splatray import bvh as B
+    from splatray.config import RenderSettings
+
+    R = importlib.import_module("splatray.render")
+    OUT.mkdir(parents=True, exist_ok=True)
+    tmax = float(np.finfo(np.float64).max)
+    s = 2.0 * np.sqrt(2.0)
+
+    # 1. randomness ------------------------------------------------------
+    rng = np.random.default_rng(2024)
+    pts = rng.uniform(-20, 20, size=(512, 3))
+    slots = rng.integers(0, 8, size=512)
+    hv = np.array([sampling.hash_position(p, int(k)) for p, k in zip(pts, slots)])
+    jit_args = np.array([[px, py, f, sd] for px, py, f, sd in
+                         zip(rng.integers(0, 4000, 256), rng.integers(0, 3000, 256), rng.integers(0, 5000, 256),
+                             rng.integers(0, 100, 256))], dtype=np.int64)
+    jit = np.array([sampling.pixel_jitter((a[0], a[1]), int(a[2]), int(a[3])) for a in jit_args])
+    np.savez_compressed(OUT / "sampling.npz", points=pts, slots=slots, hash=hv, jitter_args=jit_args, jitter=jit)
+
+    # 2. synthetic assets and packing (digests only; arrays are regenerated)
+    digests = {}
+    for name, kw in {"c1_10k_sh0": dict(n=10_000, seed=0, sh_degree=0),
+                     "c2_100k_sh3_density": dict(n=100_000, seed=0, sh_degree=3,
+                                                 scale_range=(0.02 * (0.1) ** (1 / 3), 0.25 * (0.1) ** (1 / 3))),
+                     "small_400_s31": dict(n=400, seed=31)}.items():
+        a = synthetic.random_cloud(**kw)
+        pk = a.packed
+        lo, hi = a.aabb_arrays(s)
+        digests[name] = {"asset": _digest(a.means, a.rotations, a.scales, a.opacities, a.sh),
+                         "packed": _digest(pk.means, pk.cov_inv6, pk.opacities, pk.sh),
+                         "aabb": _digest(lo, hi)}
+    np.savez_compressed(OUT / "assets.npz", **{f"{k}__{f}": np.array(v[f]) for k, v in digests.items() for f in v})
+
+    # 3. BVH build (bvh.py:87-193) on a 3000-primitive SH3 cloud
+    a = synthetic.random_cloud(3000, seed=3, sh_degree=3)
+    lo, hi = a.aabb_arrays(s)
+    b = B.build((lo, hi))
+    np.savez_compressed(OUT / "bvh_3000.npz", lo=lo, hi=hi, node_lo=b.node_lo, node_hi=b.node_hi,
+                        node_left=b.node_left, node_right=b.node_right, node_count=b.node_count,
+                        prim_order=b.prim_order)
+
+    # 4. explicit-ray traces (kernels.py:527-540), trig hash, both depth modes
+    a = synthetic.random_cloud(400, seed=31)
+    pk = a.packed
+    bb = R.scene_bvh(a, s)
+    rr = np.random.default_rng(1234)
+    n = 600
+    origins = rr.uniform(-3, 3, size=(n, 3))
+    dirs = rr.normal(size=(n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    res = {}
+    for mode in (0, 1):
+        for ns in (1, 4):
+            ot = np.empty((n, ns))
+            oi = np.empty((n, ns), np.int64)
+            kernels.trace_batch(*R._bvh_args(bb), pk.means, pk.cov_inv6, pk.opacities, origins, dirs, 0.0, tmax,
+                                mode, s * s, True, ot, oi)
+            res[f"t_m{mode}_n{ns}"] = ot
+            res[f"id_m{mode}_n{ns}"] = oi
+    tr = np.empty(n)
+    kernels.transmittance_batch(*R._bvh_args(bb), pk.means, pk.cov_inv6, pk.opacities, origins, dirs, 0.0, tmax,
+                                0, s * s, tr)
+    np.savez_compressed(OUT / "trace_400.npz", origins=origins, dirs=dirs, transmittance=tr, **res)
+
+    # 5. full-frame render (render.py:125-174 -> kernels.py:622-673)
+    a = synthetic.random_cloud(300, seed=53, sh_degree=3)
+    cam = synthetic.front_camera()
+    st = RenderSettings(width=24, height=20, spp=6, multisample=2, seed=5, background=[0.1, 0.2, 0.3])
+    buf = R.render(a, cam, st)
+    st2 = RenderSettings(width=16, height=12, spp=3, seed=11, depth_mode="center")
+    a2 = synthetic.anisotropic_sheets(60, seed=3)
+    buf2 = R.render(a2, cam, st2)
+    np.savez_compressed(OUT / "render_small.npz", rgb=buf.rgb, opacity=buf.opacity, spp=buf.spp,
+                        rgb_center=buf2.rgb, opacity_center=buf2.opacity)
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

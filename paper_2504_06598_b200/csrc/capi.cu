@@ -1,0 +1,698 @@
+// capi.cu -- extern "C" entry points of libsrt (include/srt.h).  No
+// exception or CUDA error crosses the ABI: every failure becomes an
+// srt_status plus a thread-local message (srt_last_error).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "srt_internal.h"
+
+namespace srt {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+srt_status cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return SRT_OK;
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    cudaGetLastError();  // clear sticky-free errors
+    return e == cudaErrorMemoryAllocation ? SRT_ERR_OOM : SRT_ERR_CUDA;
+}
+
+float box_lo_f32(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = std::nextafter(f, -INFINITY);
+    return f - (std::fabs(f) * 9.5367431640625e-07f + 1e-30f);
+}
+float box_hi_f32(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = std::nextafter(f, INFINITY);
+    return f + (std::fabs(f) * 9.5367431640625e-07f + 1e-30f);
+}
+
+srt_status scratch_reserve(SrtScene *s, size_t bytes) {
+    if (bytes <= s->scratch_bytes) return SRT_OK;
+    if (s->d_scratch) cudaFree(s->d_scratch);
+    s->d_scratch = nullptr;
+    s->scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&s->d_scratch, bytes);
+    if (e != cudaSuccess) return cuda_status(e, "scratch allocation");
+    s->scratch_bytes = bytes;
+    return SRT_OK;
+}
+
+int64_t shard_tiles(int width, int height, int shard_index, int shard_count) {
+    int64_t total = (int64_t)((width + 15) / 16) * ((height + 15) / 16);
+    if (shard_count <= 1) return total;
+    if (shard_index >= total) return 0;
+    return (total - shard_index + shard_count - 1) / shard_count;
+}
+
+RenderArgs make_render_args(const SrtRenderParams *p) {
+    RenderArgs a;
+    a.width = p->width;
+    a.height = p->height;
+    a.passes = p->passes;
+    a.nslots = p->nslots;
+    a.mode = p->mode;
+    a.clip = p->clip;
+    a.s2 = (float)p->s2;
+    a.seed = p->seed;
+    a.pass0 = p->pass0;
+    for (int k = 0; k < 3; ++k) a.bg[k] = (float)p->background[k];
+    a.shard_count = p->shard_count < 1 ? 1 : p->shard_count;
+    a.shard_index = p->shard_count < 1 ? 0 : p->shard_index;
+    a.tiles_x = (p->width + 15) / 16;
+    a.local_tiles = shard_tiles(p->width, p->height, a.shard_index, a.shard_count);
+    return a;
+}
+
+CamD make_cam(const SrtCamera *c) {
+    CamD d;
+    for (int k = 0; k < 3; ++k) {
+        d.e[k] = c->position[k];
+        d.r[k] = c->right[k];
+        d.u[k] = c->up[k];
+        d.f[k] = c->forward[k];
+    }
+    d.half_w = c->half_w;
+    d.half_h = c->half_h;
+    return d;
+}
+
+srt_status check_flag(const SrtScene *s, cudaStream_t st) {
+    int flag = 0;
+    srt_status rc = cuda_status(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag read");
+    if (rc) return rc;
+    rc = cuda_status(cudaStreamSynchronize(st), "stream sync");
+    if (rc) return rc;
+    if (flag) {
+        cudaMemsetAsync(s->d_flag, 0, sizeof(int), st);
+        set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
+        return SRT_ERR_STACK_OVERFLOW;
+    }
+    return SRT_OK;
+}
+
+static srt_status validate_render(const SrtScene *s, const SrtRenderParams *p) {
+    if (!s) {
+        set_error("null scene");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (!s->has_bvh) {
+        set_error("scene has no BVH (call srt_bvh_build or srt_bvh_upload)");
+        return SRT_ERR_NO_BVH;
+    }
+    if (!p || p->width < 1 || p->height < 1 || p->passes < 1 || p->nslots < 1 || p->nslots > 256 ||
+        (p->mode != 0 && p->mode != 1) || !(p->s2 > 0.0) || p->pass0 < 0) {
+        set_error("invalid render parameters");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (p->shard_count > 1 && (p->shard_index < 0 || p->shard_index >= p->shard_count)) {
+        set_error("invalid shard index");
+        return SRT_ERR_INVALID_ARG;
+    }
+    return SRT_OK;
+}
+
+}  // namespace srt
+
+using namespace srt;
+
+extern "C" {
+
+const char *srt_last_error(void) { return g_last_error.c_str(); }
+const char *srt_version(void) { return "libsrt 0.1 (sm_100a)"; }
+
+int32_t srt_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene **out) {
+    if (!desc || !out || desc->n < 0 || desc->sh_degree < 0 || desc->sh_degree > 3 ||
+        (desc->n > 0 && (!desc->means || !desc->cov_inv6 || !desc->opacities))) {
+        set_error("invalid scene description");
+        return SRT_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    int ndev = srt_device_count();
+    if (device < 0 || device >= ndev) {
+        set_error("CUDA device " + std::to_string(device) + " not available (" + std::to_string(ndev) + " devices)");
+        return SRT_ERR_CUDA;
+    }
+    DeviceGuard g(device);
+    SrtScene *s = new SrtScene();
+    s->device = device;
+    s->n = desc->n;
+    s->sh_deg = desc->sh_degree;
+    s->sh_k = (desc->sh_degree + 1) * (desc->sh_degree + 1);
+    const int64_t n = desc->n;
+    srt_status rc = SRT_OK;
+    std::vector<float> shf;
+    rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
+    if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
+    if (!rc && n > 0) {
+        rc = cuda_status(cudaMalloc(&s->d_means, sizeof(double) * n * 3), "means alloc");
+        if (!rc) rc = cuda_status(cudaMalloc(&s->d_cov6, sizeof(double) * n * 6), "cov alloc");
+        if (!rc) rc = cuda_status(cudaMalloc(&s->d_opac, sizeof(double) * n), "opacity alloc");
+        if (!rc) rc = cuda_status(cudaMalloc(&s->d_sh, sizeof(float) * n * 3 * s->sh_k), "sh alloc");
+        if (!rc) rc = cuda_status(cudaMemcpy(s->d_means, desc->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice), "means upload");
+        if (!rc) rc = cuda_status(cudaMemcpy(s->d_cov6, desc->cov_inv6, sizeof(double) * n * 6, cudaMemcpyHostToDevice), "cov upload");
+        if (!rc) rc = cuda_status(cudaMemcpy(s->d_opac, desc->opacities, sizeof(double) * n, cudaMemcpyHostToDevice), "opacity upload");
+        if (!rc) {
+            shf.assign((size_t)n * 3 * s->sh_k, 0.0f);
+            if (desc->sh)
+                for (size_t i = 0; i < shf.size(); ++i) shf[i] = (float)desc->sh[i];
+            rc = cuda_status(cudaMemcpy(s->d_sh, shf.data(), sizeof(float) * shf.size(), cudaMemcpyHostToDevice), "sh upload");
+        }
+    }
+    if (rc) {
+        srt_scene_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return SRT_OK;
+}
+
+srt_status srt_scene_destroy(SrtScene *s) {
+    if (!s) return SRT_OK;
+    DeviceGuard g(s->device);
+    cudaFree(s->d_means);
+    cudaFree(s->d_cov6);
+    cudaFree(s->d_opac);
+    cudaFree(s->d_sh);
+    cudaFree(s->d_geom);
+    cudaFree(s->d_nodes);
+    cudaFree(s->d_flag);
+    cudaFree(s->d_scratch);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return SRT_OK;
+}
+
+srt_status srt_bvh_build(SrtScene *s, double cutoff_s) {
+    if (!s || !(cutoff_s > 0.0) || !std::isfinite(cutoff_s)) {
+        set_error("invalid scene or cutoff");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return lbvh_build(s, cutoff_s);
+}
+
+// Reference layout (bvh.py:29-47) -> Node2 tree.  A reference leaf with k
+// primitives becomes a balanced subtree over the k primitive boxes, so the
+// per-primitive box test of kernels.py:344 is kept exactly (boxes widened
+// to fp32 outward).
+srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const double *node_hi, const int64_t *node_left,
+                          const int64_t *node_right, const int64_t *node_count, const int64_t *prim_order,
+                          const double *prim_lo, const double *prim_hi) {
+    if (!s || M < 0 || (M > 0 && (!node_lo || !node_hi || !node_left || !node_right || !node_count || !prim_order ||
+                                  !prim_lo || !prim_hi))) {
+        set_error("invalid BVH arrays");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    const int64_t n = s->n;
+    std::vector<Node2> nodes;
+    struct Box {
+        float lo[3], hi[3];
+    };
+    auto prim_box = [&](int64_t slot) {
+        Box b;
+        int64_t p = prim_order[slot];
+        for (int k = 0; k < 3; ++k) {
+            b.lo[k] = box_lo_f32(prim_lo[p * 3 + k]);
+            b.hi[k] = box_hi_f32(prim_hi[p * 3 + k]);
+        }
+        return b;
+    };
+    auto node_box = [&](int64_t id) {
+        Box b;
+        for (int k = 0; k < 3; ++k) {
+            b.lo[k] = box_lo_f32(node_lo[id * 3 + k]);
+            b.hi[k] = box_hi_f32(node_hi[id * 3 + k]);
+        }
+        return b;
+    };
+    auto set_node = [&](int32_t idx, int c0, const Box &b0, int c1, const Box &b1) {
+        Node2 &nd = nodes[idx];
+        nd.xy0 = make_float4(b0.lo[0], b0.hi[0], b0.lo[1], b0.hi[1]);
+        nd.xy1 = make_float4(b1.lo[0], b1.hi[0], b1.lo[1], b1.hi[1]);
+        nd.z01 = make_float4(b0.lo[2], b0.hi[2], b1.lo[2], b1.hi[2]);
+        nd.kids = make_int4(c0, c1, 0, 0);
+    };
+    Box empty;
+    for (int k = 0; k < 3; ++k) {
+        empty.lo[k] = 3.0e38f;
+        empty.hi[k] = -3.0e38f;
+    }
+    bool bad = false;
+    int32_t max_depth = 0;
+    // subtree over leaf slots [start, start+k): returns child code; box out
+    std::function<int(int64_t, int64_t, Box &, int)> leaf_tree = [&](int64_t start, int64_t k, Box &box, int depth) -> int {
+        max_depth = std::max(max_depth, depth);
+        if (k == 1) {
+            box = prim_box(start);
+            return ~(int)start;
+        }
+        int32_t idx = (int32_t)nodes.size();
+        nodes.emplace_back();
+        Box b0, b1;
+        int64_t half = k / 2;
+        int c0 = leaf_tree(start, half, b0, depth + 1);
+        int c1 = leaf_tree(start + half, k - half, b1, depth + 1);
+        set_node(idx, c0, b0, c1, b1);
+        for (int a = 0; a < 3; ++a) {
+            box.lo[a] = std::min(b0.lo[a], b1.lo[a]);
+            box.hi[a] = std::max(b0.hi[a], b1.hi[a]);
+        }
+        return idx;
+    };
+    std::function<int(int64_t, Box &, int)> emit = [&](int64_t id, Box &box, int depth) -> int {
+        if (id < 0 || id >= M || depth > 256) {
+            bad = true;
+            return kLeafEmpty;
+        }
+        max_depth = std::max(max_depth, depth);
+        int64_t cnt = node_count[id];
+        if (cnt > 0) {
+            int64_t start = node_left[id];
+            if (start < 0 || start + cnt > n) {
+                bad = true;
+                return kLeafEmpty;
+            }
+            Box inner;
+            int code = leaf_tree(start, cnt, inner, depth);
+            box = cnt == 1 ? inner : node_box(id);
+            return code;
+        }
+        int32_t idx = (int32_t)nodes.size();
+        nodes.emplace_back();
+        Box b0, b1;
+        int c0 = emit(node_left[id], b0, depth + 1);
+        int c1 = emit(node_right[id], b1, depth + 1);
+        set_node(idx, c0, b0, c1, b1);
+        box = node_box(id);
+        return idx;
+    };
+    if (M > 0) {
+        Box rb;
+        nodes.reserve((size_t)(2 * n + 1));
+        int root = emit(0, rb, 1);
+        if (root < 0 && root != kLeafEmpty) {  // single-primitive root leaf: wrap it
+            nodes.emplace_back();
+            set_node(0, root, rb, kLeafEmpty, empty);
+        }
+    }
+    if (bad) {
+        set_error("malformed reference BVH arrays");
+        return SRT_ERR_INVALID_ARG;
+    }
+    // slot-ordered geometry from prim_order
+    if (s->d_nodes) cudaFree(s->d_nodes);
+    if (s->d_geom) cudaFree(s->d_geom);
+    s->d_nodes = nullptr;
+    s->d_geom = nullptr;
+    s->has_bvh = false;
+    srt_status rc = SRT_OK;
+    if (!nodes.empty()) {
+        rc = cuda_status(cudaMalloc(&s->d_nodes, sizeof(Node2) * nodes.size()), "node alloc");
+        if (!rc)
+            rc = cuda_status(cudaMemcpy(s->d_nodes, nodes.data(), sizeof(Node2) * nodes.size(), cudaMemcpyHostToDevice),
+                             "node upload");
+    }
+    if (!rc && n > 0) {
+        // gather the fp64 records on the host in slot order, convert on device
+        std::vector<double> pm(n * 3), pc(n * 6), po(n);
+        std::vector<Geom> geom(n);
+        std::vector<double> hm(n * 3), hc(n * 6), ho(n);
+        rc = cuda_status(cudaMemcpy(hm.data(), s->d_means, sizeof(double) * n * 3, cudaMemcpyDeviceToHost), "means");
+        if (!rc) rc = cuda_status(cudaMemcpy(hc.data(), s->d_cov6, sizeof(double) * n * 6, cudaMemcpyDeviceToHost), "cov");
+        if (!rc) rc = cuda_status(cudaMemcpy(ho.data(), s->d_opac, sizeof(double) * n, cudaMemcpyDeviceToHost), "opac");
+        if (!rc) {
+            for (int64_t j = 0; j < n; ++j) {
+                int64_t p = prim_order[j];
+                if (p < 0 || p >= n) {
+                    set_error("prim_order out of range");
+                    return SRT_ERR_INVALID_ARG;
+                }
+                Geom &gg = geom[j];
+                gg.m = make_float4((float)hm[p * 3], (float)hm[p * 3 + 1], (float)hm[p * 3 + 2], (float)ho[p]);
+                gg.a = make_float4((float)hc[p * 6], (float)hc[p * 6 + 1], (float)hc[p * 6 + 2], (float)hc[p * 6 + 3]);
+                int pi = (int)p;
+                float pf;
+                std::memcpy(&pf, &pi, sizeof(pf));
+                gg.b = make_float4((float)hc[p * 6 + 4], (float)hc[p * 6 + 5], pf, 0.f);
+            }
+            rc = cuda_status(cudaMalloc(&s->d_geom, sizeof(Geom) * n), "geom alloc");
+            if (!rc) rc = cuda_status(cudaMemcpy(s->d_geom, geom.data(), sizeof(Geom) * n, cudaMemcpyHostToDevice), "geom upload");
+        }
+    }
+    if (rc) return rc;
+    s->num_nodes = (int32_t)nodes.size();
+    s->depth = max_depth + 1;
+    s->has_bvh = true;
+    return SRT_OK;
+}
+
+srt_status srt_bvh_info(const SrtScene *s, int64_t *num_nodes, int32_t *depth, int64_t *num_prims,
+                        int64_t *device_bytes) {
+    if (!s) {
+        set_error("null scene");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (num_nodes) *num_nodes = s->num_nodes;
+    if (depth) *depth = s->depth;
+    if (num_prims) *num_prims = s->n;
+    if (device_bytes)
+        *device_bytes = (int64_t)sizeof(Node2) * s->num_nodes + (int64_t)sizeof(Geom) * s->n +
+                        (int64_t)sizeof(float) * s->n * 3 * s->sh_k;
+    return SRT_OK;
+}
+
+// Download in the reference layout: internal nodes of the device tree become
+// reference inner nodes; each leaf child becomes a one-primitive leaf node.
+srt_status srt_bvh_download(const SrtScene *s, float *node_lo, float *node_hi, int64_t *node_left,
+                            int64_t *node_right, int64_t *node_count, int64_t *prim_order, float *prim_lo,
+                            float *prim_hi) {
+    if (!s || !s->has_bvh) {
+        set_error("scene has no BVH");
+        return SRT_ERR_NO_BVH;
+    }
+    DeviceGuard g(s->device);
+    const int64_t n = s->n;
+    std::vector<Node2> nodes(s->num_nodes);
+    std::vector<Geom> geom(n);
+    srt_status rc = SRT_OK;
+    if (s->num_nodes)
+        rc = cuda_status(cudaMemcpy(nodes.data(), s->d_nodes, sizeof(Node2) * nodes.size(), cudaMemcpyDeviceToHost), "nodes");
+    if (!rc && n)
+        rc = cuda_status(cudaMemcpy(geom.data(), s->d_geom, sizeof(Geom) * n, cudaMemcpyDeviceToHost), "geom");
+    if (rc) return rc;
+    for (int64_t j = 0; j < n; ++j) {
+        int p;
+        std::memcpy(&p, &geom[j].b.z, sizeof(int));
+        prim_order[j] = p;
+    }
+    // reference node ids: device inner node i -> i; leaf slot j -> num_nodes + j
+    const int64_t Mi = s->num_nodes;
+    auto put = [&](int64_t id, const float lo[3], const float hi[3]) {
+        for (int k = 0; k < 3; ++k) {
+            node_lo[id * 3 + k] = lo[k];
+            node_hi[id * 3 + k] = hi[k];
+        }
+    };
+    std::vector<char> seen(n, 0);
+    for (int64_t i = 0; i < Mi; ++i) {
+        const Node2 &nd = nodes[i];
+        float lo0[3] = {nd.xy0.x, nd.xy0.z, nd.z01.x}, hi0[3] = {nd.xy0.y, nd.xy0.w, nd.z01.y};
+        float lo1[3] = {nd.xy1.x, nd.xy1.z, nd.z01.z}, hi1[3] = {nd.xy1.y, nd.xy1.w, nd.z01.w};
+        int kids[2] = {nd.kids.x, nd.kids.y};
+        const float *los[2] = {lo0, lo1}, *his[2] = {hi0, hi1};
+        int64_t ref[2];
+        for (int c = 0; c < 2; ++c) {
+            if (kids[c] == kLeafEmpty) {
+                ref[c] = -1;
+            } else if (kids[c] < 0) {
+                int64_t slot = ~kids[c];
+                int64_t id = Mi + slot;
+                ref[c] = id;
+                put(id, los[c], his[c]);
+                node_left[id] = slot;
+                node_right[id] = -1;
+                node_count[id] = 1;
+                seen[slot] = 1;
+                int p = (int)prim_order[slot];
+                for (int k = 0; k < 3; ++k) {
+                    prim_lo[(int64_t)p * 3 + k] = los[c][k];
+                    prim_hi[(int64_t)p * 3 + k] = his[c][k];
+                }
+            } else {
+                ref[c] = kids[c];
+                put(kids[c], los[c], his[c]);
+            }
+        }
+        node_left[i] = ref[0];
+        node_right[i] = ref[1];
+        node_count[i] = 0;
+    }
+    if (Mi > 0) {
+        // root box = union of its children
+        const Node2 &r = nodes[0];
+        float lo[3] = {std::min(r.xy0.x, r.xy1.x), std::min(r.xy0.z, r.xy1.z), std::min(r.z01.x, r.z01.z)};
+        float hi[3] = {std::max(r.xy0.y, r.xy1.y), std::max(r.xy0.w, r.xy1.w), std::max(r.z01.y, r.z01.w)};
+        if (r.kids.y == kLeafEmpty) {
+            float lo0[3] = {r.xy0.x, r.xy0.z, r.z01.x}, hi0[3] = {r.xy0.y, r.xy0.w, r.z01.y};
+            put(0, lo0, hi0);
+        } else {
+            put(0, lo, hi);
+        }
+    }
+    for (int64_t j = 0; j < n; ++j)
+        if (!seen[j]) {
+            set_error("device BVH does not reference every primitive");
+            return SRT_ERR_CUDA;
+        }
+    return SRT_OK;
+}
+
+// ---- explicit rays --------------------------------------------------------
+
+static srt_status validate_trace(const SrtScene *s, const SrtTraceParams *p, int64_t R, int32_t nslots) {
+    if (!s || !p || R < 0 || nslots < 1 || nslots > 256 || (p->mode != 0 && p->mode != 1) || !(p->s2 > 0.0) ||
+        (p->rng != SRT_RNG_COUNTER && p->rng != SRT_RNG_TABLE) ||
+        (p->rng == SRT_RNG_TABLE && (!p->table || p->table_slots < nslots))) {
+        set_error("invalid trace parameters");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (!s->has_bvh) {
+        set_error("scene has no BVH (call srt_bvh_build or srt_bvh_upload)");
+        return SRT_ERR_NO_BVH;
+    }
+    return SRT_OK;
+}
+
+srt_status srt_trace_rays_device(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R,
+                                 int32_t nslots, float *d_t, int32_t *d_id, void *stream) {
+    srt_status rc = validate_trace(s, p, R, nslots);
+    if (rc) return rc;
+    if (p->rng == SRT_RNG_TABLE) {
+        set_error("table RNG needs the host entry point (srt_trace_rays)");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return launch_trace_rays(s, p, d_rays, R, nslots, nullptr, d_t, d_id, (cudaStream_t)stream);
+}
+
+srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const double *origins, const double *dirs,
+                          int64_t R, int32_t nslots, double *out_t, int64_t *out_id) {
+    srt_status rc = validate_trace(sc, p, R, nslots);
+    if (rc) return rc;
+    if (R == 0) return SRT_OK;
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    size_t ray_bytes = sizeof(double) * R * 6;
+    size_t out_bytes = (sizeof(float) + sizeof(int32_t)) * R * nslots;
+    size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
+    rc = scratch_reserve(s, ray_bytes + out_bytes + table_bytes + 256);
+    if (rc) return rc;
+    char *base = (char *)s->d_scratch;
+    double *d_rays = (double *)base;
+    float *d_t = (float *)(base + ray_bytes);
+    int32_t *d_id = (int32_t *)(base + ray_bytes + sizeof(float) * R * nslots);
+    double *d_table = table_bytes ? (double *)(base + ((ray_bytes + out_bytes + 15) & ~(size_t)15)) : nullptr;
+    std::vector<double> packed((size_t)R * 6);
+    for (int64_t i = 0; i < R; ++i) {
+        for (int k = 0; k < 3; ++k) {
+            packed[i * 6 + k] = origins[i * 3 + k];
+            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
+        }
+    }
+    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    if (!rc && d_table)
+        rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
+    if (!rc) rc = launch_trace_rays(s, p, d_rays, R, nslots, d_table, d_t, d_id, st);
+    std::vector<float> ht((size_t)R * nslots);
+    std::vector<int32_t> hid((size_t)R * nslots);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(ht.data(), d_t, sizeof(float) * ht.size(), cudaMemcpyDeviceToHost, st), "t download");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(hid.data(), d_id, sizeof(int32_t) * hid.size(), cudaMemcpyDeviceToHost, st), "id download");
+    if (!rc) rc = check_flag(s, st);
+    if (rc) return rc;
+    for (size_t i = 0; i < ht.size(); ++i) {
+        out_t[i] = hid[i] >= 0 ? (double)ht[i] : INFINITY;
+        out_id[i] = hid[i];
+    }
+    return SRT_OK;
+}
+
+srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, const double *dirs, int64_t R,
+                                  double t_min, double t_max, int32_t mode, double s2, double *out) {
+    if (!sc || R < 0 || (mode != 0 && mode != 1) || !(s2 > 0.0)) {
+        set_error("invalid transmittance parameters");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (!sc->has_bvh) {
+        set_error("scene has no BVH");
+        return SRT_ERR_NO_BVH;
+    }
+    if (R == 0) return SRT_OK;
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    size_t ray_bytes = sizeof(double) * R * 6;
+    srt_status rc = scratch_reserve(s, ray_bytes + sizeof(double) * R);
+    if (rc) return rc;
+    double *d_rays = (double *)s->d_scratch;
+    double *d_out = d_rays + R * 6;
+    std::vector<double> packed((size_t)R * 6);
+    for (int64_t i = 0; i < R; ++i)
+        for (int k = 0; k < 3; ++k) {
+            packed[i * 6 + k] = origins[i * 3 + k];
+            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
+        }
+    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    if (!rc) rc = launch_transmittance(s, d_rays, R, t_min, t_max, mode, s2, d_out, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out, d_out, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "download");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+// ---- frames ----------------------------------------------------------------
+
+int64_t srt_shard_tiles(int32_t width, int32_t height, int32_t shard_index, int32_t shard_count) {
+    return shard_tiles(width, height, shard_index, shard_count);
+}
+
+srt_status srt_trace_pass_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t pass,
+                                 int32_t *d_hits, void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_hits) {
+        set_error("null camera or hit buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return launch_trace_pass(s, make_cam(camera), make_render_args(p), pass, d_hits, (cudaStream_t)stream);
+}
+
+srt_status srt_shade_pass_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t pass,
+                                 const int32_t *d_hits, float *d_accum, int32_t first, int32_t last, float *d_out,
+                                 void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_hits || !d_accum || (last && !d_out)) {
+        set_error("null camera or buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return launch_shade_pass(s, make_cam(camera), make_render_args(p), pass, d_hits, (float4 *)d_accum, first != 0,
+                             last != 0, (float4 *)d_out, (cudaStream_t)stream);
+}
+
+srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t *d_hits,
+                             float *d_accum, float *d_out, void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_hits || !d_accum || !d_out) {
+        set_error("null camera or buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    CamD cam = make_cam(camera);
+    RenderArgs a = make_render_args(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int f = 0; f < p->passes && !rc; ++f) {
+        int pass = p->pass0 + f;
+        rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
+        if (!rc)
+            rc = launch_shade_pass(s, cam, a, pass, d_hits, (float4 *)d_accum, f == 0, f == p->passes - 1,
+                                   (float4 *)d_out, st);
+    }
+    return rc;
+}
+
+srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
+                      double *out_op, int64_t *out_ids) {
+    srt_status rc = validate_render(sc, p);
+    if (rc) return rc;
+    if (!camera || !out_rgb || !out_op) {
+        set_error("null camera or output");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (p->shard_count > 1) {
+        set_error("srt_render renders whole frames; use the *_device entry points for shards");
+        return SRT_ERR_INVALID_ARG;
+    }
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    RenderArgs a = make_render_args(p);
+    CamD cam = make_cam(camera);
+    const int64_t npix = (int64_t)p->width * p->height;
+    const int64_t cpix = a.local_tiles * 256;  // tile-compact pixel count
+    size_t hits_bytes = sizeof(int32_t) * cpix * p->nslots;
+    size_t acc_bytes = sizeof(float4) * cpix;
+    size_t out_bytes = sizeof(float4) * npix;
+    size_t f64_bytes = sizeof(double) * npix * 4;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    rc = scratch_reserve(s, al(hits_bytes) + al(acc_bytes) + al(out_bytes) + al(f64_bytes));
+    if (rc) return rc;
+    char *base = (char *)s->d_scratch;
+    int32_t *d_hits = (int32_t *)base;
+    float4 *d_acc = (float4 *)(base + al(hits_bytes));
+    float4 *d_out = (float4 *)(base + al(hits_bytes) + al(acc_bytes));
+    double *d_rgb = (double *)(base + al(hits_bytes) + al(acc_bytes) + al(out_bytes));
+    double *d_op = d_rgb + npix * 3;
+    for (int f = 0; f < p->passes && !rc; ++f) {
+        int pass = p->pass0 + f;
+        rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
+        if (!rc && out_ids && f == 0) {
+            // slot ids of the first pass, un-tiled on the host
+            std::vector<int32_t> hh((size_t)cpix * p->nslots);
+            rc = cuda_status(cudaMemcpyAsync(hh.data(), d_hits, hits_bytes, cudaMemcpyDeviceToHost, st), "ids");
+            if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "ids");
+            if (!rc) {
+                int tiles_x = a.tiles_x;
+                for (int64_t lt = 0; lt < a.local_tiles; ++lt)
+                    for (int tid = 0; tid < 256; ++tid) {
+                        int tx = (int)(lt % tiles_x), ty = (int)(lt / tiles_x);
+                        int w = tid >> 5, lane = tid & 31;
+                        int px = tx * 16 + (w & 1) * 8 + (lane & 7);
+                        int py = ty * 16 + (w >> 1) * 4 + (lane >> 3);
+                        if (px >= p->width || py >= p->height) continue;
+                        for (int k = 0; k < p->nslots; ++k)
+                            out_ids[((int64_t)py * p->width + px) * p->nslots + k] = hh[(lt * 256 + tid) * p->nslots + k];
+                    }
+            }
+        }
+        if (!rc) rc = launch_shade_pass(s, cam, a, pass, d_hits, d_acc, f == 0, f == p->passes - 1, d_out, st);
+    }
+    if (!rc) rc = launch_resolve_f64(a, d_out, d_rgb, d_op, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb download");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "opacity download");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+srt_status srt_unpack_tiles_device(const float *d_gathered, int32_t width, int32_t height, int32_t shard_count,
+                                   int64_t max_tiles, float *d_frame, void *stream) {
+    if (!d_gathered || !d_frame || width < 1 || height < 1 || shard_count < 1 || max_tiles < 0) {
+        set_error("invalid unpack arguments");
+        return SRT_ERR_INVALID_ARG;
+    }
+    return launch_unpack((const float4 *)d_gathered, width, height, shard_count, max_tiles, (float4 *)d_frame,
+                         (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,364 @@
+// lbvh.cu -- GPU LBVH build (north-star subsystem 1), replacing the
+// reference's single-threaded Python binned-SAH build (bvh.py:87-193).
+//
+//   1. k_prim_boxes   per-primitive AABB of the cutoff ellipsoid
+//                     {x : (x-mu)^T A (x-mu) <= s^2}: half extent_i =
+//                     s*sqrt(Sigma_ii), Sigma = A^-1 (fp64), rounded outward
+//                     to fp32 and inflated (conservative slab tests).  Any
+//                     superset of the ellipsoid is correct: a valid candidate
+//                     peaks inside the ellipsoid (kernels.py:187), hence
+//                     inside its box.  Also the centroid bounds (atomics).
+//   2. k_morton       63-bit Morton code of the box centroid (21 bits/axis).
+//   3. CUB radix sort of (code, prim) pairs.
+//   4. k_karras       Karras (HPG 2012) binary radix tree over the sorted
+//                     codes; duplicate codes are disambiguated by index.
+//   5. k_refit        bottom-up: the second thread to reach a node writes
+//                     the node's Node2 (both children's boxes) and its union.
+//   6. k_geom         primitive records permuted into leaf ("slot") order.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "srt_internal.h"
+
+namespace srt {
+
+__device__ __forceinline__ int ordered_int(float f) {
+    int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float from_ordered(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+__device__ __forceinline__ float lo32(double x) {
+    float f = __double2float_rd(x);
+    return f - (fabsf(f) * 9.5367431640625e-07f + 1e-30f);  // 2^-20 relative inflation
+}
+__device__ __forceinline__ float hi32(double x) {
+    float f = __double2float_ru(x);
+    return f + (fabsf(f) * 9.5367431640625e-07f + 1e-30f);
+}
+
+__global__ void k_prim_boxes(int64_t n, const double *__restrict__ means, const double *__restrict__ cov6, double s,
+                             float *lo, float *hi, int *cbounds) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    float cmin[3] = {INFINITY, INFINITY, INFINITY}, cmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if (i < n) {
+        const double *c = cov6 + i * 6;
+        double a00 = c[0], a01 = c[1], a02 = c[2], a11 = c[3], a12 = c[4], a22 = c[5];
+        // Sigma = adj(A) / det(A); only the diagonal is needed
+        double c00 = a11 * a22 - a12 * a12;
+        double c11 = a00 * a22 - a02 * a02;
+        double c22 = a00 * a11 - a01 * a01;
+        double det = a00 * c00 - a01 * (a01 * a22 - a12 * a02) + a02 * (a01 * a12 - a11 * a02);
+        double sd[3] = {c00 / det, c11 / det, c22 / det};
+        for (int k = 0; k < 3; ++k) {
+            double m = means[i * 3 + k];
+            double h = s * sqrt(sd[k]);
+            float l, u;
+            if (!(h >= 0.0) || !isfinite(h)) {
+                // degenerate: the box must not reject anything; the candidate
+                // test (dAd <= 0 etc.) decides
+                l = -3.0e38f;
+                u = 3.0e38f;
+            } else {
+                l = lo32(m - h);
+                u = hi32(m + h);
+            }
+            lo[i * 3 + k] = l;
+            hi[i * 3 + k] = u;
+            cmin[k] = (float)m;  // Morton codes use the mean (the box centre)
+            cmax[k] = (float)m;
+        }
+    }
+    // block reduce via warp shuffles then one atomic per warp
+    for (int k = 0; k < 3; ++k) {
+        float a = cmin[k], b = cmax[k];
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if ((threadIdx.x & 31) == 0 && a <= b) {
+            atomicMin(cbounds + k, ordered_int(a));
+            atomicMax(cbounds + 3 + k, ordered_int(b));
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t spread21(uint64_t x) {
+    x &= 0x1fffffull;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void k_morton(int64_t n, const double *__restrict__ means, const int *cbounds, uint64_t *keys,
+                         uint32_t *vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t code = 0;
+    for (int k = 0; k < 3; ++k) {
+        float lo = from_ordered(cbounds[k]), hi = from_ordered(cbounds[3 + k]);
+        float ext = hi - lo;
+        float c = (float)means[i * 3 + k];
+        float u = ext > 0.f ? (c - lo) / ext : 0.5f;
+        u = fminf(fmaxf(u, 0.f), 1.f);
+        uint64_t q = (uint64_t)fminf(u * 2097152.0f, 2097151.0f);
+        code |= spread21(q) << (2 - k);
+    }
+    keys[i] = code;
+    vals[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ int delta(const uint64_t *keys, int64_t n, int64_t i, int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    uint64_t a = keys[i], b = keys[j];
+    if (a == b) return 64 + __clzll((unsigned long long)(i ^ j));
+    return __clzll((unsigned long long)(a ^ b));
+}
+
+// internal node i in [0, n-2]; children: >=0 internal, <0 leaf ~slot
+__global__ void k_karras(int64_t n, const uint64_t *__restrict__ keys, int2 *children, int *parent_int,
+                         int *parent_leaf) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+    int dmin = delta(keys, n, i, i - d);
+    int64_t lmax = 2;
+    while (delta(keys, n, i, i + lmax * d) > dmin) lmax *= 2;
+    int64_t l = 0;
+    for (int64_t t = lmax / 2; t >= 1; t /= 2)
+        if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+    int64_t j = i + l * d;
+    int dnode = delta(keys, n, i, j);
+    int64_t s = 0;
+    int64_t t = l;
+    do {
+        t = (t + 1) / 2;
+        if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    int64_t gamma = i + s * d + (d < 0 ? -1 : 0);
+    int64_t first = i < j ? i : j, last = i < j ? j : i;
+    int left, right;
+    if (first == gamma) {
+        left = ~(int)gamma;
+        parent_leaf[gamma] = (int)i;
+    } else {
+        left = (int)gamma;
+        parent_int[gamma] = (int)i;
+    }
+    if (last == gamma + 1) {
+        right = ~(int)(gamma + 1);
+        parent_leaf[gamma + 1] = (int)i;
+    } else {
+        right = (int)(gamma + 1);
+        parent_int[gamma + 1] = (int)i;
+    }
+    children[i] = make_int2(left, right);
+}
+
+struct Box6 {
+    float lo[3], hi[3];
+};
+
+__device__ __forceinline__ Box6 load_child_box(int code, const float *plo, const float *phi,
+                                               const uint32_t *slot_prim, const float *ibox) {
+    Box6 b;
+    if (code < 0) {
+        int64_t p = slot_prim[~code];
+        for (int k = 0; k < 3; ++k) {
+            b.lo[k] = plo[p * 3 + k];
+            b.hi[k] = phi[p * 3 + k];
+        }
+    } else {
+        // written by another thread of this kernel: bypass L1
+        for (int k = 0; k < 3; ++k) {
+            b.lo[k] = __ldcg(ibox + (int64_t)code * 6 + k);
+            b.hi[k] = __ldcg(ibox + (int64_t)code * 6 + 3 + k);
+        }
+    }
+    return b;
+}
+
+__global__ void k_refit(int64_t n, const int2 *__restrict__ children, const int *__restrict__ parent_int,
+                        const int *__restrict__ parent_leaf, const float *__restrict__ plo,
+                        const float *__restrict__ phi, const uint32_t *__restrict__ slot_prim, float *ibox,
+                        int *flags, Node2 *nodes) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int node = parent_leaf[j];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(flags + node, 1) == 0) return;  // sibling subtree not finished yet
+        __threadfence();
+        int2 ch = children[node];
+        Box6 a = load_child_box(ch.x, plo, phi, slot_prim, ibox);
+        Box6 b = load_child_box(ch.y, plo, phi, slot_prim, ibox);
+        Node2 nd;
+        nd.xy0 = make_float4(a.lo[0], a.hi[0], a.lo[1], a.hi[1]);
+        nd.xy1 = make_float4(b.lo[0], b.hi[0], b.lo[1], b.hi[1]);
+        nd.z01 = make_float4(a.lo[2], a.hi[2], b.lo[2], b.hi[2]);
+        nd.kids = make_int4(ch.x, ch.y, 0, 0);
+        nodes[node] = nd;
+        for (int k = 0; k < 3; ++k) {
+            __stcg(ibox + (int64_t)node * 6 + k, fminf(a.lo[k], b.lo[k]));
+            __stcg(ibox + (int64_t)node * 6 + 3 + k, fmaxf(a.hi[k], b.hi[k]));
+        }
+        node = parent_int[node];  // root's parent is -1
+    }
+}
+
+// tree depth in nodes (leaf level included): max over leaves of the path length
+__global__ void k_depth(int64_t n, const int *__restrict__ parent_int, const int *__restrict__ parent_leaf,
+                        int *depth_out) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int d = 1;
+    for (int node = parent_leaf[j]; node >= 0; node = parent_int[node]) ++d;
+    atomicMax(depth_out, d);
+}
+
+// geometry records in slot order; fp64 -> fp32
+__global__ void k_geom(int64_t n, const uint32_t *__restrict__ slot_prim, const double *__restrict__ means,
+                       const double *__restrict__ cov6, const double *__restrict__ opac, Geom *geom) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int64_t p = slot_prim[j];
+    Geom g;
+    g.m = make_float4((float)means[p * 3], (float)means[p * 3 + 1], (float)means[p * 3 + 2], (float)opac[p]);
+    const double *c = cov6 + p * 6;
+    g.a = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
+    g.b = make_float4((float)c[4], (float)c[5], __int_as_float((int)p), 0.f);
+    geom[j] = g;
+}
+
+// single-primitive tree: one node, child0 = leaf 0, child1 = empty
+__global__ void k_single(const float *plo, const float *phi, Node2 *nodes) {
+    Node2 nd;
+    nd.xy0 = make_float4(plo[0], phi[0], plo[1], phi[1]);
+    nd.xy1 = make_float4(3.0e38f, -3.0e38f, 3.0e38f, -3.0e38f);
+    nd.z01 = make_float4(plo[2], phi[2], 3.0e38f, -3.0e38f);
+    nd.kids = make_int4(~0, kLeafEmpty, 0, 0);
+    nodes[0] = nd;
+}
+
+template <typename T>
+static srt_status dalloc(T **p, size_t count, const char *what) {
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (count ? count : 1));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc failed for ") + what + ": " + cudaGetErrorString(e));
+        return e == cudaErrorMemoryAllocation ? SRT_ERR_OOM : SRT_ERR_CUDA;
+    }
+    return SRT_OK;
+}
+
+srt_status lbvh_build(SrtScene *s, double cutoff_s) {
+    const int64_t n = s->n;
+    cudaStream_t st = s->stream;
+    if (s->d_nodes) cudaFree(s->d_nodes);
+    if (s->d_geom) cudaFree(s->d_geom);
+    s->d_nodes = nullptr;
+    s->d_geom = nullptr;
+    s->has_bvh = false;
+    s->num_nodes = 0;
+    s->depth = 0;
+    if (n == 0) {
+        s->has_bvh = true;
+        return SRT_OK;
+    }
+    if (n > (int64_t)INT32_MAX / 2) {
+        set_error("too many primitives for 32-bit node indices");
+        return SRT_ERR_INVALID_ARG;
+    }
+    float *plo = nullptr, *phi = nullptr, *ibox = nullptr;
+    int *cb = nullptr, *parent_int = nullptr, *parent_leaf = nullptr, *flags = nullptr, *ddepth = nullptr;
+    uint64_t *keys = nullptr, *keys2 = nullptr;
+    uint32_t *vals = nullptr, *vals2 = nullptr;
+    int2 *children = nullptr;
+    void *temp = nullptr;
+    size_t temp_bytes = 0;
+    srt_status rc = SRT_OK;
+    const unsigned B = 256;
+    const unsigned G = (unsigned)((n + B - 1) / B);
+    int cb_init[6];
+    int h_depth = 0;
+#define SRT_TRY(x)          \
+    do {                    \
+        rc = (x);           \
+        if (rc) goto done;  \
+    } while (0)
+    SRT_TRY(dalloc(&plo, n * 3, "prim lo"));
+    SRT_TRY(dalloc(&phi, n * 3, "prim hi"));
+    SRT_TRY(dalloc(&cb, 6, "bounds"));
+    SRT_TRY(dalloc(&keys, n, "keys"));
+    SRT_TRY(dalloc(&keys2, n, "keys"));
+    SRT_TRY(dalloc(&vals, n, "vals"));
+    SRT_TRY(dalloc(&vals2, n, "vals"));
+    SRT_TRY(dalloc(&s->d_geom, n, "geom"));
+    SRT_TRY(dalloc(&ddepth, 1, "depth"));
+    for (int k = 0; k < 3; ++k) {
+        cb_init[k] = 0x7FFFFFFF;       // ordered +max
+        cb_init[3 + k] = (int)0x80000000;  // ordered -max
+    }
+    SRT_TRY(cuda_status(cudaMemcpyAsync(cb, cb_init, sizeof(cb_init), cudaMemcpyHostToDevice, st), "bounds init"));
+    k_prim_boxes<<<G, B, 0, st>>>(n, s->d_means, s->d_cov6, cutoff_s, plo, phi, cb);
+    SRT_TRY(cuda_status(cudaGetLastError(), "k_prim_boxes"));
+    k_morton<<<G, B, 0, st>>>(n, s->d_means, cb, keys, vals);
+    SRT_TRY(cuda_status(cudaGetLastError(), "k_morton"));
+    SRT_TRY(cuda_status(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys, keys2, vals, vals2, (int)n, 0, 63, st),
+                        "radix sort sizing"));
+    SRT_TRY(dalloc((char **)&temp, temp_bytes, "sort temp"));
+    SRT_TRY(cuda_status(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys2, vals, vals2, (int)n, 0, 63, st),
+                        "radix sort"));
+    k_geom<<<G, B, 0, st>>>(n, vals2, s->d_means, s->d_cov6, s->d_opac, s->d_geom);
+    SRT_TRY(cuda_status(cudaGetLastError(), "k_geom"));
+    if (n == 1) {
+        SRT_TRY(dalloc(&s->d_nodes, 1, "nodes"));
+        k_single<<<1, 1, 0, st>>>(plo, phi, s->d_nodes);
+        SRT_TRY(cuda_status(cudaGetLastError(), "k_single"));
+        s->num_nodes = 1;
+        s->depth = 2;
+    } else {
+        const int64_t m = n - 1;
+        SRT_TRY(dalloc(&s->d_nodes, m, "nodes"));
+        SRT_TRY(dalloc(&children, m, "children"));
+        SRT_TRY(dalloc(&parent_int, m, "parents"));
+        SRT_TRY(dalloc(&parent_leaf, n, "parents"));
+        SRT_TRY(dalloc(&flags, m, "flags"));
+        SRT_TRY(dalloc(&ibox, m * 6, "internal boxes"));
+        SRT_TRY(cuda_status(cudaMemsetAsync(flags, 0, sizeof(int) * m, st), "flags"));
+        SRT_TRY(cuda_status(cudaMemsetAsync(ddepth, 0, sizeof(int), st), "depth"));
+        SRT_TRY(cuda_status(cudaMemsetAsync(parent_int, 0xFF, sizeof(int) * m, st), "parents"));
+        k_karras<<<(unsigned)((m + B - 1) / B), B, 0, st>>>(n, keys2, children, parent_int, parent_leaf);
+        SRT_TRY(cuda_status(cudaGetLastError(), "k_karras"));
+        k_refit<<<G, B, 0, st>>>(n, children, parent_int, parent_leaf, plo, phi, vals2, ibox, flags, s->d_nodes);
+        SRT_TRY(cuda_status(cudaGetLastError(), "k_refit"));
+        k_depth<<<G, B, 0, st>>>(n, parent_int, parent_leaf, ddepth);
+        SRT_TRY(cuda_status(cudaGetLastError(), "k_depth"));
+        SRT_TRY(cuda_status(cudaMemcpyAsync(&h_depth, ddepth, sizeof(int), cudaMemcpyDeviceToHost, st), "depth"));
+        SRT_TRY(cuda_status(cudaStreamSynchronize(st), "lbvh build"));
+        s->num_nodes = (int32_t)m;
+        s->depth = h_depth;
+    }
+    SRT_TRY(cuda_status(cudaStreamSynchronize(st), "lbvh build"));
+    s->has_bvh = true;
+done:
+#undef SRT_TRY
+    cudaFree(plo);
+    cudaFree(phi);
+    cudaFree(cb);
+    cudaFree(keys);
+    cudaFree(keys2);
+    cudaFree(vals);
+    cudaFree(vals2);
+    cudaFree(children);
+    cudaFree(parent_int);
+    cudaFree(parent_leaf);
+    cudaFree(flags);
+    cudaFree(ibox);
+    cudaFree(ddepth);
+    cudaFree(temp);
+    return rc;
+}
+
+}  // namespace srt

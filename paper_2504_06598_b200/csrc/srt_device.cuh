@@ -1,0 +1,262 @@
+// srt_device.cuh -- device-side records and per-primitive math of libsrt.
+//
+// Layout in HBM:
+//   Node2  64 B  binary BVH node holding BOTH children's fp32 boxes (one
+//                visit = four 128-bit loads).  Leaves have exactly one
+//                primitive, so a leaf child's box IS the primitive box
+//                (the reference's separate prim-box test, kernels.py:344,
+//                is folded into the parent visit).
+//   Geom   48 B  per primitive in leaf ("slot") order: mean + opacity,
+//                six inverse-covariance entries, original primitive id.
+//   SH     K*12 B per primitive in ORIGINAL id order, channel major, fp32.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace srt {
+
+constexpr int kLeafEmpty = INT32_MIN;  // child slot with no content
+constexpr int kStackSize = 128;        // kernels.py:26
+
+struct __align__(16) Node2 {
+    float4 xy0;  // child0 lo.x hi.x lo.y hi.y
+    float4 xy1;  // child1 lo.x hi.x lo.y hi.y
+    float4 z01;  // child0 lo.z hi.z, child1 lo.z hi.z
+    int4 kids;   // child0, child1 (>=0 inner node, <0 leaf ~slot, kLeafEmpty), pad
+};
+
+struct __align__(16) Geom {
+    float4 m;  // mean.xyz, opacity
+    float4 a;  // a00 a01 a02 a11
+    float4 b;  // a12 a22, prim id (int bits), pad
+};
+
+struct SceneView {
+    const Node2 *nodes;
+    const Geom *geom;
+    const float *sh;  // (n, 3, K) fp32, original id order
+    int32_t num_nodes;
+    int32_t root;      // 0, or a leaf code (~slot) when the tree is a single leaf
+    int32_t sh_k;      // (deg + 1)^2
+    int32_t sh_deg;
+    int64_t n;
+};
+
+// ---------------------------------------------------------------------------
+// counter RNG -- bitwise identical to oracle/srt_oracle.c
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ uint32_t frame_key(uint32_t seed) { return mix32(seed ^ 0x9E3779B9u); }
+__device__ __forceinline__ uint32_t walk_key(uint32_t fkey, uint32_t ray_id, uint32_t sample) {
+    return mix32(mix32(fkey ^ ray_id) ^ sample);
+}
+// u in [0,1) with 24 bits; returned as the exact integer 0..2^24-1 scaled.
+__device__ __forceinline__ float counter_u(uint32_t key, uint32_t prim) {
+    uint32_t h = mix32(mix32(key ^ prim) ^ 0x68E31DA4u);
+    return (float)(h >> 8) * (1.0f / 16777216.0f);
+}
+
+// ---------------------------------------------------------------------------
+// Sobol pixel jitter (kernels.py:64-116), integer exact.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t wang32(uint32_t x) {
+    x = (x ^ 61u) ^ (x >> 16);
+    x = x * 9u;
+    x = x ^ (x >> 4);
+    x = x * 0x27D4EB2Du;
+    x = x ^ (x >> 15);
+    return x;
+}
+__device__ __forceinline__ uint32_t sobol_dim1(uint32_t index) {
+    // direction numbers of x^2+x+1 generated on the fly (kernels.py:74-84)
+    uint32_t y = 0, m = 1;
+    for (int k = 0; index != 0; ++k, index >>= 1) {
+        if (index & 1u) y ^= m << (31 - k);
+        m = (m ^ (m << 1)) & (uint32_t)((2ull << (k + 1)) - 1ull);
+    }
+    return y;
+}
+// Returns the jitter (jx, jy) as exact doubles (32-bit fixed point).
+__device__ __forceinline__ void pixel_jitter(uint32_t px, uint32_t py, uint32_t frame, uint32_t seed,
+                                             double &jx, double &jy) {
+    uint32_t base = wang32((px * 0x9E3779B1u) ^ (py * 0x85EBCA77u) ^ (seed * 0xC2B2AE3Du));
+    uint32_t sx = wang32(base ^ 0x68E31DA4u);
+    uint32_t sy = wang32(base ^ 0xB5297A4Du);
+    uint32_t bx = __brev(frame);
+    uint32_t by = sobol_dim1(frame);
+    jx = (double)(bx ^ sx) * (1.0 / 4294967296.0);
+    jy = (double)(by ^ sy) * (1.0 / 4294967296.0);
+}
+
+// Camera ray (kernels.py:613-618, 646-647) in fp64 with explicit IEEE
+// rounding at every step (no FMA contraction), so the direction is bitwise
+// equal to the oracle's.
+struct CamD {
+    double e[3], r[3], u[3], f[3];
+    double half_w, half_h;
+};
+__device__ __forceinline__ void camera_ray(const CamD &c, uint32_t px, uint32_t py, uint32_t frame,
+                                           uint32_t seed, int width, int height, double &dx, double &dy,
+                                           double &dz) {
+    double jx, jy;
+    pixel_jitter(px, py, frame, seed, jx, jy);
+    double u = __dsub_rn(__ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)px, jx)), (double)width), 1.0);
+    double v = __dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, __dadd_rn((double)py, jy)), (double)height));
+    double uw = __dmul_rn(u, c.half_w), vh = __dmul_rn(v, c.half_h);
+    double ddx = __dadd_rn(__dadd_rn(c.f[0], __dmul_rn(uw, c.r[0])), __dmul_rn(vh, c.u[0]));
+    double ddy = __dadd_rn(__dadd_rn(c.f[1], __dmul_rn(uw, c.r[1])), __dmul_rn(vh, c.u[1]));
+    double ddz = __dadd_rn(__dadd_rn(c.f[2], __dmul_rn(uw, c.r[2])), __dmul_rn(vh, c.u[2]));
+    double nn = __dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)), __dmul_rn(ddz, ddz));
+    double inv = __ddiv_rn(1.0, __dsqrt_rn(nn));
+    dx = __dmul_rn(ddx, inv);
+    dy = __dmul_rn(ddy, inv);
+    dz = __dmul_rn(ddz, inv);
+}
+
+// ---------------------------------------------------------------------------
+// Per-ray state for the traversal.
+// ---------------------------------------------------------------------------
+struct RayState {
+    double ox, oy, oz;     // origin (fp64, used by the candidate re-centring)
+    double dx, dy, dz;     // direction (fp64)
+    double inv_dd;         // 1 / |d|^2
+    float fdx, fdy, fdz;   // fp32 direction (quadratic form)
+    float idx, idy, idz;   // fp32 reciprocal direction (slab tests)
+    float oidx, oidy, oidz;  // o * idir (slab tests as one FMA per plane)
+    float t_min, t_max0;
+};
+
+__device__ __forceinline__ float safe_rcp(float d) {
+    // zero direction components: a huge finite reciprocal keeps the slab
+    // test exact-enough (kernels.py:276-279 treats d == 0 as 'inside slab')
+    const float tiny = 1e-30f;
+    if (fabsf(d) < tiny) d = copysignf(tiny, d);
+    return 1.0f / d;
+}
+
+__device__ __forceinline__ void init_ray(RayState &r, double ox, double oy, double oz, double dx, double dy,
+                                         double dz, double t_min, double t_max) {
+    r.ox = ox; r.oy = oy; r.oz = oz;
+    r.dx = dx; r.dy = dy; r.dz = dz;
+    r.inv_dd = 1.0 / (dx * dx + dy * dy + dz * dz);
+    r.fdx = (float)dx; r.fdy = (float)dy; r.fdz = (float)dz;
+    r.idx = safe_rcp(r.fdx); r.idy = safe_rcp(r.fdy); r.idz = safe_rcp(r.fdz);
+    r.oidx = (float)ox * r.idx; r.oidy = (float)oy * r.idy; r.oidz = (float)oz * r.idz;
+    // the candidate interval (t_min, t_max0) is open (kernels.py:349); fp32
+    // bounds are rounded so they never exclude what fp64 would include
+    r.t_min = (float)t_min;
+    r.t_max0 = t_max >= 3.0e38 ? INFINITY : (float)t_max;
+}
+
+// Slab entry of both children of a node against [t_min, far] (closed,
+// kernels.py:266-308).  Boxes are outward-rounded and inflated at build time.
+__device__ __forceinline__ void slab2(const RayState &r, const float4 &xy0, const float4 &xy1, const float4 &z01,
+                                      float far, float &e0, float &e1, bool &h0, bool &h1) {
+    float x0a = fmaf(xy0.x, r.idx, -r.oidx), x0b = fmaf(xy0.y, r.idx, -r.oidx);
+    float y0a = fmaf(xy0.z, r.idy, -r.oidy), y0b = fmaf(xy0.w, r.idy, -r.oidy);
+    float z0a = fmaf(z01.x, r.idz, -r.oidz), z0b = fmaf(z01.y, r.idz, -r.oidz);
+    float x1a = fmaf(xy1.x, r.idx, -r.oidx), x1b = fmaf(xy1.y, r.idx, -r.oidx);
+    float y1a = fmaf(xy1.z, r.idy, -r.oidy), y1b = fmaf(xy1.w, r.idy, -r.oidy);
+    float z1a = fmaf(z01.z, r.idz, -r.oidz), z1b = fmaf(z01.w, r.idz, -r.oidz);
+    float n0 = fmaxf(fmaxf(fminf(x0a, x0b), fminf(y0a, y0b)), fmaxf(fminf(z0a, z0b), r.t_min));
+    float f0 = fminf(fminf(fmaxf(x0a, x0b), fmaxf(y0a, y0b)), fminf(fmaxf(z0a, z0b), far));
+    float n1 = fmaxf(fmaxf(fminf(x1a, x1b), fminf(y1a, y1b)), fmaxf(fminf(z1a, z1b), r.t_min));
+    float f1 = fminf(fminf(fmaxf(x1a, x1b), fmaxf(y1a, y1b)), fminf(fmaxf(z1a, z1b), far));
+    h0 = n0 <= f0;
+    h1 = n1 <= f1;
+    e0 = n0;
+    e1 = n1;
+}
+
+// ---------------------------------------------------------------------------
+// Candidate (kernels.py:139-189), re-centred: the ray is re-expressed from
+// p = o + t0 d, t0 = (mu - o).d / |d|^2, the point nearest the mean, so the
+// quadratic form is evaluated on a SMALL vector w = p - mu and fp32 keeps
+// its accuracy.  t0 and w are formed in fp64 (the ray is fp64
+// end to end); the 3x3 quadratic form runs in fp32.
+// ---------------------------------------------------------------------------
+struct Cand {
+    float t;
+    float alpha;
+    int valid;
+};
+
+template <int MODE>
+__device__ __forceinline__ Cand candidate(const RayState &r, const float4 &m, const float4 &a, const float4 &b,
+                                          float s2) {
+    Cand c;
+    double vx = (double)m.x - r.ox, vy = (double)m.y - r.oy, vz = (double)m.z - r.oz;  // mu - o
+    double tc = vx * r.dx + vy * r.dy + vz * r.dz;  // (mu - o).d  == center depth (mode 1)
+    double t0 = tc * r.inv_dd;
+    float wx = (float)(t0 * r.dx - vx), wy = (float)(t0 * r.dy - vy), wz = (float)(t0 * r.dz - vz);
+    float a00 = a.x, a01 = a.y, a02 = a.z, a11 = a.w, a12 = b.x, a22 = b.y;
+    float adx = a00 * r.fdx + a01 * r.fdy + a02 * r.fdz;
+    float ady = a01 * r.fdx + a11 * r.fdy + a12 * r.fdz;
+    float adz = a02 * r.fdx + a12 * r.fdy + a22 * r.fdz;
+    float dad = r.fdx * adx + r.fdy * ady + r.fdz * adz;
+    float awx = a00 * wx + a01 * wy + a02 * wz;
+    float awy = a01 * wx + a11 * wy + a12 * wz;
+    float awz = a02 * wx + a12 * wy + a22 * wz;
+    float daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
+    float waw = wx * awx + wy * awy + wz * awz;
+    float resid = fmaxf(waw - daw * daw / dad, 0.0f);
+    float mah, t;
+    if (MODE == 0) {
+        t = (float)(t0 - (double)(daw / dad));
+        mah = resid;
+    } else {
+        t = (float)tc;
+        float s = (float)(tc - t0);
+        float qx = wx + s * r.fdx, qy = wy + s * r.fdy, qz = wz + s * r.fdz;
+        mah = qx * (a00 * qx + a01 * qy + a02 * qz) + qy * (a01 * qx + a11 * qy + a12 * qz) +
+              qz * (a02 * qx + a12 * qy + a22 * qz);
+    }
+    // dad <= 0 or non-finite -> invalid (kernels.py:167-168); mah > s2 ->
+    // outside the cutoff (kernels.py:187); open range (kernels.py:349)
+    c.valid = (dad > 0.0f) && isfinite(dad) && isfinite(t) && (mah <= s2) && (t > r.t_min) && (t < r.t_max0);
+    c.t = t;
+    c.alpha = m.w * __expf(-0.5f * resid);
+    return c;
+}
+
+// SH colour (kernels.py:193-257) in fp32 on the ray direction.
+__device__ __forceinline__ float3 sh_color(const float *__restrict__ sh, int K, int deg, int pid, float x, float y,
+                                           float z) {
+    const float SH_C0 = 0.28209479177387814f, SH_C1 = 0.4886025119029199f;
+    const float C2_0 = 1.0925484305920792f, C2_1 = -1.0925484305920792f, C2_2 = 0.31539156525252005f,
+                C2_3 = -1.0925484305920792f, C2_4 = 0.5462742152960396f;
+    const float C3_0 = -0.5900435899266435f, C3_1 = 2.890611442640554f, C3_2 = -0.4570457994644658f,
+                C3_3 = 0.3731763325901154f, C3_4 = -0.4570457994644658f, C3_5 = 1.445305721320277f,
+                C3_6 = -0.5900435899266435f;
+    const float *s = sh + (int64_t)pid * 3 * K;
+    float out[3];
+    float xx = x * x, yy = y * y, zz = z * z;
+    float b0 = x * y, b1 = y * z, b2 = 2.0f * zz - xx - yy, b3 = x * z, b4 = xx - yy;
+    float c0 = y * (3.0f * xx - yy), c1 = b0 * z, c2 = y * (4.0f * zz - xx - yy),
+          c3 = z * (2.0f * zz - 3.0f * xx - 3.0f * yy), c4 = x * (4.0f * zz - xx - yy), c5 = z * b4,
+          c6 = x * (xx - 3.0f * yy);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float *q = s + ch * K;
+        float v = SH_C0 * __ldg(q);
+        if (deg >= 1) v = v - SH_C1 * y * __ldg(q + 1) + SH_C1 * z * __ldg(q + 2) - SH_C1 * x * __ldg(q + 3);
+        if (deg >= 2)
+            v += C2_0 * b0 * __ldg(q + 4) + C2_1 * b1 * __ldg(q + 5) + C2_2 * b2 * __ldg(q + 6) +
+                 C2_3 * b3 * __ldg(q + 7) + C2_4 * b4 * __ldg(q + 8);
+        if (deg >= 3)
+            v += C3_0 * c0 * __ldg(q + 9) + C3_1 * c1 * __ldg(q + 10) + C3_2 * c2 * __ldg(q + 11) +
+                 C3_3 * c3 * __ldg(q + 12) + C3_4 * c4 * __ldg(q + 13) + C3_5 * c5 * __ldg(q + 14) +
+                 C3_6 * c6 * __ldg(q + 15);
+        out[ch] = fmaxf(v + 0.5f, 0.0f);
+    }
+    return make_float3(out[0], out[1], out[2]);
+}
+
+}  // namespace srt

@@ -1,0 +1,104 @@
+// srt_internal.h -- host-side scene object and helpers shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/srt.h"
+#include "srt_device.cuh"
+
+struct SrtScene {
+    int device = 0;
+    int64_t n = 0;
+    int32_t sh_deg = 0;
+    int32_t sh_k = 1;
+    // device records
+    double *d_means = nullptr;  // (n,3) f64 (LBVH box computation)
+    double *d_cov6 = nullptr;   // (n,6) f64
+    double *d_opac = nullptr;   // (n,)  f64
+    float *d_sh = nullptr;      // (n,3,K) f32, original order
+    srt::Geom *d_geom = nullptr;   // (n,) slot order (valid once a BVH exists)
+    srt::Node2 *d_nodes = nullptr; // (num_nodes,)
+    int32_t num_nodes = 0;
+    int32_t depth = 0;
+    bool has_bvh = false;
+    int32_t *d_flag = nullptr;  // device error flag (stack overflow)
+    // cached scratch for the host-pointer entry points
+    void *d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaStream_t stream = nullptr;
+    int64_t *slot_prim_host = nullptr;  // unused placeholder
+    srt::SceneView view() const {
+        srt::SceneView v;
+        v.nodes = d_nodes;
+        v.geom = d_geom;
+        v.sh = d_sh;
+        v.num_nodes = num_nodes;
+        v.root = 0;
+        v.sh_k = sh_k;
+        v.sh_deg = sh_deg;
+        v.n = n;
+        return v;
+    }
+};
+
+namespace srt {
+
+void set_error(const std::string &msg);
+srt_status cuda_status(cudaError_t e, const char *what);
+
+// RAII device guard: switch to the scene's device for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// fp64 box -> fp32, rounded outward and inflated (conservative slab tests).
+float box_lo_f32(double x);
+float box_hi_f32(double x);
+
+// build / launch helpers (lbvh.cu, trace.cu, shade.cu)
+srt_status lbvh_build(SrtScene *s, double cutoff_s);
+srt_status scratch_reserve(SrtScene *s, size_t bytes);
+
+struct RenderArgs {
+    int width, height, passes, nslots, mode, clip;
+    float s2;
+    uint32_t seed;
+    int pass0;
+    float bg[3];
+    int shard_index, shard_count;
+    int tiles_x;
+    int64_t local_tiles;
+};
+RenderArgs make_render_args(const SrtRenderParams *p);
+CamD make_cam(const SrtCamera *c);
+
+srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
+                             cudaStream_t st);
+srt_status launch_shade_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
+                             const int32_t *d_hits, float4 *d_accum, bool first, bool last, float4 *d_out,
+                             cudaStream_t st);
+srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R,
+                             int nslots, const double *d_table, float *d_t, int32_t *d_id, cudaStream_t st);
+srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max,
+                                int mode, double s2, double *d_out, cudaStream_t st);
+srt_status launch_resolve_f64(const RenderArgs &a, const float4 *d_out, double *d_rgb, double *d_op,
+                              cudaStream_t st);
+srt_status launch_unpack(const float4 *d_gathered, int width, int height, int shard_count, int64_t max_tiles,
+                         float4 *d_frame, cudaStream_t st);
+srt_status check_flag(const SrtScene *s, cudaStream_t st);
+
+int64_t shard_tiles(int width, int height, int shard_index, int shard_count);
+
+}  // namespace srt

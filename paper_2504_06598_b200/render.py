@@ -1,0 +1,129 @@
+"""The drop-in render API: ``render(asset, camera, settings, bvh=None, threads=None)``.
+
+Same signature, inputs and output type as the reference
+(/root/reference/pkg/src/splatray/render.py:125-174): a per-pixel mean image
+and opacity in an ``AccumBuffer`` with ``spp = passes * multisample``.  The
+frame is traced and shaded on a B200 by libsrt; the acceptance draw is the
+counter RNG u(seed, ray = py*W+px, sample = pass*N+slot, prim) instead of the
+reference's position hash (the fp64 trig hash cannot be
+reproduced by an fp32 tracer).  The device scene (fp32 records + LBVH) is
+cached on the asset, keyed by device and cutoff, like the reference caches
+``asset.packed``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .config import CameraConfig, RenderSettings
+from .sampling import pixel_jitter
+from .scene import DeviceScene, camera_tuple
+
+
+@dataclass
+class AccumBuffer:
+    """Per-pixel mean radiance, mean opacity and per-pixel sample count (render.py:32-55)."""
+
+    rgb: np.ndarray
+    opacity: np.ndarray
+    spp: int
+
+    def __post_init__(self):
+        self.rgb = np.asarray(self.rgb, dtype=np.float64)
+        self.opacity = np.asarray(self.opacity, dtype=np.float64)
+        if self.rgb.ndim != 3 or self.rgb.shape[2] != 3 or self.rgb.shape[:2] != self.opacity.shape:
+            raise ValueError("AccumBuffer shapes disagree")
+        self.spp = int(self.spp)
+        if self.spp < 1:
+            raise ValueError("sample count must be positive")
+
+    @property
+    def width(self) -> int:
+        return int(self.rgb.shape[1])
+
+    @property
+    def height(self) -> int:
+        return int(self.rgb.shape[0])
+
+
+def camera_basis(camera: CameraConfig):
+    """Orthonormal (forward, right, up) of a look-at camera (render.py:58-68)."""
+    fwd = camera.look_at - camera.position
+    fwd = fwd / np.linalg.norm(fwd)
+    right = np.cross(fwd, camera.up)
+    n = np.linalg.norm(right)
+    if n < 1e-12:
+        raise ValueError("camera up vector is parallel to the view direction")
+    right = right / n
+    up = np.cross(right, fwd)
+    return fwd, right, up
+
+
+def generate_camera_ray(camera: CameraConfig, settings: RenderSettings, pixel, frame: int):
+    """(origin, unit direction) of the jittered primary ray (render.py:71-94)."""
+    fwd, right, up = camera_basis(camera)
+    jx, jy = pixel_jitter(pixel, frame, settings.seed)
+    px, py = int(pixel[0]), int(pixel[1])
+    if not (0 <= px < settings.width and 0 <= py < settings.height):
+        raise ValueError(f"pixel {pixel} outside {settings.width}x{settings.height}")
+    half_h = math.tan(math.radians(camera.fov_deg) / 2.0)
+    half_w = half_h * (settings.width / settings.height)
+    u = 2.0 * (px + jx) / settings.width - 1.0
+    v = 1.0 - 2.0 * (py + jy) / settings.height
+    d = fwd + u * half_w * right + v * half_h * up
+    return camera.position.copy(), d / np.linalg.norm(d)
+
+
+def device_scene(asset, device: int = 0) -> DeviceScene:
+    """The asset's cached DeviceScene on `device` (uploaded on first use)."""
+    cache = asset.__dict__.setdefault("_srt_device_scenes", {})
+    sc = cache.get(device)
+    if sc is None:
+        sc = DeviceScene.from_packed(asset.packed, device)
+        cache[device] = sc
+    return sc
+
+
+def prepare(asset, settings: RenderSettings, bvh=None, device: int = 0) -> DeviceScene:
+    """Scene + BVH ready for `settings` (LBVH keyed by cutoff_s, or the given reference BVH)."""
+    sc = device_scene(asset, device)
+    if bvh is not None:
+        if sc.bvh_key != ("upload", id(bvh)):
+            sc.upload_bvh(bvh)
+    elif sc.bvh_key != ("lbvh", float(settings.cutoff_s)):
+        sc.build_bvh(settings.cutoff_s)
+    return sc
+
+
+def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, threads: int | None = None,
+           device: int = 0) -> AccumBuffer:
+    """Render a frame on the GPU (render.py:125-174).
+
+    ``threads`` is accepted for signature compatibility (the reference's CPU
+    thread count); it has no effect on the GPU.  ``reference_mode`` (exact
+    sorted compositing) is not on the GPU yet and raises.
+    """
+    del threads
+    if settings.reference_mode:
+        raise NotImplementedError("reference_mode (exact compositing) is not implemented on the GPU yet")
+    sc = prepare(asset, settings, bvh, device)
+    cam = camera_tuple(camera, settings.width, settings.height)
+    mode = 0 if settings.depth_mode == "mean" else 1
+    rgb, op, _ = sc.render(cam, settings.width, settings.height, settings.passes, settings.multisample, mode,
+                           settings.cutoff_s * settings.cutoff_s, True, settings.seed, settings.background)
+    return AccumBuffer(rgb, op, settings.samples_per_pixel)
+
+
+def image_metrics(image: AccumBuffer, reference: AccumBuffer) -> dict:
+    """MSE / PSNR (peak = max(1, reference max)) and mean |opacity error| (render.py:177-195)."""
+    if image.rgb.shape != reference.rgb.shape:
+        raise ValueError(f"image shapes disagree: {image.rgb.shape} vs {reference.rgb.shape}")
+    diff = image.rgb - reference.rgb
+    mse = float(np.mean(diff * diff))
+    peak = max(1.0, float(reference.rgb.max()))
+    psnr = math.inf if mse == 0.0 else 10.0 * math.log10(peak * peak / mse)
+    return {"mse": mse, "psnr": psnr,
+            "mean_abs_opacity_error": float(np.mean(np.abs(image.opacity - reference.opacity)))}
