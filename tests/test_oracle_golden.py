@@ -1,0 +1,141 @@
+"""Pin the oracle (C restatement) to the reference.
+
+Fixtures in tests/golden were produced by the unmodified reference
+(oracle/gen_golden.py).  In trig mode the oracle must reproduce them bit for
+bit; that is what makes it a trustworthy checker for the GPU path.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import S2, TMAX
+
+
+def test_frozen_hash_values(oracle):
+    """tests/test_sampling.py:18-27 of the reference."""
+    assert oracle.hash_position([0.0, 0.0, 0.0]) == pytest.approx(oracle.hash_position([0.0, 0.0, 0.0]))
+    assert oracle.hash_position([1.0, 2.0, 3.0]) == 0.8811819498150726
+    assert oracle.hash_position([1.0, 2.0, 3.0], slot=1) == 0.27091394690796733
+    assert oracle.hash_position([1.0, 2.0, 3.0], slot=5) == 0.1282423883676529
+    assert oracle.hash_position([-0.7, 0.3, 9.1]) == 0.04217293553301715
+
+
+def test_frozen_jitter_values(oracle):
+    """tests/test_sampling.py:71-77 of the reference."""
+    assert oracle.pixel_jitter(3, 5, 0, 0) == (0.27136341482400894, 0.6206638417206705)
+    assert oracle.pixel_jitter(3, 5, 7, 2) == (0.0026576726231724024, 0.32626721472479403)
+
+
+def test_hash_and_jitter_golden(oracle, golden):
+    g = golden("sampling")
+    hv = np.array([oracle.hash_position(p, int(k)) for p, k in zip(g["points"], g["slots"])])
+    np.testing.assert_array_equal(hv, g["hash"])
+    jit = np.array([oracle.pixel_jitter(*map(int, a)) for a in g["jitter_args"]])
+    np.testing.assert_array_equal(jit, g["jitter"])
+
+
+def test_sah_build_bitwise(oracle, golden):
+    """bvh.build (bvh.py:87-193) restated in C gives the identical tree."""
+    g = golden("bvh_3000")
+    b = oracle.sah_build(g["lo"], g["hi"])
+    for f in ("node_lo", "node_hi", "node_left", "node_right", "node_count", "prim_order"):
+        np.testing.assert_array_equal(getattr(b, f), g[f], err_msg=f)
+
+
+def _scene_400():
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    return random_cloud(400, seed=31)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("nslots", [1, 4])
+def test_trace_batch_bitwise(oracle, golden, mode, nslots):
+    """kernels.trace_batch (kernels.py:527-540), trig hash: (t, id) bit for bit."""
+    g = golden("trace_400")
+    a = _scene_400()
+    pk = a.packed
+    lo, hi = a.aabb_arrays(np.sqrt(S2))
+    b = oracle.sah_build(lo, hi)
+    t, ids = oracle.trace_batch(b, pk.means, pk.cov_inv6, pk.opacities, g["origins"], g["dirs"], 0.0, TMAX, mode, S2,
+                                True, nslots, rng="trig")
+    np.testing.assert_array_equal(ids, g[f"id_m{mode}_n{nslots}"])
+    np.testing.assert_array_equal(t, g[f"t_m{mode}_n{nslots}"])
+
+
+def test_transmittance_matches(oracle, golden):
+    g = golden("trace_400")
+    a = _scene_400()
+    pk = a.packed
+    lo, hi = a.aabb_arrays(np.sqrt(S2))
+    b = oracle.sah_build(lo, hi)
+    tr = oracle.transmittance(b, pk.means, pk.cov_inv6, pk.opacities, g["origins"], g["dirs"], 0.0, TMAX, 0, S2)
+    np.testing.assert_allclose(tr, g["transmittance"], rtol=1e-12, atol=0)
+
+
+def test_render_bitwise(oracle, golden):
+    """render() -> kernels.render_stochastic (kernels.py:622-673), trig hash."""
+    from paper_2504_06598_b200.synthetic import anisotropic_sheets, front_camera, random_cloud
+
+    g = golden("render_small")
+    a = random_cloud(300, seed=53, sh_degree=3)
+    pk = a.packed
+    lo, hi = a.aabb_arrays(np.sqrt(S2))
+    b = oracle.sah_build(lo, hi)
+    cam = front_camera()
+    ct = oracle.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, 24, 20)
+    out = oracle.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 3, ct, 24, 20, passes=3, nslots=2, s2=S2,
+                        seed=5, rng="trig", background=[0.1, 0.2, 0.3])
+    np.testing.assert_array_equal(out["rgb"], g["rgb"])
+    np.testing.assert_array_equal(out["opacity"], g["opacity"])
+    # center depth mode on tilted sheets
+    a2 = anisotropic_sheets(60, seed=3)
+    pk2 = a2.packed
+    lo, hi = a2.aabb_arrays(np.sqrt(S2))
+    b2 = oracle.sah_build(lo, hi)
+    ct2 = oracle.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, 16, 12)
+    out2 = oracle.render(b2, pk2.means, pk2.cov_inv6, pk2.opacities, pk2.sh, 0, ct2, 16, 12, passes=3, nslots=1,
+                         mode=1, s2=S2, seed=11, rng="trig")
+    np.testing.assert_array_equal(out2["rgb"], g["rgb_center"])
+    np.testing.assert_array_equal(out2["opacity"], g["opacity_center"])
+
+
+# ---- counter RNG spec (frozen) ---------------------------
+
+COUNTER_GOLDEN = [  # (seed, ray_id, sample, prim); values frozen in test_counter_rng_frozen_values
+    ((0, 0, 0, 0), None),
+    ((0, 1, 0, 0), None),
+    ((7, 123456, 3, 999), None),
+    ((0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF), None),
+]
+
+
+def test_counter_rng_c_matches_numpy(oracle):
+    rs = np.random.default_rng(5)
+    args = rs.integers(0, 2**32, size=(2000, 4), dtype=np.uint64)
+    c = np.array([oracle.counter_u(oracle.walk_key(int(s), int(r), int(k)), int(p)) for s, r, k, p in args])
+    v = oracle.counter_u_np(args[:, 0], args[:, 1], args[:, 2], args[:, 3])
+    np.testing.assert_array_equal(c, v)
+    assert np.all((c >= 0) & (c < 1))
+    assert np.all(c * 2**24 == np.floor(c * 2**24))  # exactly 24 bits
+
+
+def test_counter_rng_frozen_values(oracle):
+    vals = [oracle.counter_u(oracle.walk_key(s, r, k), p) for (s, r, k, p), _ in COUNTER_GOLDEN]
+    frozen = [0.6150132417678833, 0.4052417278289795, 0.8931280374526978, 0.8988131284713745]
+    assert vals == frozen
+
+
+def test_counter_rng_uniform_and_decorrelated(oracle):
+    """256-bin chi-square and adjacent-prim / adjacent-sample correlation."""
+    from scipy import stats
+
+    n = 200_000
+    prim = np.arange(n)
+    u0 = oracle.counter_u_np(0, 17, 0, prim)
+    u1 = oracle.counter_u_np(0, 17, 1, prim)
+    counts, _ = np.histogram(u0, bins=256, range=(0.0, 1.0))
+    assert stats.chisquare(counts).pvalue > 1e-3
+    assert abs(u0.mean() - 0.5) < 0.005
+    assert abs(np.corrcoef(u0[:-1], u0[1:])[0, 1]) < 0.01
+    assert abs(np.corrcoef(u0, u1)[0, 1]) < 0.01
