@@ -77,6 +77,11 @@ class ClockSampler:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t0 = time.time()
+            while time.time() - t0 < 5.0:  # wait for the first sample so the timed region is covered
+                if self.path.exists() and self.path.stat().st_size > 0:
+                    break
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
@@ -221,21 +226,22 @@ def run_ours(args) -> None:
         if ev is not None:
             ev[2].record(stream)
 
-    for _ in range(max(args.warmup, 0)):
-        step()
-    torch.cuda.synchronize(dev)
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    wall0 = time.perf_counter()
     with sampler:
+        for _ in range(max(args.warmup, 0)):
+            step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        wall0 = time.perf_counter()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)  # evict the scene from L2 between steps (outside the step events)
             step(events[i])
         torch.cuda.synchronize(dev)
-    wall = time.perf_counter() - wall0
+        wall = time.perf_counter() - wall0
+        time.sleep(0.25)  # let the sampler record the tail of the timed region
     if world > 1:
         dist.barrier()
     step_ms = [e[0].elapsed_time(e[2]) for e in events]
@@ -316,7 +322,7 @@ def run_ours(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -159,6 +159,11 @@ srt_status srt_shade_pass_device(const SrtScene *scene, const SrtCamera *camera,
 srt_status srt_render_device(const SrtScene *scene, const SrtCamera *camera,
                              const SrtRenderParams *params, int32_t *d_hits, float *d_accum,
                              float *d_out, void *stream);
+/* Traversal work counters accumulated while the environment variable
+ * SRT_TRACE_STATS=1 is set: out[8] = node visits, leaf visits, screen
+ * passes, exact evaluations, accepted slot updates, stack pops, culled
+ * pops, walks.  reset != 0 zeroes them. */
+srt_status srt_trace_stats(const SrtScene *scene, uint64_t *out, int32_t reset);
 /* Number of 16x16 tiles a shard owns (buffer sizing for tile-compact layout). */
 int64_t srt_shard_tiles(int32_t width, int32_t height, int32_t shard_index,
                         int32_t shard_count);

@@ -78,6 +78,7 @@ SYMBOLS = [
                                      _vp, _i32, _i32, _vp, _vp]),
     ("srt_render_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp,
                                  _vp]),
+    ("srt_trace_stats", _i32, [_vp, _vp, _i32]),
     ("srt_shard_tiles", _i64, [_i32, _i32, _i32, _i32]),
     ("srt_unpack_tiles_device", _i32, [_vp, _i32, _i32, _i32, _i64, _vp, _vp]),
 ]

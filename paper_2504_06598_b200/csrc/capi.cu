@@ -161,6 +161,9 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_work, sizeof(uint32_t) * 4), "work counter alloc");
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 8), "stats alloc");
+    if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 8), "stats init");
     if (!rc && n > 0) {
         rc = cuda_status(cudaMalloc(&s->d_means, sizeof(double) * n * 3), "means alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_cov6, sizeof(double) * n * 6), "cov alloc");
@@ -193,6 +196,9 @@ srt_status srt_scene_destroy(SrtScene *s) {
     cudaFree(s->d_sh);
     cudaFree(s->d_geom);
     cudaFree(s->d_nodes);
+    cudaFree(s->d_nodes4);
+    cudaFree(s->d_work);
+    cudaFree(s->d_stats);
     cudaFree(s->d_flag);
     cudaFree(s->d_scratch);
     if (s->stream) cudaStreamDestroy(s->stream);
@@ -361,6 +367,8 @@ srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const d
     if (rc) return rc;
     s->num_nodes = (int32_t)nodes.size();
     s->depth = max_depth + 1;
+    rc = collapse4(s);
+    if (rc) return rc;
     s->has_bvh = true;
     return SRT_OK;
 }
@@ -682,6 +690,18 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb download");
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "opacity download");
     if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+srt_status srt_trace_stats(const SrtScene *s, uint64_t *out, int32_t reset) {
+    if (!s || !out) {
+        set_error("null scene or output");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    srt_status rc = cuda_status(cudaDeviceSynchronize(), "sync");
+    if (!rc) rc = cuda_status(cudaMemcpy(out, s->d_stats, sizeof(uint64_t) * 8, cudaMemcpyDeviceToHost), "stats");
+    if (!rc && reset) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(uint64_t) * 8), "stats reset");
     return rc;
 }
 

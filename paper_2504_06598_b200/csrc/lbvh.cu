@@ -341,6 +341,7 @@ srt_status lbvh_build(SrtScene *s, double cutoff_s) {
         s->depth = h_depth;
     }
     SRT_TRY(cuda_status(cudaStreamSynchronize(st), "lbvh build"));
+    SRT_TRY(collapse4(s));
     s->has_bvh = true;
 done:
 #undef SRT_TRY
@@ -358,6 +359,153 @@ done:
     cudaFree(ibox);
     cudaFree(ddepth);
     cudaFree(temp);
+    return rc;
+}
+
+}  // namespace srt
+
+// ---------------------------------------------------------------------------
+// Binary -> 4-wide collapse.  Each 4-wide node starts from a binary node's two
+// children and repeatedly opens the inner child with the largest surface
+// area until it holds 4 children (or only leaves remain).  Breadth-first
+// waves over a device worklist; boxes come from the parents' Node2 records.
+// ---------------------------------------------------------------------------
+namespace srt {
+
+struct Entry4 {
+    int code;
+    float lo[3], hi[3];
+};
+
+__device__ __forceinline__ void node2_child(const Node2 &nd, int c, Entry4 &e) {
+    if (c == 0) {
+        e.code = nd.kids.x;
+        e.lo[0] = nd.xy0.x; e.hi[0] = nd.xy0.y; e.lo[1] = nd.xy0.z; e.hi[1] = nd.xy0.w;
+        e.lo[2] = nd.z01.x; e.hi[2] = nd.z01.y;
+    } else {
+        e.code = nd.kids.y;
+        e.lo[0] = nd.xy1.x; e.hi[0] = nd.xy1.y; e.lo[1] = nd.xy1.z; e.hi[1] = nd.xy1.w;
+        e.lo[2] = nd.z01.z; e.hi[2] = nd.z01.w;
+    }
+}
+
+__device__ __forceinline__ float area(const Entry4 &e) {
+    float dx = e.hi[0] - e.lo[0], dy = e.hi[1] - e.lo[1], dz = e.hi[2] - e.lo[2];
+    return dx * dy + dy * dz + dz * dx;
+}
+
+// work item: (binary node id, 4-wide node index)
+__global__ void k_collapse4(const Node2 *__restrict__ n2, const int2 *__restrict__ work_in, int n_in,
+                            int2 *work_out, int *n_out, int *n4_count, Node4 *n4) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_in) return;
+    int2 w = work_in[i];
+    Entry4 e[4];
+    int cnt = 0;
+    Node2 root = n2[w.x];
+    for (int c = 0; c < 2; ++c) {
+        node2_child(root, c, e[cnt]);
+        if (e[cnt].code != kLeafEmpty) ++cnt;
+    }
+    while (cnt < 4) {
+        int best = -1;
+        float ba = -1.f;
+        for (int k = 0; k < cnt; ++k)
+            if (e[k].code >= 0 && area(e[k]) > ba) {
+                ba = area(e[k]);
+                best = k;
+            }
+        if (best < 0) break;
+        Node2 nd = n2[e[best].code];
+        Entry4 a, b;
+        node2_child(nd, 0, a);
+        node2_child(nd, 1, b);
+        if (a.code == kLeafEmpty) {
+            e[best] = b;
+        } else if (b.code == kLeafEmpty) {
+            e[best] = a;
+        } else {
+            e[best] = a;
+            e[cnt++] = b;
+        }
+    }
+    int ninner = 0;
+    for (int k = 0; k < cnt; ++k) ninner += e[k].code >= 0;
+    int base4 = ninner ? atomicAdd(n4_count, ninner) : 0;
+    int basew = ninner ? atomicAdd(n_out, ninner) : 0;
+    float lo[3][4], hi[3][4];
+    int kids[4];
+    int j = 0;
+    for (int k = 0; k < 4; ++k) {
+        if (k < cnt) {
+            for (int a = 0; a < 3; ++a) {
+                lo[a][k] = e[k].lo[a];
+                hi[a][k] = e[k].hi[a];
+            }
+            if (e[k].code >= 0) {
+                kids[k] = base4 + j;
+                work_out[basew + j] = make_int2(e[k].code, base4 + j);
+                ++j;
+            } else {
+                kids[k] = e[k].code;
+            }
+        } else {
+            for (int a = 0; a < 3; ++a) {
+                lo[a][k] = 3.0e38f;
+                hi[a][k] = -3.0e38f;
+            }
+            kids[k] = kLeafEmpty;
+        }
+    }
+    Node4 o;
+    o.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    o.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    o.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    o.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    o.kids = make_int4(kids[0], kids[1], kids[2], kids[3]);
+    o.pad = make_int4(cnt, 0, 0, 0);
+    n4[w.y] = o;
+}
+
+srt_status collapse4(SrtScene *s) {
+    cudaStream_t st = s->stream;
+    if (s->d_nodes4) cudaFree(s->d_nodes4);
+    s->d_nodes4 = nullptr;
+    s->num_nodes4 = 0;
+    if (s->num_nodes == 0) return SRT_OK;
+    const int m2 = s->num_nodes;
+    srt_status rc = SRT_OK;
+    int2 *wa = nullptr, *wb = nullptr;
+    int *counters = nullptr;  // [0] n4 count, [1] work_out count
+    int h[2] = {1, 0};
+    int n_in = 1;
+    int2 root = make_int2(0, 0);
+    // a 4-wide tree over m2 binary inner nodes has at most m2 nodes
+    rc = cuda_status(cudaMalloc(&s->d_nodes4, sizeof(Node4) * m2), "node4 alloc");
+    if (!rc) rc = cuda_status(cudaMalloc(&wa, sizeof(int2) * m2), "worklist");
+    if (!rc) rc = cuda_status(cudaMalloc(&wb, sizeof(int2) * m2), "worklist");
+    if (!rc) rc = cuda_status(cudaMalloc(&counters, sizeof(int) * 2), "counters");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(wa, &root, sizeof(int2), cudaMemcpyHostToDevice, st), "root");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(counters, h, sizeof(h), cudaMemcpyHostToDevice, st), "counters");
+    while (!rc && n_in > 0) {
+        rc = cuda_status(cudaMemsetAsync(counters + 1, 0, sizeof(int), st), "counter reset");
+        if (rc) break;
+        k_collapse4<<<(n_in + 127) / 128, 128, 0, st>>>(s->d_nodes, wa, n_in, wb, counters + 1, counters,
+                                                       s->d_nodes4);
+        rc = cuda_status(cudaGetLastError(), "k_collapse4");
+        if (!rc) rc = cuda_status(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, st), "counters");
+        if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "collapse");
+        n_in = h[1];
+        int2 *t = wa;
+        wa = wb;
+        wb = t;
+    }
+    if (!rc) s->num_nodes4 = h[0];
+    cudaFree(wa);
+    cudaFree(wb);
+    cudaFree(counters);
     return rc;
 }
 

@@ -25,6 +25,15 @@ struct __align__(16) Node2 {
     int4 kids;   // child0, child1 (>=0 inner node, <0 leaf ~slot, kLeafEmpty), pad
 };
 
+// 4-wide node, one 128-B line: child boxes SoA + child codes.  Produced by
+// collapsing the binary tree (greedy largest-area expansion); unused slots
+// have an empty box and code kLeafEmpty.
+struct __align__(128) Node4 {
+    float4 lox, hix, loy, hiy, loz, hiz;
+    int4 kids;
+    int4 pad;
+};
+
 struct __align__(16) Geom {
     float4 m;  // mean.xyz, opacity
     float4 a;  // a00 a01 a02 a11
@@ -33,6 +42,8 @@ struct __align__(16) Geom {
 
 struct SceneView {
     const Node2 *nodes;
+    const Node4 *nodes4;
+    int32_t num_nodes4;
     const Geom *geom;
     const float *sh;  // (n, 3, K) fp32, original id order
     int32_t num_nodes;
@@ -124,6 +135,8 @@ __device__ __forceinline__ void camera_ray(const CamD &c, uint32_t px, uint32_t 
 // Per-ray state for the traversal.
 // ---------------------------------------------------------------------------
 struct RayState {
+    float fox, foy, foz;   // fp32 origin (stage-1 screen)
+    float omag;            // max |o_i| (screen error model)
     double ox, oy, oz;     // origin (fp64, used by the candidate re-centring)
     double dx, dy, dz;     // direction (fp64)
     double inv_dd;         // 1 / |d|^2
@@ -144,6 +157,8 @@ __device__ __forceinline__ float safe_rcp(float d) {
 __device__ __forceinline__ void init_ray(RayState &r, double ox, double oy, double oz, double dx, double dy,
                                          double dz, double t_min, double t_max) {
     r.ox = ox; r.oy = oy; r.oz = oz;
+    r.fox = (float)ox; r.foy = (float)oy; r.foz = (float)oz;
+    r.omag = fmaxf(fabsf(r.fox), fmaxf(fabsf(r.foy), fabsf(r.foz)));
     r.dx = dx; r.dy = dy; r.dz = dz;
     r.inv_dd = 1.0 / (dx * dx + dy * dy + dz * dz);
     r.fdx = (float)dx; r.fdy = (float)dy; r.fdz = (float)dz;
@@ -224,6 +239,61 @@ __device__ __forceinline__ Cand candidate(const RayState &r, const float4 &m, co
     c.t = t;
     c.alpha = m.w * __expf(-0.5f * resid);
     return c;
+}
+
+// Stage-1 screen: the same quantities as `candidate` in plain fp32 (no
+// fp64), with a conservative bound on their rounding error.  A candidate the
+// screen rejects is certainly invalid or beyond `far`; `alpha_hi` bounds
+// alpha from above, so a draw u >= alpha_hi is certainly a rejection and the
+// exact fp64 evaluation can be skipped (it runs for ~1 candidate in 10).
+struct Screen {
+    float t_lo;      // lower bound of the candidate depth
+    float alpha_hi;  // upper bound of alpha
+    bool maybe;      // could be a valid candidate inside (t_min, far]
+};
+
+template <int MODE>
+__device__ __forceinline__ Screen screen(const RayState &r, const float4 &m, const float4 &a, const float4 &b,
+                                         float s2, float far) {
+    Screen sc;
+    float vx = m.x - r.fox, vy = m.y - r.foy, vz = m.z - r.foz;
+    float tc = vx * r.fdx + vy * r.fdy + vz * r.fdz;
+    float t0 = tc * (float)r.inv_dd;
+    float wx = fmaf(t0, r.fdx, -vx), wy = fmaf(t0, r.fdy, -vy), wz = fmaf(t0, r.fdz, -vz);
+    float a00 = a.x, a01 = a.y, a02 = a.z, a11 = a.w, a12 = b.x, a22 = b.y;
+    float adx = a00 * r.fdx + a01 * r.fdy + a02 * r.fdz;
+    float ady = a01 * r.fdx + a11 * r.fdy + a12 * r.fdz;
+    float adz = a02 * r.fdx + a12 * r.fdy + a22 * r.fdz;
+    float dad = r.fdx * adx + r.fdy * ady + r.fdz * adz;
+    float awx = a00 * wx + a01 * wy + a02 * wz;
+    float awy = a01 * wx + a11 * wy + a12 * wz;
+    float awz = a02 * wx + a12 * wy + a22 * wz;
+    float daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
+    float waw = wx * awx + wy * awy + wz * awz;
+    float inv_dad = 1.0f / dad;
+    float resid = waw - daw * daw * inv_dad;
+    float mah, t;
+    // absolute error of w: roundings of |o|, |mu|, |t0|-sized terms
+    float mmag = fmaxf(fabsf(m.x), fmaxf(fabsf(m.y), fabsf(m.z)));
+    float e = 4.0e-7f * (fabsf(t0) + r.omag + mmag) + 1e-30f;
+    float tr = fabsf(a00) + fabsf(a11) + fabsf(a22) + 2.0f * (fabsf(a01) + fabsf(a02) + fabsf(a12));
+    float mr = 4.0f * sqrtf(s2 * tr) * e + 4.0f * tr * e * e + 2.0e-5f * (fabsf(waw) + 1e-6f);
+    if (MODE == 0) {
+        t = t0 - daw * inv_dad;
+        mah = resid;
+    } else {
+        t = tc;
+        float sd = tc - t0;
+        float qx = fmaf(sd, r.fdx, wx), qy = fmaf(sd, r.fdy, wy), qz = fmaf(sd, r.fdz, wz);
+        mah = qx * (a00 * qx + a01 * qy + a02 * qz) + qy * (a01 * qx + a11 * qy + a12 * qz) +
+              qz * (a02 * qx + a12 * qy + a22 * qz);
+        mr += 2.0e-5f * fabsf(mah);
+    }
+    float mt = e * (1.0f + sqrtf(fmaxf(tr * inv_dad, 0.0f))) + 2.0e-6f * (fabsf(t) + 1.0f);
+    sc.t_lo = t - mt;
+    sc.maybe = (dad > 0.0f) && (mah - mr <= s2) && (t - mt <= far) && (t + mt > r.t_min) && (t - mt < r.t_max0);
+    sc.alpha_hi = m.w * __expf(-0.5f * fmaxf(resid - mr, 0.0f)) * 1.0001f + 1e-7f;
+    return sc;
 }
 
 // SH colour (kernels.py:193-257) in fp32 on the ray direction.

@@ -20,8 +20,12 @@ struct SrtScene {
     double *d_opac = nullptr;   // (n,)  f64
     float *d_sh = nullptr;      // (n,3,K) f32, original order
     srt::Geom *d_geom = nullptr;   // (n,) slot order (valid once a BVH exists)
-    srt::Node2 *d_nodes = nullptr; // (num_nodes,)
+    srt::Node2 *d_nodes = nullptr; // (num_nodes,) binary tree (build / upload output)
     int32_t num_nodes = 0;
+    srt::Node4 *d_nodes4 = nullptr; // (num_nodes4,) 4-wide tree traced by the kernels
+    int32_t num_nodes4 = 0;
+    uint32_t *d_work = nullptr;     // persistent-kernel work counters
+    unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
     bool has_bvh = false;
     int32_t *d_flag = nullptr;  // device error flag (stack overflow)
@@ -33,6 +37,8 @@ struct SrtScene {
     srt::SceneView view() const {
         srt::SceneView v;
         v.nodes = d_nodes;
+        v.nodes4 = d_nodes4;
+        v.num_nodes4 = num_nodes4;
         v.geom = d_geom;
         v.sh = d_sh;
         v.num_nodes = num_nodes;
@@ -69,6 +75,7 @@ float box_hi_f32(double x);
 
 // build / launch helpers (lbvh.cu, trace.cu, shade.cu)
 srt_status lbvh_build(SrtScene *s, double cutoff_s);
+srt_status collapse4(SrtScene *s);
 srt_status scratch_reserve(SrtScene *s, size_t bytes);
 
 struct RenderArgs {

@@ -1,16 +1,27 @@
-// trace.cu -- stochastic BVH walk (kernels.py:312-388) for camera rays and
-// explicit rays, plus the unclipped transmittance walk (kernels.py:392-432).
+// trace.cu -- stochastic BVH walk (kernels.py:312-388) over the 4-wide tree,
+// for camera rays (one pass of render_stochastic, kernels.py:644-656) and
+// explicit rays (trace_batch, kernels.py:527-540), plus the unclipped
+// transmittance walk (kernels.py:392-432).
 //
-// One thread per ray.  Camera rays are mapped 8x4 pixels per warp inside
-// 16x16 tiles so a warp's rays are coherent and share node fetches.  Each
-// visit reads one 64-B Node2 (both children's boxes), tests both boxes,
-// resolves leaf children (single primitives) on the spot and descends into
-// the nearer inner child, pushing the farther one with its entry distance.
+// Execution model: persistent warps.  A grid of
+// SMs x resident-blocks warps pulls ray indices from one atomic counter; a
+// warp refills its idle lanes (consecutive indices = an 8x4 pixel block, so
+// new rays stay coherent with the warp's others) whenever at least kRefill
+// lanes are idle.  Per lane the walk is "while-while" (Aila & Laine 2009):
+// an inner loop visits 4-wide nodes, pushing hit children (inner nodes AND
+// single-primitive leaves) far-to-near on a local stack; a leaf reached at
+// the front is postponed while the lane keeps traversing, and the warp
+// switches to candidate evaluation once every lane holds a postponed leaf.
+// That keeps the expensive candidate code (kernels.py:139-189 + the
+// acceptance draw) executing with most lanes converged.
 #include <cfloat>
+#include <cstdlib>
 
 #include "srt_internal.h"
 
 namespace srt {
+
+constexpr int kDone = kLeafEmpty;  // "no item" code for the next node / postponed leaf
 
 template <int NS>
 struct Slots {
@@ -18,108 +29,6 @@ struct Slots {
     int id[NS];
     uint32_t key[NS];
 };
-
-// Acceptance draw of slot k for primitive `pid` (kernels.py:354 with the
-// counter generator; RNG==SRT_RNG_TABLE reads an explicit uniform).
-template <int RNG>
-__device__ __forceinline__ bool accepts(uint32_t key, const double *table, int64_t tstride, int pid, int k,
-                                        float alpha) {
-    if (RNG == SRT_RNG_TABLE) return __ldg(table + (int64_t)pid * tstride + k) < (double)alpha;
-    return counter_u(key, (uint32_t)pid) < alpha;
-}
-
-template <int NS, int MODE, int RNG>
-__device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r, float s2, int clip, int slot,
-                                           Slots<NS> &sl, float &far, const double *table, int64_t tstride) {
-    const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
-    float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
-    Cand c = candidate<MODE>(r, m, a, b, s2);
-    if (!c.valid) return;
-    int pid = __float_as_int(b.z);
-    bool improved = false;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-        // strict t < slot_t (kernels.py:354); an exact tie goes to the
-        // smaller primitive id so the result is visit-order independent
-        bool nearer = c.t < sl.t[k] || (c.t == sl.t[k] && pid < sl.id[k]);
-        if (nearer && accepts<RNG>(sl.key[k], table, tstride, pid, k, c.alpha)) {
-            sl.t[k] = c.t;
-            sl.id[k] = pid;
-            improved = true;
-        }
-    }
-    if (improved && clip) {
-        // clip to the farthest slot once every slot holds a hit (kernels.py:358-364);
-        // inactive slots hold -inf and never bind
-        float worst = sl.t[0];
-#pragma unroll
-        for (int k = 1; k < NS; ++k) worst = fmaxf(worst, sl.t[k]);
-        far = fminf(far, worst);
-    }
-}
-
-template <int NS, int MODE, int RNG>
-__device__ __forceinline__ void walk(const SceneView &s, const RayState &r, float s2, int clip, Slots<NS> &sl,
-                                     const double *table, int64_t tstride, int *overflow) {
-    if (s.num_nodes == 0) return;
-    float far = r.t_max0;
-    int stk_node[kStackSize];
-    float stk_t[kStackSize];
-    int sp = 0;
-    int cur = 0;
-    while (true) {
-        const float4 *np = reinterpret_cast<const float4 *>(s.nodes + cur);
-        float4 xy0 = __ldg(np), xy1 = __ldg(np + 1), z01 = __ldg(np + 2);
-        int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 3));
-        float e0, e1;
-        bool h0, h1;
-        slab2(r, xy0, xy1, z01, far, e0, e1, h0, h1);
-        int c0 = kids.x, c1 = kids.y;
-        if (e1 < e0) {  // near child first
-            int ti = c0; c0 = c1; c1 = ti;
-            float tf = e0; e0 = e1; e1 = tf;
-            bool tb = h0; h0 = h1; h1 = tb;
-        }
-        if (h0 && c0 < 0) {
-            if (c0 != kLeafEmpty) visit_leaf<NS, MODE, RNG>(s, r, s2, clip, ~c0, sl, far, table, tstride);
-            h0 = false;
-        }
-        if (h1 && c1 < 0) {
-            if (c1 != kLeafEmpty && e1 <= far) visit_leaf<NS, MODE, RNG>(s, r, s2, clip, ~c1, sl, far, table, tstride);
-            h1 = false;
-        }
-        h0 = h0 && e0 <= far;
-        h1 = h1 && e1 <= far;
-        if (h0) {
-            if (h1) {
-                if (sp >= kStackSize) {
-                    atomicExch(overflow, 1);
-                    return;
-                }
-                stk_node[sp] = c1;
-                stk_t[sp] = e1;
-                ++sp;
-            }
-            cur = c0;
-            continue;
-        }
-        if (h1) {
-            cur = c1;
-            continue;
-        }
-        // pop, culling entries beyond the (possibly clipped) far bound
-        bool found = false;
-        while (sp > 0) {
-            --sp;
-            if (stk_t[sp] <= far) {
-                cur = stk_node[sp];
-                found = true;
-                break;
-            }
-        }
-        if (!found) return;
-    }
-}
 
 template <int NS>
 __device__ __forceinline__ void init_slots(Slots<NS> &sl, int nslots) {
@@ -131,8 +40,217 @@ __device__ __forceinline__ void init_slots(Slots<NS> &sl, int nslots) {
     }
 }
 
+// Acceptance draw of slot k (kernels.py:354): counter generator or table.
+template <int RNG>
+__device__ __forceinline__ bool accepts(uint32_t key, const double *table, int64_t tstride, int pid, int k,
+                                        float alpha) {
+    if (RNG == SRT_RNG_TABLE) return __ldg(table + (int64_t)pid * tstride + k) < (double)alpha;
+    return counter_u(key, (uint32_t)pid) < alpha;
+}
+
+struct WalkCfg {
+    float s2;
+    int clip;
+    const double *table;
+    int64_t tstride;
+};
+
+// Optional per-walk work counters (SRT_TRACE_STATS=1): node visits, leaf
+// visits, screen passes, exact evaluations, accepted updates, stack pops,
+// culled pops, walks.  Accumulated per lane, flushed with one atomic each.
+template <bool STATS>
+struct Counters {
+    __device__ __forceinline__ void add(int, unsigned) {}
+    __device__ __forceinline__ void flush(unsigned long long *) {}
+};
+template <>
+struct Counters<true> {
+    unsigned c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    __device__ __forceinline__ void add(int i, unsigned v) { c[i] += v; }
+    __device__ __forceinline__ void flush(unsigned long long *out) {
+        for (int i = 0; i < 8; ++i)
+            if (c[i]) atomicAdd(out + i, (unsigned long long)c[i]);
+        for (int i = 0; i < 8; ++i) c[i] = 0;
+    }
+};
+
+template <int NS, int MODE, int RNG, bool STATS>
+__device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r, const WalkCfg &w, int slot,
+                                           Slots<NS> &sl, float &far, Counters<STATS> &ct) {
+    ct.add(1, 1);
+    const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+    float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+    // stage 1: fp32 screen -- can this candidate be accepted by any slot?
+    Screen sc = screen<MODE>(r, m, a, b, w.s2, far);
+    if (!sc.maybe) return;
+    ct.add(2, 1);
+    int pid = __float_as_int(b.z);
+    bool need = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        if (sc.t_lo <= sl.t[k]) {
+            float u = RNG == SRT_RNG_TABLE ? (float)__ldg(w.table + (int64_t)pid * w.tstride + k)
+                                           : counter_u(sl.key[k], (uint32_t)pid);
+            need |= u <= sc.alpha_hi;
+        }
+    }
+    if (!need) return;
+    ct.add(3, 1);
+    // stage 2: exact evaluation (fp64 re-centring, kernels.py:139-189)
+    Cand c = candidate<MODE>(r, m, a, b, w.s2);
+    if (!c.valid) return;
+    bool improved = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        // strict t < slot_t (kernels.py:354); an exact tie goes to the
+        // smaller primitive id so the result is visit-order independent
+        bool nearer = c.t < sl.t[k] || (c.t == sl.t[k] && pid < sl.id[k]);
+        if (nearer && accepts<RNG>(sl.key[k], w.table, w.tstride, pid, k, c.alpha)) {
+            sl.t[k] = c.t;
+            sl.id[k] = pid;
+            improved = true;
+        }
+    }
+    ct.add(4, improved ? 1u : 0u);
+    if (improved && w.clip) {
+        // clip to the farthest slot once every slot holds a hit (kernels.py:358-364);
+        // inactive slots hold -inf and never bind
+        float worst = sl.t[0];
+#pragma unroll
+        for (int k = 1; k < NS; ++k) worst = fmaxf(worst, sl.t[k]);
+        far = fminf(far, worst);
+    }
+}
+
+__device__ __forceinline__ int ordered_key(float t, int k) {
+    int i = __float_as_int(t);
+    i = i >= 0 ? i : i ^ 0x7FFFFFFF;
+    return (i & ~3) | k;
+}
+__device__ __forceinline__ float key_t(int key) {
+    int ki = key & ~3;
+    return __int_as_float(ki >= 0 ? ki : ki ^ 0x7FFFFFFF);
+}
+
+__device__ __forceinline__ int pick(const int4 &v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+
+// Per-lane traversal state (registers + a local-memory stack).
+struct Walk {
+    int next;  // next inner node, or kDone
+    int sp;
+    float far;
+    int stk_code[kStackSize];
+    float stk_t[kStackSize];
+
+    float popped_t;  // entry distance of the last popped node
+
+    template <class CT>
+    __device__ __forceinline__ int pop(CT &ct) {
+        while (sp > 0) {
+            --sp;
+            ct.add(5, 1);
+            if (stk_t[sp] <= far) {  // cull beyond the (clipped) far bound
+                popped_t = stk_t[sp];
+                return stk_code[sp];
+            }
+            ct.add(6, 1);
+        }
+        return kDone;
+    }
+};
+
+// Slab test of the 4 children of a node against [t_min, far] (closed,
+// kernels.py:266-308): bit k of the result is set when child k is hit;
+// key[k] = entry distance (orderable int) with k in the low 2 bits.
+__device__ __forceinline__ unsigned slab4(const RayState &r, const float4 *np, float far, int4 &kids, int key[4]) {
+    float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3), loz = __ldg(np + 4),
+           hiz = __ldg(np + 5);
+    kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+    float lx[4] = {lox.x, lox.y, lox.z, lox.w}, hx[4] = {hix.x, hix.y, hix.z, hix.w};
+    float ly[4] = {loy.x, loy.y, loy.z, loy.w}, hy[4] = {hiy.x, hiy.y, hiy.z, hiy.w};
+    float lz[4] = {loz.x, loz.y, loz.z, loz.w}, hz[4] = {hiz.x, hiz.y, hiz.z, hiz.w};
+    unsigned hitm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float xa = fmaf(lx[k], r.idx, -r.oidx), xb = fmaf(hx[k], r.idx, -r.oidx);
+        float ya = fmaf(ly[k], r.idy, -r.oidy), yb = fmaf(hy[k], r.idy, -r.oidy);
+        float za = fmaf(lz[k], r.idz, -r.oidz), zb = fmaf(hz[k], r.idz, -r.oidz);
+        float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
+        float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
+        // empty slots carry inverted boxes, which min/max slab tests would see
+        // as infinite: mask them by code
+        bool hit = tn <= tf && pick(kids, k) != kLeafEmpty;
+        key[k] = ordered_key(tn, k);
+        hitm |= hit ? (1u << k) : 0u;
+    }
+    return hitm;
+}
+
+// Visit one 4-wide node: resolve the hit leaf children (single primitives)
+// on the spot -- they may clip `far` -- then descend into the nearest hit
+// inner child, pushing the others far-to-near.  Returns the next inner node.
+template <int NS, int MODE, int RNG, bool STATS>
+__device__ __forceinline__ int visit_node(const SceneView &s, const RayState &r, const WalkCfg &w, Walk &wk,
+                                          Slots<NS> &sl, int node, int *overflow, Counters<STATS> &ct) {
+    ct.add(0, 1);
+    int4 kids;
+    int key[4];
+    unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), wk.far, kids, key);
+    unsigned leafm = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) leafm |= pick(kids, k) < 0 ? (1u << k) : 0u;
+    unsigned lm = hitm & leafm;
+    while (lm) {
+        int k = __ffs(lm) - 1;
+        lm &= lm - 1;
+        visit_leaf<NS, MODE, RNG, STATS>(s, r, w, ~pick(kids, k), sl, wk.far, ct);
+    }
+    unsigned im = hitm & ~leafm;
+    if (!im) return wk.pop(ct);
+    // order the hit inner children by entry distance
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (!(im & (1u << k))) key[k] = 0x7FFFFFFF;
+    int ni = __popc(im);
+    if (ni > 1) {
+#define SRT_CX(a, b)                      \
+    {                                     \
+        int lo_ = min(key[a], key[b]);    \
+        int hi_ = max(key[a], key[b]);    \
+        key[a] = lo_;                     \
+        key[b] = hi_;                     \
+    }
+        SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
+#undef SRT_CX
+        if (wk.sp + ni - 1 > kStackSize) {
+            atomicExch(overflow, 1);
+            wk.sp = 0;
+            return kDone;
+        }
+#pragma unroll
+        for (int j = 3; j >= 1; --j) {
+            if (j < ni) {
+                float te = key_t(key[j]);
+                if (te <= wk.far) {
+                    wk.stk_code[wk.sp] = pick(kids, key[j] & 3);
+                    wk.stk_t[wk.sp] = te;
+                    ++wk.sp;
+                }
+            }
+        }
+    } else {
+        int k = __ffs(im) - 1;
+        key[0] = key[k];
+    }
+    if (key_t(key[0]) <= wk.far) return pick(kids, key[0] & 3);
+    return wk.pop(ct);
+}
+
+
 // ---------------------------------------------------------------------------
-// camera rays: one pass of render_stochastic (kernels.py:644-656)
+// ray sources
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void tile_pixel(const RenderArgs &a, int64_t lt, int tid, int &px, int &py) {
     int64_t gt = lt * a.shard_count + a.shard_index;
@@ -142,148 +260,665 @@ __device__ __forceinline__ void tile_pixel(const RenderArgs &a, int64_t lt, int 
     py = ty * 16 + (w >> 1) * 4 + (lane >> 3);
 }
 
-template <int NS, int MODE>
-__global__ void __launch_bounds__(256) k_trace_pass(SceneView s, CamD cam, RenderArgs a, int pass, int32_t *hits,
-                                                    int *overflow) {
-    int64_t lt = blockIdx.x;
-    int px, py;
-    tile_pixel(a, lt, threadIdx.x, px, py);
-    int64_t slot_base = (lt * 256 + threadIdx.x) * a.nslots;
-    if (px >= a.width || py >= a.height) return;
-    double dx, dy, dz;
-    camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)pass, a.seed, a.width, a.height, dx, dy, dz);
+struct CameraSource {
+    static constexpr bool kCoherent = true;  // neighbouring indices = neighbouring pixels
+    CamD cam;
+    RenderArgs a;
+    int pass;
+    uint32_t fkey;
+    int32_t *hits;
+    __host__ __device__ __forceinline__ uint32_t total() const { return (uint32_t)(a.local_tiles * 256); }
+    template <int NS>
+    __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
+        int px, py;
+        tile_pixel(a, idx >> 8, idx & 255, px, py);
+        if (px >= a.width || py >= a.height) return false;
+        double dx, dy, dz;
+        camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)pass, a.seed, a.width, a.height, dx, dy, dz);
+        init_ray(r, cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX);
+        init_slots<NS>(sl, a.nslots);
+        uint32_t ray_id = (uint32_t)py * (uint32_t)a.width + (uint32_t)px;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, (uint32_t)pass * (uint32_t)a.nslots + k);
+        return true;
+    }
+    template <int NS>
+    __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
+        int32_t *h = hits + (int64_t)idx * a.nslots;
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            if (k < a.nslots) h[k] = sl.id[k];
+    }
+};
+
+struct ArraySource {
+    static constexpr bool kCoherent = false;
+    const double *rays;  // (R, 6)
+    uint32_t R;
+    double t_min, t_max;
+    int nslots;
+    uint32_t fkey, ray_id0, sample0;
+    float *out_t;
+    int32_t *out_id;
+    __host__ __device__ __forceinline__ uint32_t total() const { return R; }
+    template <int NS>
+    __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
+        const double *q = rays + (int64_t)idx * 6;
+        init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+        init_slots<NS>(sl, nslots);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id0 + idx, sample0 + (uint32_t)k);
+        return true;
+    }
+    template <int NS>
+    __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+            if (k < nslots) {
+                out_t[(int64_t)idx * nslots + k] = sl.id[k] >= 0 ? sl.t[k] : INFINITY;
+                out_id[(int64_t)idx * nslots + k] = sl.id[k];
+            }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// persistent kernel
+// ---------------------------------------------------------------------------
+constexpr int kTraceThreads = 128;
+
+// REFILL: refill a warp once this many lanes are idle (32 = whole-warp
+// granularity).
+template <int NS, int MODE, int RNG, class Src, int REFILL, bool STATS>
+__global__ void __launch_bounds__(kTraceThreads) k_trace(SceneView s, Src src, WalkCfg w, uint32_t *work,
+                                                          int *overflow, unsigned long long *stats) {
+    Counters<STATS> ct;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t total = src.total();
     RayState r;
-    init_ray(r, cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX);
     Slots<NS> sl;
-    init_slots<NS>(sl, a.nslots);
-    uint32_t fk = frame_key(a.seed);
-    uint32_t ray_id = (uint32_t)py * (uint32_t)a.width + (uint32_t)px;
-#pragma unroll
-    for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fk, ray_id, (uint32_t)pass * (uint32_t)a.nslots + k);
-    walk<NS, MODE, SRT_RNG_COUNTER>(s, r, a.s2, a.clip, sl, nullptr, 0, overflow);
-#pragma unroll
-    for (int k = 0; k < NS; ++k)
-        if (k < a.nslots) hits[slot_base + k] = sl.id[k];
+    Walk wk;
+    bool active = false;
+    bool exhausted = false;
+    uint32_t idx = 0;
+    while (true) {
+        unsigned idle = __ballot_sync(FULL, !active);
+        if (!exhausted && __popc(idle) >= REFILL) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(work, (uint32_t)__popc(idle));
+            base = __shfl_sync(FULL, base, 0);
+            if (base + (uint32_t)__popc(idle) >= total) exhausted = true;
+            if (!active) {
+                uint32_t my = base + (uint32_t)__popc(idle & ((1u << lane) - 1u));
+                if (my < total && src.template init<NS>(my, r, sl)) {
+                    idx = my;
+                    active = true;
+                    wk.sp = 0;
+                    wk.far = r.t_max0;
+                    wk.next = s.num_nodes4 > 0 ? 0 : kDone;
+                }
+            }
+        } else if (exhausted && idle == FULL) {
+            ct.flush(stats);
+            break;
+        }
+        if (active) {
+            // one node visit per round, so finished lanes are refilled while
+            // the rest of the warp keeps walking
+            if (wk.next >= 0) wk.next = visit_node<NS, MODE, RNG, STATS>(s, r, w, wk, sl, wk.next, overflow, ct);
+            if (wk.next < 0) {
+                ct.add(7, 1);
+                src.template finish<NS>(idx, sl);
+                active = false;
+            }
+        }
+    }
 }
 
-template <int NS, int MODE>
-static void launch_trace_pass_t(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
-                                cudaStream_t st) {
-    if (a.local_tiles <= 0) return;
-    k_trace_pass<NS, MODE><<<(unsigned)a.local_tiles, 256, 0, st>>>(s->view(), cam, a, pass, d_hits, s->d_flag);
+// ---------------------------------------------------------------------------
+// Warp-cooperative kernel.  Each lane walks its own ray through the inner
+// nodes, but leaf work is compacted across the warp: every round, the hit
+// leaf children of all 32 lanes go into a warp queue in shared memory and
+// are screened by all 32 lanes together (ballot/prefix-sum compaction), with
+// the owner's ray read from shared memory.  Slot updates are 64-bit
+// shared-memory atomicMin of (orderable t, prim id): the closest accepted
+// hit, ties to the smaller id -- exactly the order-free semantics of
+// kernels.py:353-357.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long pack_hit(float t, int pid) {
+    unsigned u = __float_as_uint(t);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)u << 32) | (unsigned)pid;
+}
+__device__ __forceinline__ float unpack_t(unsigned long long v) {
+    unsigned u = (unsigned)(v >> 32);
+    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    return __uint_as_float(u);
+}
+
+template <int NS, int MODE, int RNG, bool STATS>
+__device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, const WalkCfg &w, int slot,
+                                         unsigned long long *best, const uint32_t *keys, float far,
+                                         Counters<STATS> &ct) {
+    ct.add(1, 1);
+    const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+    float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+    Screen sc = screen<MODE>(r, m, a, b, w.s2, far);
+    if (!sc.maybe) return;
+    ct.add(2, 1);
+    int pid = __float_as_int(b.z);
+    bool need = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+        if (sc.t_lo <= unpack_t(best[k])) {
+            float u = RNG == SRT_RNG_TABLE ? (float)__ldg(w.table + (int64_t)pid * w.tstride + k)
+                                           : counter_u(keys[k], (uint32_t)pid);
+            need |= u <= sc.alpha_hi;
+        }
+    }
+    if (!need) return;
+    ct.add(3, 1);
+    Cand c = candidate<MODE>(r, m, a, b, w.s2);
+    if (!c.valid) return;
+    unsigned long long key = pack_hit(c.t, pid);
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        if (key < best[k] && accepts<RNG>(keys[k], w.table, w.tstride, pid, k, c.alpha)) {
+            atomicMin(best + k, key);
+            ct.add(4, 1);
+        }
+}
+
+// Inner children of a visited node: descend into the nearest hit one, push
+// the others far-to-near.  Returns the next node (or a popped one).
+template <bool STATS>
+__device__ __forceinline__ int descend(Walk &wk, const int4 &kids, int key[4], unsigned im, float &next_t,
+                                       int *overflow, Counters<STATS> &ct) {
+    if (!im) {
+        int n = wk.pop(ct);
+        next_t = wk.popped_t;
+        return n;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (!(im & (1u << k))) key[k] = 0x7FFFFFFF;
+    int ni = __popc(im);
+    if (ni > 1) {
+#define SRT_CX(a, b)                      \
+    {                                     \
+        int lo_ = min(key[a], key[b]);    \
+        int hi_ = max(key[a], key[b]);    \
+        key[a] = lo_;                     \
+        key[b] = hi_;                     \
+    }
+        SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
+#undef SRT_CX
+        if (wk.sp + ni - 1 > kStackSize) {
+            atomicExch(overflow, 1);
+            wk.sp = 0;
+            return kDone;
+        }
+#pragma unroll
+        for (int j = 3; j >= 1; --j) {
+            if (j < ni) {
+                wk.stk_code[wk.sp] = pick(kids, key[j] & 3);
+                wk.stk_t[wk.sp] = key_t(key[j]);
+                ++wk.sp;
+            }
+        }
+    } else {
+        key[0] = key[__ffs(im) - 1];
+    }
+    next_t = key_t(key[0]);
+    return pick(kids, key[0] & 3);
+}
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+__global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src src, WalkCfg w, uint32_t *work,
+                                                               int *overflow, unsigned long long *stats) {
+    constexpr int W = kTraceThreads / 32;
+    __shared__ RayState sray[W][32];
+    __shared__ unsigned long long sbest[W][32][NS];
+    __shared__ uint32_t skey[W][32][NS];
+    __shared__ float sfar[W][32];
+    __shared__ int sjob[W][128];
+    __shared__ unsigned char sown[W][128];
+    const unsigned FULL = 0xffffffffu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t total = src.total();
+    Counters<STATS> ct;
+    RayState r;
+    Slots<NS> sl;
+    Walk wk;
+    float next_t = 0.f;
+    bool active = false;
+    bool exhausted = false;
+    uint32_t idx = 0;
+    while (true) {
+        unsigned idle = __ballot_sync(FULL, !active);
+        if (idle == FULL) {
+            if (exhausted) break;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(work, 32u);
+            base = __shfl_sync(FULL, base, 0);
+            if (base + 32u >= total) exhausted = true;
+            uint32_t my = base + (uint32_t)lane;
+            if (my < total && src.template init<NS>(my, r, sl)) {
+                idx = my;
+                active = true;
+                wk.sp = 0;
+                wk.far = r.t_max0;
+                wk.next = s.num_nodes4 > 0 ? 0 : kDone;
+                next_t = r.t_min;
+                sray[wid][lane] = r;
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    sbest[wid][lane][k] = pack_hit(sl.t[k], -1);
+                    skey[wid][lane][k] = sl.key[k];
+                }
+            }
+            if (__ballot_sync(FULL, active) == 0) continue;
+        }
+        // ---- inner traversal step (per lane) ----
+        unsigned lm = 0;
+        int4 kids = make_int4(kDone, kDone, kDone, kDone);
+        if (active && wk.next >= 0) {
+            ct.add(0, 1);
+            int key[4];
+            unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + wk.next), wk.far, kids, key);
+            unsigned leafm = (kids.x < 0 ? 1u : 0u) | (kids.y < 0 ? 2u : 0u) | (kids.z < 0 ? 4u : 0u) |
+                             (kids.w < 0 ? 8u : 0u);
+            lm = hitm & leafm;
+            wk.next = descend<STATS>(wk, kids, key, hitm & ~leafm, next_t, overflow, ct);
+        }
+        // ---- warp-compacted leaf jobs ----
+        int cnt = __popc(lm);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int njobs = __shfl_sync(FULL, incl, 31);
+        if (njobs) {
+            int off = incl - cnt;
+            if (lm & 1u) { sjob[wid][off] = ~kids.x; sown[wid][off] = (unsigned char)lane; ++off; }
+            if (lm & 2u) { sjob[wid][off] = ~kids.y; sown[wid][off] = (unsigned char)lane; ++off; }
+            if (lm & 4u) { sjob[wid][off] = ~kids.z; sown[wid][off] = (unsigned char)lane; ++off; }
+            if (lm & 8u) { sjob[wid][off] = ~kids.w; sown[wid][off] = (unsigned char)lane; ++off; }
+            sfar[wid][lane] = wk.far;
+            __syncwarp();
+            for (int jb = 0; jb < njobs; jb += 32) {
+                int j = jb + lane;
+                if (j < njobs) {
+                    int o = sown[wid][j];
+                    leaf_job<NS, MODE, RNG, STATS>(s, sray[wid][o], w, sjob[wid][j], sbest[wid][o], skey[wid][o],
+                                                    sfar[wid][o], ct);
+                }
+            }
+            __syncwarp();
+            if (active && w.clip) {
+                // clip to the farthest slot once every slot holds a hit (kernels.py:358-364)
+                float worst = unpack_t(sbest[wid][lane][0]);
+#pragma unroll
+                for (int k = 1; k < NS; ++k) worst = fmaxf(worst, unpack_t(sbest[wid][lane][k]));
+                wk.far = fminf(wk.far, worst);
+            }
+        }
+        if (active) {
+            if (wk.next >= 0 && next_t > wk.far) {
+                wk.next = wk.pop(ct);
+                next_t = wk.popped_t;
+            }
+            if (wk.next < 0) {
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                    unsigned long long v = sbest[wid][lane][k];
+                    sl.id[k] = (int)(unsigned)v;
+                    sl.t[k] = unpack_t(v);
+                }
+                src.template finish<NS>(idx, sl);
+                ct.add(7, 1);
+                active = false;
+            }
+        }
+    }
+    ct.flush(stats);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-packet kernel (camera rays): the 32 rays of an 8x4 pixel block walk
+// the tree TOGETHER.  Node addresses, the stack and the visit order are
+// warp-uniform (one 128-B node fetch serves the warp); every lane slab-tests
+// the node's children against its own ray and far bound; the warp descends
+// into every child that any lane hits, nearest (warp-min entry) first, and
+// culls a popped node when its warp-min entry lies beyond every lane's far.
+// Leaf work is compacted across the warp exactly as in k_trace_coop.
+// ---------------------------------------------------------------------------
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+__global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
+                                                                 int *overflow, unsigned long long *stats) {
+    constexpr int W = kTraceThreads / 32;
+    constexpr int PSTACK = 64;
+    __shared__ RayState sray[W][32];
+    __shared__ unsigned long long sbest[W][32][NS];
+    __shared__ uint32_t skey[W][32][NS];
+    __shared__ float sfar[W][32];
+    __shared__ int sjob[W][128];
+    __shared__ unsigned char sown[W][128];
+    __shared__ int sstk_node[W][PSTACK];
+    __shared__ int sstk_key[W][PSTACK];
+    const unsigned FULL = 0xffffffffu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t total = src.total();
+    Counters<STATS> ct;
+    RayState r;
+    Slots<NS> sl;
+    while (true) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(work, 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= total) break;
+        uint32_t idx = base + (uint32_t)lane;
+        bool valid = idx < total && src.template init<NS>(idx, r, sl);
+        float far;
+        if (valid) {
+            far = r.t_max0;
+            sray[wid][lane] = r;
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                sbest[wid][lane][k] = pack_hit(sl.t[k], -1);
+                skey[wid][lane][k] = sl.key[k];
+            }
+            ct.add(7, 1);
+        } else {
+            init_ray(r, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
+            far = -INFINITY;  // hits nothing
+        }
+        int sp = 0;
+        int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
+        while (node != kDone) {
+            if (lane == 0) ct.add(0, 1);
+            int4 kids;
+            int key[4];
+            unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
+            unsigned leafm = (kids.x < 0 ? 1u : 0u) | (kids.y < 0 ? 2u : 0u) | (kids.z < 0 ? 4u : 0u) |
+                             (kids.w < 0 ? 8u : 0u);
+            unsigned lm = hitm & leafm;
+            // ---- leaf jobs of the whole warp ----
+            int cnt = __popc(lm);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            int njobs = __shfl_sync(FULL, incl, 31);
+            if (njobs) {
+                int off = incl - cnt;
+                if (lm & 1u) { sjob[wid][off] = ~kids.x; sown[wid][off] = (unsigned char)lane; ++off; }
+                if (lm & 2u) { sjob[wid][off] = ~kids.y; sown[wid][off] = (unsigned char)lane; ++off; }
+                if (lm & 4u) { sjob[wid][off] = ~kids.z; sown[wid][off] = (unsigned char)lane; ++off; }
+                if (lm & 8u) { sjob[wid][off] = ~kids.w; sown[wid][off] = (unsigned char)lane; ++off; }
+                sfar[wid][lane] = far;
+                __syncwarp();
+                for (int jb = 0; jb < njobs; jb += 32) {
+                    int j = jb + lane;
+                    if (j < njobs) {
+                        int o = sown[wid][j];
+                        leaf_job<NS, MODE, RNG, STATS>(s, sray[wid][o], w, sjob[wid][j], sbest[wid][o],
+                                                        skey[wid][o], sfar[wid][o], ct);
+                    }
+                }
+                __syncwarp();
+                if (valid && w.clip) {
+                    // clip to the farthest slot once every slot holds a hit (kernels.py:358-364)
+                    float worst = unpack_t(sbest[wid][lane][0]);
+#pragma unroll
+                    for (int k = 1; k < NS; ++k) worst = fmaxf(worst, unpack_t(sbest[wid][lane][k]));
+                    far = fminf(far, worst);
+                }
+            }
+            // ---- inner children: warp-uniform order by the warp-min entry ----
+            unsigned im = hitm & ~leafm;
+            int wk[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) wk[k] = __reduce_min_sync(FULL, (im >> k) & 1u ? key[k] : 0x7FFFFFFF);
+            int nin = (wk[0] != 0x7FFFFFFF) + (wk[1] != 0x7FFFFFFF) + (wk[2] != 0x7FFFFFFF) + (wk[3] != 0x7FFFFFFF);
+            // warp-max far (orderable) for culling
+            int ofar = __float_as_int(far);
+            ofar = ofar >= 0 ? ofar : ofar ^ 0x7FFFFFFF;
+            int maxfar = __reduce_max_sync(FULL, ofar);
+            if (nin > 0) {
+#define SRT_CX(a, b)                    \
+    {                                   \
+        int lo_ = min(wk[a], wk[b]);    \
+        int hi_ = max(wk[a], wk[b]);    \
+        wk[a] = lo_;                    \
+        wk[b] = hi_;                    \
+    }
+                SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
+#undef SRT_CX
+                if (sp + nin - 1 > PSTACK) {
+                    if (lane == 0) atomicExch(overflow, 1);
+                    node = kDone;
+                    break;
+                }
+                for (int j = nin - 1; j >= 1; --j) {
+                    if (lane == 0) {
+                        sstk_node[wid][sp] = pick(kids, wk[j] & 3);
+                        sstk_key[wid][sp] = wk[j] & ~3;
+                    }
+                    ++sp;
+                }
+                node = pick(kids, wk[0] & 3);
+                if ((wk[0] & ~3) > maxfar) node = kDone;  // beyond every lane's far: pop instead
+            } else {
+                node = kDone;
+            }
+            if (node == kDone) {
+                __syncwarp();
+                while (sp > 0) {
+                    --sp;
+                    if (lane == 0) ct.add(5, 1);
+                    if (sstk_key[wid][sp] <= maxfar) {
+                        node = sstk_node[wid][sp];
+                        break;
+                    }
+                    if (lane == 0) ct.add(6, 1);
+                }
+            }
+            __syncwarp();
+        }
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k) {
+                unsigned long long v = sbest[wid][lane][k];
+                sl.id[k] = (int)(unsigned)v;
+                sl.t[k] = unpack_t(v);
+            }
+            src.template finish<NS>(idx, sl);
+        }
+        __syncwarp();
+    }
+    ct.flush(stats);
+}
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st);
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st);
+
+static int g_num_sms = 0;
+
+template <int NS, int MODE, int RNG, class Src, int REFILL, bool STATS>
+static srt_status launch_trace_v(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace<NS, MODE, RNG, Src, REFILL, STATS>,
+                                                      kTraceThreads, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    if (rc) return rc;
+    int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
+    int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
+    if (grid > need) grid = need;
+    k_trace<NS, MODE, RNG, Src, REFILL, STATS>
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+    return cuda_status(cudaGetLastError(), "k_trace launch");
+}
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace_coop<NS, MODE, RNG, Src, STATS>,
+                                                      kTraceThreads, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    if (rc) return rc;
+    int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
+    int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
+    if (grid > need) grid = need;
+    k_trace_coop<NS, MODE, RNG, Src, STATS>
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+    return cuda_status(cudaGetLastError(), "k_trace_coop launch");
+}
+
+// Traversal policy, env SRT_TRACE_VARIANT: 2 warp-cooperative leaf
+// compaction (default), 0 per-lane walk with whole-warp refill, 1 per-lane
+// walk with refill at 8 idle lanes; SRT_TRACE_STATS=1 enables counters.
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS>,
+                                                      kTraceThreads, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    if (rc) return rc;
+    int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
+    int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
+    if (grid > need) grid = need;
+    k_trace_packet<NS, MODE, RNG, Src, STATS>
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+    return cuda_status(cudaGetLastError(), "k_trace_packet launch");
+}
+
+template <int NS, int MODE, int RNG, class Src>
+static srt_status launch_trace_t(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+    if (src.total() == 0) return SRT_OK;
+    static const int variant = env_int("SRT_TRACE_VARIANT", 3);
+    static const bool stats = env_int("SRT_TRACE_STATS", 0) != 0 && s->d_stats;
+    if (variant == 3 && Src::kCoherent) {
+        if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
+        return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
+    }
+    if (variant == 2 || variant == 3) {
+        if (stats) return launch_trace_coop<NS, MODE, RNG, Src, true>(s, src, w, st);
+        return launch_trace_coop<NS, MODE, RNG, Src, false>(s, src, w, st);
+    }
+    if (stats) {
+        if (NS == 1 && variant == 1) return launch_trace_v<NS, MODE, RNG, Src, 8, true>(s, src, w, st);
+        return launch_trace_v<NS, MODE, RNG, Src, 32, true>(s, src, w, st);
+    }
+    if (NS == 1 && variant == 1) return launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st);
+    return launch_trace_v<NS, MODE, RNG, Src, 32, false>(s, src, w, st);
+}
+
+template <class Src, int RNG>
+static srt_status dispatch(const SrtScene *s, const Src &src, const WalkCfg &w, int nslots, int mode, cudaStream_t st) {
+#define SRT_NS(NS)                                                      \
+    return mode == 0 ? launch_trace_t<NS, 0, RNG, Src>(s, src, w, st)   \
+                     : launch_trace_t<NS, 1, RNG, Src>(s, src, w, st);
+    if (nslots <= 1) SRT_NS(1)
+    if (nslots <= 2) SRT_NS(2)
+    if (nslots <= 4) SRT_NS(4)
+    if (nslots <= 8) SRT_NS(8)
+    if (nslots <= 16) SRT_NS(16)
+#undef SRT_NS
+    set_error("nslots > 16 is not supported by the GPU tracer yet");
+    return SRT_ERR_UNSUPPORTED;
 }
 
 srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
                              cudaStream_t st) {
-#define SRT_DISPATCH_MODE(NS)                                               \
-    if (a.mode == 0)                                                        \
-        launch_trace_pass_t<NS, 0>(s, cam, a, pass, d_hits, st);            \
-    else                                                                    \
-        launch_trace_pass_t<NS, 1>(s, cam, a, pass, d_hits, st);
-    if (a.nslots <= 1) {
-        SRT_DISPATCH_MODE(1)
-    } else if (a.nslots <= 2) {
-        SRT_DISPATCH_MODE(2)
-    } else if (a.nslots <= 4) {
-        SRT_DISPATCH_MODE(4)
-    } else if (a.nslots <= 8) {
-        SRT_DISPATCH_MODE(8)
-    } else if (a.nslots <= 16) {
-        SRT_DISPATCH_MODE(16)
-    } else {
-        set_error("nslots > 16 is not supported by the GPU tracer yet");
-        return SRT_ERR_UNSUPPORTED;
+    CameraSource src;
+    src.cam = cam;
+    src.a = a;
+    src.pass = pass;
+    src.fkey = 0;
+    src.hits = d_hits;
+    // frame key computed on the host side of the device function (same mixer)
+    {
+        uint32_t x = a.seed ^ 0x9E3779B9u;
+        x ^= x >> 16;
+        x *= 0x7feb352du;
+        x ^= x >> 15;
+        x *= 0x846ca68bu;
+        x ^= x >> 16;
+        src.fkey = x;
     }
-#undef SRT_DISPATCH_MODE
-    return cuda_status(cudaGetLastError(), "k_trace_pass launch");
-}
-
-// ---------------------------------------------------------------------------
-// explicit rays (kernels.trace_batch, kernels.py:527-540)
-// ---------------------------------------------------------------------------
-struct TraceArgs {
-    double t_min, t_max;
-    float s2;
-    int clip, nslots;
-    uint32_t seed, ray_id0, sample0;
-    int64_t tstride;
-};
-
-template <int NS, int MODE, int RNG>
-__global__ void __launch_bounds__(128) k_trace_rays(SceneView s, TraceArgs a, const double *__restrict__ rays,
-                                                    int64_t R, const double *table, float *out_t, int32_t *out_id,
-                                                    int *overflow) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R) return;
-    const double *q = rays + i * 6;
-    RayState r;
-    init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], a.t_min, a.t_max);
-    Slots<NS> sl;
-    init_slots<NS>(sl, a.nslots);
-    uint32_t fk = frame_key(a.seed);
-#pragma unroll
-    for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fk, a.ray_id0 + (uint32_t)i, a.sample0 + (uint32_t)k);
-    walk<NS, MODE, RNG>(s, r, a.s2, a.clip, sl, table, a.tstride, overflow);
-#pragma unroll
-    for (int k = 0; k < NS; ++k)
-        if (k < a.nslots) {
-            out_t[i * a.nslots + k] = sl.id[k] >= 0 ? sl.t[k] : INFINITY;
-            out_id[i * a.nslots + k] = sl.id[k];
-        }
-}
-
-template <int NS>
-static void launch_rays_t(const SrtScene *s, const TraceArgs &ta, int mode, int rng, const double *d_rays, int64_t R,
-                          const double *d_table, float *d_t, int32_t *d_id, cudaStream_t st) {
-    unsigned blocks = (unsigned)((R + 127) / 128);
-    if (blocks == 0) return;
-    SceneView v = s->view();
-    if (rng == SRT_RNG_TABLE) {
-        if (mode == 0)
-            k_trace_rays<NS, 0, SRT_RNG_TABLE><<<blocks, 128, 0, st>>>(v, ta, d_rays, R, d_table, d_t, d_id, s->d_flag);
-        else
-            k_trace_rays<NS, 1, SRT_RNG_TABLE><<<blocks, 128, 0, st>>>(v, ta, d_rays, R, d_table, d_t, d_id, s->d_flag);
-    } else {
-        if (mode == 0)
-            k_trace_rays<NS, 0, SRT_RNG_COUNTER><<<blocks, 128, 0, st>>>(v, ta, d_rays, R, d_table, d_t, d_id, s->d_flag);
-        else
-            k_trace_rays<NS, 1, SRT_RNG_COUNTER><<<blocks, 128, 0, st>>>(v, ta, d_rays, R, d_table, d_t, d_id, s->d_flag);
-    }
+    WalkCfg w{a.s2, a.clip, nullptr, 0};
+    return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
 }
 
 srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int nslots,
                              const double *d_table, float *d_t, int32_t *d_id, cudaStream_t st) {
-    TraceArgs ta;
-    ta.t_min = p->t_min;
-    ta.t_max = p->t_max;
-    ta.s2 = (float)p->s2;
-    ta.clip = p->clip;
-    ta.nslots = nslots;
-    ta.seed = p->seed;
-    ta.ray_id0 = p->ray_id0;
-    ta.sample0 = p->sample0;
-    ta.tstride = p->table_slots;
-    if (nslots <= 1)
-        launch_rays_t<1>(s, ta, p->mode, p->rng, d_rays, R, d_table, d_t, d_id, st);
-    else if (nslots <= 2)
-        launch_rays_t<2>(s, ta, p->mode, p->rng, d_rays, R, d_table, d_t, d_id, st);
-    else if (nslots <= 4)
-        launch_rays_t<4>(s, ta, p->mode, p->rng, d_rays, R, d_table, d_t, d_id, st);
-    else if (nslots <= 8)
-        launch_rays_t<8>(s, ta, p->mode, p->rng, d_rays, R, d_table, d_t, d_id, st);
-    else if (nslots <= 16)
-        launch_rays_t<16>(s, ta, p->mode, p->rng, d_rays, R, d_table, d_t, d_id, st);
-    else {
-        set_error("nslots > 16 is not supported by the GPU tracer yet");
-        return SRT_ERR_UNSUPPORTED;
+    if (R > (int64_t)UINT32_MAX) {
+        set_error("too many rays in one call");
+        return SRT_ERR_INVALID_ARG;
     }
-    return cuda_status(cudaGetLastError(), "k_trace_rays launch");
+    ArraySource src;
+    src.rays = d_rays;
+    src.R = (uint32_t)R;
+    src.t_min = p->t_min;
+    src.t_max = p->t_max;
+    src.nslots = nslots;
+    uint32_t x = p->seed ^ 0x9E3779B9u;
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    src.fkey = x;
+    src.ray_id0 = p->ray_id0;
+    src.sample0 = p->sample0;
+    src.out_t = d_t;
+    src.out_id = d_id;
+    WalkCfg w{(float)p->s2, p->clip, d_table, p->table_slots};
+    if (p->rng == SRT_RNG_TABLE) return dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st);
+    return dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
 }
 
 // ---------------------------------------------------------------------------
 // transmittance: prod(1 - alpha) over every valid candidate, no clipping
-// (kernels.py:392-432).  Order of the product differs from the reference's
-// walk; the value agrees to product-reordering roundoff.
+// (kernels.py:392-432).  The product order differs from the reference's
+// walk; the value agrees to product-reordering roundoff (fp32 alphas).
 // ---------------------------------------------------------------------------
 template <int MODE>
 __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double *__restrict__ rays, int64_t R,
@@ -295,45 +930,32 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
     RayState r;
     init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
     double result = 1.0;
-    if (s.num_nodes > 0) {
-        int stk[kStackSize];
-        int sp = 0, cur = 0;
-        while (true) {
-            const float4 *np = reinterpret_cast<const float4 *>(s.nodes + cur);
-            float4 xy0 = __ldg(np), xy1 = __ldg(np + 1), z01 = __ldg(np + 2);
-            int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 3));
-            float e0, e1;
-            bool h0, h1;
-            slab2(r, xy0, xy1, z01, r.t_max0, e0, e1, h0, h1);
-            int cs[2] = {kids.x, kids.y};
-            bool hs[2] = {h0, h1};
-            int next = -1;
-            for (int c = 0; c < 2; ++c) {
-                if (!hs[c]) continue;
-                if (cs[c] < 0) {
-                    if (cs[c] == kLeafEmpty) continue;
-                    const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~cs[c]);
-                    float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
-                    Cand cd = candidate<MODE>(r, m, a, b, s2);
-                    if (cd.valid) result *= 1.0 - (double)cd.alpha;
-                } else if (next < 0) {
-                    next = cs[c];
-                } else {
-                    if (sp >= kStackSize) {
-                        atomicExch(overflow, 1);
-                        out[i] = result;
-                        return;
-                    }
-                    stk[sp++] = cs[c];
-                }
+    int stk[kStackSize];
+    int sp = 0;
+    int node = s.num_nodes4 > 0 ? 0 : kDone;
+    while (node != kDone) {
+        int4 kids;
+        int key[4];
+        unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), r.t_max0, kids, key);
+        node = kDone;
+        while (hitm) {
+            int k = __ffs(hitm) - 1;
+            hitm &= hitm - 1;
+            int code = pick(kids, k);
+            if (code < 0) {
+                const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~code);
+                float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+                Cand cd = candidate<MODE>(r, m, a, b, s2);
+                if (cd.valid) result *= 1.0 - (double)cd.alpha;
+            } else if (node == kDone) {
+                node = code;
+            } else if (sp < kStackSize) {
+                stk[sp++] = code;
+            } else {
+                atomicExch(overflow, 1);
             }
-            if (next >= 0) {
-                cur = next;
-                continue;
-            }
-            if (sp == 0) break;
-            cur = stk[--sp];
         }
+        if (node == kDone && sp > 0) node = stk[--sp];
     }
     out[i] = result;
 }

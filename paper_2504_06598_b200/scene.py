@@ -191,6 +191,14 @@ class DeviceScene:
                                      _ptr(ids)))
         return rgb, op, ids
 
+    def trace_stats(self, reset: bool = True) -> dict:
+        """Traversal counters (collected only when SRT_TRACE_STATS=1 was set)."""
+        out = np.zeros(8, np.uint64)
+        check(_lib.load().srt_trace_stats(self.handle, _ptr(out), int(bool(reset))))
+        names = ("node_visits", "leaf_visits", "screen_pass", "exact_evals", "accepts", "pops", "culled_pops",
+                 "walks")
+        return dict(zip(names, (int(v) for v in out)))
+
     # device-pointer variants (bench.py, multi_gpu.py); pointers are ints
     def trace_pass_device(self, camera, prm, pass_index, d_hits, stream) -> None:
         check(_lib.load().srt_trace_pass_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),

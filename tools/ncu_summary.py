@@ -1,0 +1,73 @@
+"""Summarise an ncu --set full report (+ optional launch-list CSV) into profiles/.
+
+    python tools/ncu_summary.py gpurun_out/prof_trace.ncu-rep gpurun_out/launches.csv profiles/r01_xxx
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
+    "l1tex__t_bytes.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+    "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "smsp__sass_average_branch_targets_threads_uniform.pct",
+]
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u = rows[0], rows[1]
+    kernels = []
+    for v in rows[2:]:
+        d = {"kernel": v[h.index("Kernel Name")]}
+        for i, name in enumerate(h):
+            if name in KEYS or name.startswith("smsp__average_warps_issue_stalled_") and name.endswith("_per_issue_active.ratio"):
+                d[name] = (v[i], u[i])
+        kernels.append(d)
+    return kernels
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[start]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = {}
+    for r in rows[start + 1:]:
+        name = r[ki].split("(")[0]
+        agg.setdefault(name, []).append(float(r[vi]))
+    total = sum(sum(v) for v in agg.values())
+    return {k: {"launches": len(v), "total_ns": sum(v), "share": sum(v) / total} for k, v in
+            sorted(agg.items(), key=lambda kv: -sum(kv[1]))}
+
+
+def main():
+    rep, lcsv, outdir = sys.argv[1], sys.argv[2], Path(sys.argv[3])
+    outdir.mkdir(parents=True, exist_ok=True)
+    summary = {"full": raw(rep)}
+    if lcsv != "-":
+        summary["launch_list"] = launches(lcsv)
+    (outdir / "ncu_summary.json").write_text(json.dumps(summary, indent=1))
+    lines = []
+    for k in summary["full"]:
+        lines.append(f"== {k['kernel'][:100]}")
+        for name, (val, unit) in sorted((n, v) for n, v in k.items() if n != "kernel"):
+            lines.append(f"  {name:75s} {val:>16s} {unit}")
+    if "launch_list" in summary:
+        lines.append("== launch list (ncu --metrics gpu__time_duration.sum, cold, serialised)")
+        for name, d in summary["launch_list"].items():
+            lines.append(f"  {name[:70]:70s} n={d['launches']:3d} total={d['total_ns']/1e3:10.1f} us share={d['share']:.3f}")
+    (outdir / "ncu_summary.txt").write_text("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
