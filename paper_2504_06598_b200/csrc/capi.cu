@@ -358,7 +358,10 @@ srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const d
                 int pi = (int)p;
                 float pf;
                 std::memcpy(&pf, &pi, sizeof(pf));
-                gg.b = make_float4((float)hc[p * 6 + 4], (float)hc[p * 6 + 5], pf, 0.f);
+                const double *cc = &hc[p * 6];
+                double tr = std::fabs(cc[0]) + std::fabs(cc[3]) + std::fabs(cc[5]) +
+                            2.0 * (std::fabs(cc[1]) + std::fabs(cc[2]) + std::fabs(cc[4]));
+                gg.b = make_float4((float)cc[4], (float)cc[5], pf, (float)(std::sqrt(tr) * 1.0000002));
             }
             rc = cuda_status(cudaMalloc(&s->d_geom, sizeof(Geom) * n), "geom alloc");
             if (!rc) rc = cuda_status(cudaMemcpy(s->d_geom, geom.data(), sizeof(Geom) * n, cudaMemcpyHostToDevice), "geom upload");

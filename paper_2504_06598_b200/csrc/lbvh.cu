@@ -228,7 +228,8 @@ __global__ void k_geom(int64_t n, const uint32_t *__restrict__ slot_prim, const 
     g.m = make_float4((float)means[p * 3], (float)means[p * 3 + 1], (float)means[p * 3 + 2], (float)opac[p]);
     const double *c = cov6 + p * 6;
     g.a = make_float4((float)c[0], (float)c[1], (float)c[2], (float)c[3]);
-    g.b = make_float4((float)c[4], (float)c[5], __int_as_float((int)p), 0.f);
+    double tr = fabs(c[0]) + fabs(c[3]) + fabs(c[5]) + 2.0 * (fabs(c[1]) + fabs(c[2]) + fabs(c[4]));
+    g.b = make_float4((float)c[4], (float)c[5], __int_as_float((int)p), (float)(sqrt(tr) * 1.0000002));
     geom[j] = g;
 }
 

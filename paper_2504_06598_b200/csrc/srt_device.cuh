@@ -37,7 +37,7 @@ struct __align__(128) Node4 {
 struct __align__(16) Geom {
     float4 m;  // mean.xyz, opacity
     float4 a;  // a00 a01 a02 a11
-    float4 b;  // a12 a22, prim id (int bits), pad
+    float4 b;  // a12 a22, prim id (int bits), sqrt(sum |a_ij|) (screen error bound)
 };
 
 struct SceneView {
@@ -254,7 +254,7 @@ struct Screen {
 
 template <int MODE>
 __device__ __forceinline__ Screen screen(const RayState &r, const float4 &m, const float4 &a, const float4 &b,
-                                         float s2, float far) {
+                                         float s2, float sqrt_s2, float far) {
     Screen sc;
     float vx = m.x - r.fox, vy = m.y - r.foy, vz = m.z - r.foz;
     float tc = vx * r.fdx + vy * r.fdy + vz * r.fdz;
@@ -270,14 +270,16 @@ __device__ __forceinline__ Screen screen(const RayState &r, const float4 &m, con
     float awz = a02 * wx + a12 * wy + a22 * wz;
     float daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
     float waw = wx * awx + wy * awy + wz * awz;
-    float inv_dad = 1.0f / dad;
+    float rs = rsqrtf(dad);
+    float inv_dad = rs * rs;
     float resid = waw - daw * daw * inv_dad;
     float mah, t;
-    // absolute error of w: roundings of |o|, |mu|, |t0|-sized terms
-    float mmag = fmaxf(fabsf(m.x), fmaxf(fabsf(m.y), fabsf(m.z)));
-    float e = 4.0e-7f * (fabsf(t0) + r.omag + mmag) + 1e-30f;
-    float tr = fabsf(a00) + fabsf(a11) + fabsf(a22) + 2.0f * (fabsf(a01) + fabsf(a02) + fabsf(a12));
-    float mr = 4.0f * sqrtf(s2 * tr) * e + 4.0f * tr * e * e + 2.0e-5f * (fabsf(waw) + 1e-6f);
+    // absolute error of w: roundings of |o|-, |mu|- and |t0|-sized terms
+    // (|mu| <= |mu - o| + |o|); sqrt_tr = sqrt(sum |a_ij|) bounds sqrt(lambda_max)
+    float sqrt_tr = b.w;
+    float e = 4.0e-7f * (fabsf(t0) + 2.0f * r.omag + fabsf(vx) + fabsf(vy) + fabsf(vz)) + 1e-30f;
+    float es = e * sqrt_tr;
+    float mr = es * (4.0f * sqrt_s2 + 4.0f * es) + 2.0e-5f * (fabsf(waw) + 1e-6f);
     if (MODE == 0) {
         t = t0 - daw * inv_dad;
         mah = resid;
@@ -289,7 +291,7 @@ __device__ __forceinline__ Screen screen(const RayState &r, const float4 &m, con
               qz * (a02 * qx + a12 * qy + a22 * qz);
         mr += 2.0e-5f * fabsf(mah);
     }
-    float mt = e * (1.0f + sqrtf(fmaxf(tr * inv_dad, 0.0f))) + 2.0e-6f * (fabsf(t) + 1.0f);
+    float mt = e + es * rs + 2.0e-6f * (fabsf(t) + 1.0f);
     sc.t_lo = t - mt;
     sc.maybe = (dad > 0.0f) && (mah - mr <= s2) && (t - mt <= far) && (t + mt > r.t_min) && (t - mt < r.t_max0);
     sc.alpha_hi = m.w * __expf(-0.5f * fmaxf(resid - mr, 0.0f)) * 1.0001f + 1e-7f;

@@ -15,6 +15,7 @@
 // That keeps the expensive candidate code (kernels.py:139-189 + the
 // acceptance draw) executing with most lanes converged.
 #include <cfloat>
+#include <cmath>
 #include <cstdlib>
 
 #include "srt_internal.h"
@@ -50,6 +51,7 @@ __device__ __forceinline__ bool accepts(uint32_t key, const double *table, int64
 
 struct WalkCfg {
     float s2;
+    float sqrt_s2;
     int clip;
     const double *table;
     int64_t tstride;
@@ -81,7 +83,7 @@ __device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
     float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
     // stage 1: fp32 screen -- can this candidate be accepted by any slot?
-    Screen sc = screen<MODE>(r, m, a, b, w.s2, far);
+    Screen sc = screen<MODE>(r, m, a, b, w.s2, w.sqrt_s2, far);
     if (!sc.maybe) return;
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
@@ -164,6 +166,7 @@ struct Walk {
 // Slab test of the 4 children of a node against [t_min, far] (closed,
 // kernels.py:266-308): bit k of the result is set when child k is hit;
 // key[k] = entry distance (orderable int) with k in the low 2 bits.
+template <bool NONNEG = false>
 __device__ __forceinline__ unsigned slab4(const RayState &r, const float4 *np, float far, int4 &kids, int key[4]) {
     float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3), loz = __ldg(np + 4),
            hiz = __ldg(np + 5);
@@ -182,7 +185,7 @@ __device__ __forceinline__ unsigned slab4(const RayState &r, const float4 *np, f
         // empty slots carry inverted boxes, which min/max slab tests would see
         // as infinite: mask them by code
         bool hit = tn <= tf && pick(kids, k) != kLeafEmpty;
-        key[k] = ordered_key(tn, k);
+        key[k] = NONNEG ? ((__float_as_int(tn) & ~3) | k) : ordered_key(tn, k);
         hitm |= hit ? (1u << k) : 0u;
     }
     return hitm;
@@ -403,7 +406,7 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
     ct.add(1, 1);
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
     float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
-    Screen sc = screen<MODE>(r, m, a, b, w.s2, far);
+    Screen sc = screen<MODE>(r, m, a, b, w.s2, w.sqrt_s2, far);
     if (!sc.maybe) return;
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
@@ -641,25 +644,22 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             if (lane == 0) ct.add(0, 1);
             int4 kids;
             int key[4];
-            unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
+            unsigned hitm = slab4<true>(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
+            // node address and child codes are warp-uniform
             unsigned leafm = (kids.x < 0 ? 1u : 0u) | (kids.y < 0 ? 2u : 0u) | (kids.z < 0 ? 4u : 0u) |
                              (kids.w < 0 ? 8u : 0u);
             unsigned lm = hitm & leafm;
-            // ---- leaf jobs of the whole warp ----
-            int cnt = __popc(lm);
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            int njobs = __shfl_sync(FULL, incl, 31);
+            // ---- leaf jobs of the whole warp: ballot compaction ----
+            const unsigned lt = (1u << lane) - 1u;
+            unsigned b0 = __ballot_sync(FULL, lm & 1u), b1 = __ballot_sync(FULL, lm & 2u);
+            unsigned b2 = __ballot_sync(FULL, lm & 4u), b3 = __ballot_sync(FULL, lm & 8u);
+            int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
+            int njobs = n0 + n1 + n2 + n3;
             if (njobs) {
-                int off = incl - cnt;
-                if (lm & 1u) { sjob[wid][off] = ~kids.x; sown[wid][off] = (unsigned char)lane; ++off; }
-                if (lm & 2u) { sjob[wid][off] = ~kids.y; sown[wid][off] = (unsigned char)lane; ++off; }
-                if (lm & 4u) { sjob[wid][off] = ~kids.z; sown[wid][off] = (unsigned char)lane; ++off; }
-                if (lm & 8u) { sjob[wid][off] = ~kids.w; sown[wid][off] = (unsigned char)lane; ++off; }
+                if (lm & 1u) { int o = __popc(b0 & lt); sjob[wid][o] = ~kids.x; sown[wid][o] = (unsigned char)lane; }
+                if (lm & 2u) { int o = n0 + __popc(b1 & lt); sjob[wid][o] = ~kids.y; sown[wid][o] = (unsigned char)lane; }
+                if (lm & 4u) { int o = n0 + n1 + __popc(b2 & lt); sjob[wid][o] = ~kids.z; sown[wid][o] = (unsigned char)lane; }
+                if (lm & 8u) { int o = n0 + n1 + n2 + __popc(b3 & lt); sjob[wid][o] = ~kids.w; sown[wid][o] = (unsigned char)lane; }
                 sfar[wid][lane] = far;
                 __syncwarp();
                 for (int jb = 0; jb < njobs; jb += 32) {
@@ -883,7 +883,7 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
         x ^= x >> 16;
         src.fkey = x;
     }
-    WalkCfg w{a.s2, a.clip, nullptr, 0};
+    WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
     return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
 }
 
@@ -910,7 +910,7 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     src.sample0 = p->sample0;
     src.out_t = d_t;
     src.out_id = d_id;
-    WalkCfg w{(float)p->s2, p->clip, d_table, p->table_slots};
+    WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
     if (p->rng == SRT_RNG_TABLE) return dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st);
     return dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
 }
