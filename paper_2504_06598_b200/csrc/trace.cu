@@ -645,21 +645,31 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             int4 kids;
             int key[4];
             unsigned hitm = slab4<true>(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
-            // node address and child codes are warp-uniform
-            unsigned leafm = (kids.x < 0 ? 1u : 0u) | (kids.y < 0 ? 2u : 0u) | (kids.z < 0 ? 4u : 0u) |
-                             (kids.w < 0 ? 8u : 0u);
-            unsigned lm = hitm & leafm;
-            // ---- leaf jobs of the whole warp: ballot compaction ----
+            // Child codes are warp-uniform, so leaf/inner is a uniform branch per
+            // child: one collective each (ballot for leaves, min-reduce for inner).
             const unsigned lt = (1u << lane) - 1u;
-            unsigned b0 = __ballot_sync(FULL, lm & 1u), b1 = __ballot_sync(FULL, lm & 2u);
-            unsigned b2 = __ballot_sync(FULL, lm & 4u), b3 = __ballot_sync(FULL, lm & 8u);
-            int n0 = __popc(b0), n1 = __popc(b1), n2 = __popc(b2), n3 = __popc(b3);
-            int njobs = n0 + n1 + n2 + n3;
+            int wkey[4];
+            int njobs = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int code = pick(kids, k);
+                bool h = (hitm >> k) & 1u;
+                wkey[k] = 0x7FFFFFFF;
+                if (code == kLeafEmpty) continue;
+                if (code < 0) {
+                    unsigned bm = __ballot_sync(FULL, h);
+                    if (h) {
+                        int o = njobs + __popc(bm & lt);
+                        sjob[wid][o] = ~code;
+                        sown[wid][o] = (unsigned char)lane;
+                    }
+                    njobs += __popc(bm);
+                } else {
+                    wkey[k] = __reduce_min_sync(FULL, h ? key[k] : 0x7FFFFFFF);
+                }
+            }
+            // ---- leaf jobs of the whole warp ----
             if (njobs) {
-                if (lm & 1u) { int o = __popc(b0 & lt); sjob[wid][o] = ~kids.x; sown[wid][o] = (unsigned char)lane; }
-                if (lm & 2u) { int o = n0 + __popc(b1 & lt); sjob[wid][o] = ~kids.y; sown[wid][o] = (unsigned char)lane; }
-                if (lm & 4u) { int o = n0 + n1 + __popc(b2 & lt); sjob[wid][o] = ~kids.z; sown[wid][o] = (unsigned char)lane; }
-                if (lm & 8u) { int o = n0 + n1 + n2 + __popc(b3 & lt); sjob[wid][o] = ~kids.w; sown[wid][o] = (unsigned char)lane; }
                 sfar[wid][lane] = far;
                 __syncwarp();
                 for (int jb = 0; jb < njobs; jb += 32) {
@@ -680,43 +690,37 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
                 }
             }
             // ---- inner children: warp-uniform order by the warp-min entry ----
-            unsigned im = hitm & ~leafm;
-            int wk[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) wk[k] = __reduce_min_sync(FULL, (im >> k) & 1u ? key[k] : 0x7FFFFFFF);
-            int nin = (wk[0] != 0x7FFFFFFF) + (wk[1] != 0x7FFFFFFF) + (wk[2] != 0x7FFFFFFF) + (wk[3] != 0x7FFFFFFF);
-            // warp-max far (orderable) for culling
-            int ofar = __float_as_int(far);
-            ofar = ofar >= 0 ? ofar : ofar ^ 0x7FFFFFFF;
-            int maxfar = __reduce_max_sync(FULL, ofar);
+            int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
+                      (wkey[3] != 0x7FFFFFFF);
+            node = kDone;
             if (nin > 0) {
-#define SRT_CX(a, b)                    \
-    {                                   \
-        int lo_ = min(wk[a], wk[b]);    \
-        int hi_ = max(wk[a], wk[b]);    \
-        wk[a] = lo_;                    \
-        wk[b] = hi_;                    \
+#define SRT_CX(a, b)                      \
+    {                                     \
+        int lo_ = min(wkey[a], wkey[b]);  \
+        int hi_ = max(wkey[a], wkey[b]);  \
+        wkey[a] = lo_;                    \
+        wkey[b] = hi_;                    \
     }
                 SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
 #undef SRT_CX
                 if (sp + nin - 1 > PSTACK) {
                     if (lane == 0) atomicExch(overflow, 1);
-                    node = kDone;
                     break;
                 }
-                for (int j = nin - 1; j >= 1; --j) {
-                    if (lane == 0) {
-                        sstk_node[wid][sp] = pick(kids, wk[j] & 3);
-                        sstk_key[wid][sp] = wk[j] & ~3;
-                    }
-                    ++sp;
+                if (lane == 0) {
+#pragma unroll
+                    for (int j = 3; j >= 1; --j)
+                        if (j < nin) {
+                            sstk_node[wid][sp + nin - 1 - j] = pick(kids, wkey[j] & 3);
+                            sstk_key[wid][sp + nin - 1 - j] = wkey[j] & ~3;
+                        }
                 }
-                node = pick(kids, wk[0] & 3);
-                if ((wk[0] & ~3) > maxfar) node = kDone;  // beyond every lane's far: pop instead
-            } else {
-                node = kDone;
+                sp += nin - 1;
+                node = pick(kids, wkey[0] & 3);
             }
-            if (node == kDone) {
+            if (node == kDone && sp > 0) {
+                // pop, culling entries beyond every lane's far bound
+                int maxfar = __reduce_max_sync(FULL, __float_as_int(far));  // far >= 0 or -inf (done lanes)
                 __syncwarp();
                 while (sp > 0) {
                     --sp;
