@@ -203,8 +203,8 @@ struct Cand {
     int valid;
 };
 
-template <int MODE>
-__device__ __forceinline__ Cand candidate(const RayState &r, const float4 &m, const float4 &a, const float4 &b,
+template <int MODE, class R>
+__device__ __forceinline__ Cand candidate(const R &r, const float4 &m, const float4 &a, const float4 &b,
                                           float s2) {
     Cand c;
     double vx = (double)m.x - r.ox, vy = (double)m.y - r.oy, vz = (double)m.z - r.oz;  // mu - o
@@ -252,8 +252,16 @@ struct Screen {
     bool maybe;      // could be a valid candidate inside (t_min, far]
 };
 
-template <int MODE>
-__device__ __forceinline__ Screen screen(const RayState &r, const float4 &m, const float4 &a, const float4 &b,
+// Minimal fp32 ray for the screen (camera rays share one origin).
+struct ScreenRay {
+    float fox, foy, foz, omag;
+    float fdx, fdy, fdz;
+    double inv_dd;
+    float t_min, t_max0;
+};
+
+template <int MODE, class R>
+__device__ __forceinline__ Screen screen(const R &r, const float4 &m, const float4 &a, const float4 &b,
                                          float s2, float sqrt_s2, float far) {
     Screen sc;
     float vx = m.x - r.fox, vy = m.y - r.foy, vz = m.z - r.foz;

@@ -432,6 +432,39 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
         }
 }
 
+// Leaf job of the packet kernel: screen on the owner's fp32 direction and
+// the shared camera origin; the exact fp64 stage rebuilds the owner's ray
+// from its fp64 direction only when the screen cannot decide.
+template <int NS, int MODE, bool STATS>
+__device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, const ScreenRay &sr, const double *dd,
+                                           const WalkCfg &w, int slot, unsigned long long *best,
+                                           const uint32_t *keys, float far, Counters<STATS> &ct) {
+    ct.add(1, 1);
+    const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+    float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+    Screen sc = screen<MODE>(sr, m, a, b, w.s2, w.sqrt_s2, far);
+    if (!sc.maybe) return;
+    ct.add(2, 1);
+    int pid = __float_as_int(b.z);
+    bool need = false;
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        if (sc.t_lo <= unpack_t(best[k])) need |= counter_u(keys[k], (uint32_t)pid) <= sc.alpha_hi;
+    if (!need) return;
+    ct.add(3, 1);
+    RayState r;
+    init_ray(r, cam.e[0], cam.e[1], cam.e[2], dd[0], dd[1], dd[2], 0.0, DBL_MAX);
+    Cand c = candidate<MODE>(r, m, a, b, w.s2);
+    if (!c.valid) return;
+    unsigned long long key = pack_hit(c.t, pid);
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+        if (key < best[k] && counter_u(keys[k], (uint32_t)pid) < c.alpha) {
+            atomicMin(best + k, key);
+            ct.add(4, 1);
+        }
+}
+
 // Inner children of a visited node: descend into the nearest hit one, push
 // the others far-to-near.  Returns the next node (or a popped one).
 template <bool STATS>
@@ -603,10 +636,10 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
                                                                  int *overflow, unsigned long long *stats) {
     constexpr int W = kTraceThreads / 32;
     constexpr int PSTACK = 64;
-    __shared__ RayState sray[W][32];
+    __shared__ float4 sdir[W][32];      // fp32 direction + far bound of each lane's ray
+    __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
     __shared__ unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
-    __shared__ float sfar[W][32];
     __shared__ int sjob[W][128];
     __shared__ unsigned char sown[W][128];
     __shared__ int sstk_node[W][PSTACK];
@@ -614,6 +647,8 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t total = src.total();
+    const float cfox = (float)src.cam.e[0], cfoy = (float)src.cam.e[1], cfoz = (float)src.cam.e[2];
+    const float comag = fmaxf(fabsf(cfox), fmaxf(fabsf(cfoy), fabsf(cfoz)));
     Counters<STATS> ct;
     RayState r;
     Slots<NS> sl;
@@ -627,7 +662,9 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
         float far;
         if (valid) {
             far = r.t_max0;
-            sray[wid][lane] = r;
+            sdd[wid][lane][0] = r.dx;
+            sdd[wid][lane][1] = r.dy;
+            sdd[wid][lane][2] = r.dz;
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
                 sbest[wid][lane][k] = pack_hit(sl.t[k], -1);
@@ -670,14 +707,21 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             }
             // ---- leaf jobs of the whole warp ----
             if (njobs) {
-                sfar[wid][lane] = far;
+                sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
                 __syncwarp();
                 for (int jb = 0; jb < njobs; jb += 32) {
                     int j = jb + lane;
                     if (j < njobs) {
                         int o = sown[wid][j];
-                        leaf_job<NS, MODE, RNG, STATS>(s, sray[wid][o], w, sjob[wid][j], sbest[wid][o],
-                                                        skey[wid][o], sfar[wid][o], ct);
+                        float4 dv = sdir[wid][o];
+                        ScreenRay sr;
+                        sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
+                        sr.fdx = dv.x; sr.fdy = dv.y; sr.fdz = dv.z;
+                        sr.inv_dd = 1.0;  // camera directions are unit in fp64
+                        sr.t_min = 0.0f;
+                        sr.t_max0 = INFINITY;
+                        packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
+                                                    skey[wid][o], dv.w, ct);
                     }
                 }
                 __syncwarp();
@@ -838,9 +882,11 @@ static srt_status launch_trace_t(const SrtScene *s, const Src &src, const WalkCf
     if (src.total() == 0) return SRT_OK;
     static const int variant = env_int("SRT_TRACE_VARIANT", 3);
     static const bool stats = env_int("SRT_TRACE_STATS", 0) != 0 && s->d_stats;
-    if (variant == 3 && Src::kCoherent) {
-        if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
-        return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
+    if constexpr (Src::kCoherent) {
+        if (variant == 3) {
+            if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
+            return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
+        }
     }
     if (variant == 2 || variant == 3) {
         if (stats) return launch_trace_coop<NS, MODE, RNG, Src, true>(s, src, w, st);
