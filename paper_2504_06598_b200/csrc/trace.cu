@@ -640,8 +640,8 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
     __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
     __shared__ unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
-    __shared__ int sjob[W][128];
-    __shared__ unsigned char sown[W][128];
+    __shared__ int sjob[W][160];
+    __shared__ unsigned char sown[W][160];
     __shared__ int sstk_node[W][PSTACK];
     __shared__ int sstk_key[W][PSTACK];
     const unsigned FULL = 0xffffffffu;
@@ -676,7 +676,36 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             far = -INFINITY;  // hits nothing
         }
         int sp = 0;
+        int njobs = 0;  // leaf jobs queued for the warp (processed in batches of >= 32)
         int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
+        auto run_jobs = [&]() {
+            sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
+            __syncwarp();
+            for (int jb = 0; jb < njobs; jb += 32) {
+                int j = jb + lane;
+                if (j < njobs) {
+                    int o = sown[wid][j];
+                    float4 dv = sdir[wid][o];
+                    ScreenRay sr;
+                    sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
+                    sr.fdx = dv.x; sr.fdy = dv.y; sr.fdz = dv.z;
+                    sr.inv_dd = 1.0;  // camera directions are unit in fp64
+                    sr.t_min = 0.0f;
+                    sr.t_max0 = INFINITY;
+                    packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
+                                                skey[wid][o], dv.w, ct);
+                }
+            }
+            __syncwarp();
+            njobs = 0;
+            if (valid && w.clip) {
+                // clip to the farthest slot once every slot holds a hit (kernels.py:358-364)
+                float worst = unpack_t(sbest[wid][lane][0]);
+#pragma unroll
+                for (int k = 1; k < NS; ++k) worst = fmaxf(worst, unpack_t(sbest[wid][lane][k]));
+                far = fminf(far, worst);
+            }
+        };
         while (node != kDone) {
             if (lane == 0) ct.add(0, 1);
             int4 kids;
@@ -686,7 +715,6 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             // child: one collective each (ballot for leaves, min-reduce for inner).
             const unsigned lt = (1u << lane) - 1u;
             int wkey[4];
-            int njobs = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 int code = pick(kids, k);
@@ -705,34 +733,9 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
                     wkey[k] = __reduce_min_sync(FULL, h ? key[k] : 0x7FFFFFFF);
                 }
             }
-            // ---- leaf jobs of the whole warp ----
-            if (njobs) {
-                sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
-                __syncwarp();
-                for (int jb = 0; jb < njobs; jb += 32) {
-                    int j = jb + lane;
-                    if (j < njobs) {
-                        int o = sown[wid][j];
-                        float4 dv = sdir[wid][o];
-                        ScreenRay sr;
-                        sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
-                        sr.fdx = dv.x; sr.fdy = dv.y; sr.fdz = dv.z;
-                        sr.inv_dd = 1.0;  // camera directions are unit in fp64
-                        sr.t_min = 0.0f;
-                        sr.t_max0 = INFINITY;
-                        packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
-                                                    skey[wid][o], dv.w, ct);
-                    }
-                }
-                __syncwarp();
-                if (valid && w.clip) {
-                    // clip to the farthest slot once every slot holds a hit (kernels.py:358-364)
-                    float worst = unpack_t(sbest[wid][lane][0]);
-#pragma unroll
-                    for (int k = 1; k < NS; ++k) worst = fmaxf(worst, unpack_t(sbest[wid][lane][k]));
-                    far = fminf(far, worst);
-                }
-            }
+            // leaf jobs run in batches: deferring them a node or two only delays
+            // the far-bound clip, never changes a result (order-free acceptance)
+            if (njobs >= 32) run_jobs();
             // ---- inner children: warp-uniform order by the warp-min entry ----
             int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
                       (wkey[3] != 0x7FFFFFFF);
@@ -762,18 +765,22 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
                 sp += nin - 1;
                 node = pick(kids, wkey[0] & 3);
             }
-            if (node == kDone && sp > 0) {
-                // pop, culling entries beyond every lane's far bound
-                int maxfar = __reduce_max_sync(FULL, __float_as_int(far));  // far >= 0 or -inf (done lanes)
-                __syncwarp();
-                while (sp > 0) {
-                    --sp;
-                    if (lane == 0) ct.add(5, 1);
-                    if (sstk_key[wid][sp] <= maxfar) {
-                        node = sstk_node[wid][sp];
-                        break;
+            if (node == kDone) {
+                if (sp == 0 && njobs) run_jobs();
+                if (sp > 0) {
+                    // pop, culling entries beyond every lane's far bound
+                    int maxfar = __reduce_max_sync(FULL, __float_as_int(far));  // far >= 0, or -inf when idle
+                    __syncwarp();
+                    while (sp > 0) {
+                        --sp;
+                        if (lane == 0) ct.add(5, 1);
+                        if (sstk_key[wid][sp] <= maxfar) {
+                            node = sstk_node[wid][sp];
+                            break;
+                        }
+                        if (lane == 0) ct.add(6, 1);
                     }
-                    if (lane == 0) ct.add(6, 1);
+                    if (node == kDone && njobs) run_jobs();
                 }
             }
             __syncwarp();
