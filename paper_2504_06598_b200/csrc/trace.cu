@@ -631,17 +631,19 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
 // culls a popped node when its warp-min entry lies beyond every lane's far.
 // Leaf work is compacted across the warp exactly as in k_trace_coop.
 // ---------------------------------------------------------------------------
-template <int NS, int MODE, int RNG, class Src, bool STATS>
-__global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
-                                                                 int *overflow, unsigned long long *stats) {
+// BATCH: leaf jobs are run once at least BATCH are queued; MINB: minimum
+// resident blocks per SM requested from the register allocator.
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1>
+__global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
+                                                                       int *overflow, unsigned long long *stats) {
     constexpr int W = kTraceThreads / 32;
     constexpr int PSTACK = 64;
     __shared__ float4 sdir[W][32];      // fp32 direction + far bound of each lane's ray
     __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
     __shared__ unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
-    __shared__ int sjob[W][160];
-    __shared__ unsigned char sown[W][160];
+    __shared__ int sjob[W][BATCH + 128];
+    __shared__ unsigned char sown[W][BATCH + 128];
     __shared__ int sstk_node[W][PSTACK];
     __shared__ int sstk_key[W][PSTACK];
     const unsigned FULL = 0xffffffffu;
@@ -735,7 +737,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_packet(SceneView s, Src
             }
             // leaf jobs run in batches: deferring them a node or two only delays
             // the far-bound clip, never changes a result (order-free acceptance)
-            if (njobs >= 32) run_jobs();
+            if (njobs >= BATCH) run_jobs();
             // ---- inner children: warp-uniform order by the warp-min entry ----
             int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
                       (wkey[3] != 0x7FFFFFFF);
@@ -861,12 +863,12 @@ static int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int NS, int MODE, int RNG, class Src, bool STATS>
-static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH, int MINB>
+static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS>,
-                                                      kTraceThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>, kTraceThreads, 0);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     if (!g_num_sms) {
@@ -879,9 +881,24 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
-    k_trace_packet<NS, MODE, RNG, Src, STATS>
+    k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>
         <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
+}
+
+static int env_int(const char *name, int dflt);
+
+template <int NS, int MODE, int RNG, class Src, bool STATS>
+static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
+    // SRT_PACKET_CFG (experiments, N=1 mean-depth only): 0 batch 32 (default),
+    // 1 batch 64, 2 batch 32 + 8 blocks/SM, 3 batch 64 + 8 blocks/SM
+    static const int cfg = env_int("SRT_PACKET_CFG", 0);
+    if constexpr (NS == 1 && MODE == 0 && !STATS) {
+        if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
+        if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8>(s, src, w, st);
+        if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
+    }
+    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1>(s, src, w, st);
 }
 
 template <int NS, int MODE, int RNG, class Src>

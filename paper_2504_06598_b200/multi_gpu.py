@@ -1,0 +1,230 @@
+"""Multi-GPU frame driver: one process per GPU, scene replicated, work sharded,
+one NCCL collective per frame.
+
+Two shardings, both with no exchange during tracing:
+
+* ``"tiles"``   16x16 tiles interleaved over ranks (tile t -> rank t % G).
+  Interleaving balances the dense centre of the cloud against the empty
+  border.  Each rank writes its tiles into a tile-compact buffer
+  ``(max_tiles * 256, 4)``; rank 0 gathers the G buffers with one
+  ``torch.distributed.gather`` (NCCL over NVLink) and scatters them into the
+  frame (``srt_unpack_tiles_device`` on the GPU).
+* ``"samples"`` passes split into contiguous ranges (rank r traces passes
+  [P r / G, P (r + 1) / G)).  The counter RNG is keyed on the GLOBAL pass
+  index, so every sample is the one the single-GPU render draws.  Rank 0
+  gathers the per-rank partial means and combines them in rank order (a
+  fixed-order sum, so the result does not depend on NCCL's reduction order).
+
+The host-side bookkeeping (tile ownership, pixel order of the compact layout,
+pass ranges, assembly) is plain numpy here so it can be exercised with the
+gloo backend on CPU; the GPU path swaps in libsrt kernels for the per-rank
+trace and the unpack.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+TILE = 16
+
+
+# ---------------------------------------------------------------------------
+# host-side bookkeeping (mirrors tile_pixel in csrc/trace.cu / shade.cu)
+# ---------------------------------------------------------------------------
+
+def tiles_xy(width: int, height: int) -> tuple[int, int]:
+    return (width + TILE - 1) // TILE, (height + TILE - 1) // TILE
+
+
+def shard_tile_ids(width: int, height: int, rank: int, world: int) -> np.ndarray:
+    """Global 16x16 tile ids owned by `rank` (t % world == rank), in local order."""
+    tx, ty = tiles_xy(width, height)
+    return np.arange(rank, tx * ty, world, dtype=np.int64)
+
+
+def max_shard_tiles(width: int, height: int, world: int) -> int:
+    return len(shard_tile_ids(width, height, 0, world))
+
+
+def compact_pixels(width: int, height: int, rank: int, world: int):
+    """(px, py, valid) of each entry of the rank's tile-compact buffer: local
+    tile j covers entries [256 j, 256 j + 256); inside a tile, warp w holds an
+    8x4 block at ((w & 1) * 8, (w >> 1) * 4) and lane l its pixel (l & 7, l >> 3)."""
+    tx, _ = tiles_xy(width, height)
+    tiles = shard_tile_ids(width, height, rank, world)
+    tid = np.arange(256)
+    w, lane = tid >> 5, tid & 31
+    ox = (w & 1) * 8 + (lane & 7)
+    oy = (w >> 1) * 4 + (lane >> 3)
+    px = ((tiles % tx) * TILE)[:, None] + ox[None, :]
+    py = ((tiles // tx) * TILE)[:, None] + oy[None, :]
+    px, py = px.reshape(-1), py.reshape(-1)
+    return px, py, (px < width) & (py < height)
+
+
+def assemble_tiles(gathered: list, width: int, height: int) -> np.ndarray:
+    """Scatter G tile-compact (n, 4) buffers into a (H, W, 4) frame (CPU
+    statement of srt_unpack_tiles_device)."""
+    world = len(gathered)
+    frame = np.zeros((height, width, 4), np.float32)
+    for r, buf in enumerate(gathered):
+        px, py, ok = compact_pixels(width, height, r, world)
+        b = np.asarray(buf, np.float32).reshape(-1, 4)[: px.shape[0]]
+        frame[py[ok], px[ok]] = b[ok]
+    return frame
+
+
+def pass_range(passes: int, rank: int, world: int) -> tuple[int, int]:
+    """[first, last) global pass indices of `rank` under sample sharding."""
+    return passes * rank // world, passes * (rank + 1) // world
+
+
+def combine_samples(gathered_means: list, pass_counts: list) -> np.ndarray:
+    """Fixed-order combination of per-rank partial means (weights = passes)."""
+    total = float(sum(pass_counts))
+    acc = np.zeros_like(np.asarray(gathered_means[0], np.float64))
+    for m, c in zip(gathered_means, pass_counts):
+        if c:
+            acc += np.asarray(m, np.float64) * c
+    return acc / total
+
+
+# ---------------------------------------------------------------------------
+# the driver
+# ---------------------------------------------------------------------------
+
+@dataclass
+class ShardPlan:
+    mode: str
+    rank: int
+    world: int
+    width: int
+    height: int
+    passes: int
+
+    @property
+    def pass0(self) -> int:
+        return pass_range(self.passes, self.rank, self.world)[0] if self.mode == "samples" else 0
+
+    @property
+    def local_passes(self) -> int:
+        if self.mode == "samples":
+            a, b = pass_range(self.passes, self.rank, self.world)
+            return b - a
+        return self.passes
+
+    @property
+    def buffer_pixels(self) -> int:
+        if self.mode == "samples":
+            return self.width * self.height
+        return max_shard_tiles(self.width, self.height, self.world) * 256
+
+
+def plan(mode: str, rank: int, world: int, width: int, height: int, passes: int) -> ShardPlan:
+    if mode not in ("tiles", "samples"):
+        raise ValueError(f"unknown sharding {mode!r}")
+    return ShardPlan(mode, rank, world, width, height, passes)
+
+
+def render_frame(p: ShardPlan, shard_render: Callable, group=None, device=None):
+    """Run one sharded frame.
+
+    ``shard_render(plan) -> torch.Tensor (buffer_pixels, 4) float32`` renders
+    the rank's share (tile-compact means for "tiles", row-major when there is
+    a single rank; a full frame of partial means over its pass range for
+    "samples").  Returns the (H, W, 4) float32
+    frame on rank 0 and None elsewhere.  One ``gather`` per frame.
+    """
+    import torch
+    import torch.distributed as dist
+
+    local = shard_render(p)
+    if p.world == 1:
+        # a single rank renders the whole frame row-major (no compact layout)
+        return local.reshape(-1)[: p.height * p.width * 4].reshape(p.height, p.width, 4)
+    else:
+        gathered = [torch.empty_like(local) for _ in range(p.world)] if p.rank == 0 else None
+        dist.gather(local, gathered, dst=0, group=group)
+    if p.rank != 0:
+        return None
+    if p.mode == "tiles":
+        if local.is_cuda:
+            from .scene import unpack_tiles_device
+
+            packed = torch.cat([g.reshape(-1) for g in gathered])
+            frame = torch.zeros(p.height * p.width * 4, dtype=torch.float32, device=local.device)
+            unpack_tiles_device(packed.data_ptr(), p.width, p.height, p.world,
+                                max_shard_tiles(p.width, p.height, p.world), frame.data_ptr(),
+                                torch.cuda.current_stream(local.device).cuda_stream)
+            return frame.reshape(p.height, p.width, 4)
+        return torch.from_numpy(assemble_tiles([g.numpy() for g in gathered], p.width, p.height))
+    counts = [pass_range(p.passes, r, p.world)[1] - pass_range(p.passes, r, p.world)[0] for r in range(p.world)]
+    if local.is_cuda:
+        acc = torch.zeros_like(local, dtype=torch.float64)
+        for g, c in zip(gathered, counts):  # fixed rank order
+            if c:
+                acc += g.double() * c
+        return (acc / float(sum(counts))).float().reshape(p.height, p.width, 4)
+    return torch.from_numpy(combine_samples([g.numpy() for g in gathered], counts).astype(np.float32)).reshape(
+        p.height, p.width, 4)
+
+
+def gpu_shard_renderer(scene, camera_tuple, settings, device):
+    """shard_render callback tracing the rank's share with libsrt on `device`."""
+    import torch
+
+    from .scene import make_camera, make_render_params
+
+    cam = make_camera(camera_tuple)
+    mode = 0 if settings.depth_mode == "mean" else 1
+
+    def run(p: ShardPlan):
+        dev = torch.device("cuda", device)
+        if p.mode == "tiles":
+            prm = make_render_params(p.width, p.height, p.passes, settings.multisample, mode,
+                                     settings.cutoff_s ** 2, True, settings.seed, settings.background,
+                                     0, p.rank, p.world)
+        else:
+            prm = make_render_params(p.width, p.height, max(p.local_passes, 1), settings.multisample, mode,
+                                     settings.cutoff_s ** 2, True, settings.seed, settings.background, p.pass0)
+        from .scene import shard_tiles
+
+        n = max(p.buffer_pixels, p.width * p.height if p.world == 1 else 0)
+        out = torch.zeros((n, 4), dtype=torch.float32, device=dev)
+        if p.mode == "samples" and p.local_passes == 0:
+            return out
+        # trace scratch in the tile-compact layout of the traced tiles
+        tiles = shard_tiles(p.width, p.height, p.rank, p.world) if p.mode == "tiles" else shard_tiles(p.width, p.height)
+        hits = torch.empty(max(tiles, 1) * 256 * settings.multisample, dtype=torch.int32, device=dev)
+        acc = torch.empty((max(tiles, 1) * 256, 4), dtype=torch.float32, device=dev)
+        scene.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(),
+                            torch.cuda.current_stream(dev).cuda_stream)
+        return out
+
+    return run
+
+
+def render_distributed(asset, camera, settings, mode: str = "tiles", group=None, device: int | None = None):
+    """Drop-in multi-GPU render: call on every rank of an initialised process
+    group (NCCL).  Returns the AccumBuffer on rank 0, None on the others."""
+    import torch
+    import torch.distributed as dist
+
+    from .render import AccumBuffer, prepare
+    from .scene import camera_tuple
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if device is None:
+        device = torch.cuda.current_device()
+    sc = prepare(asset, settings, device=device)
+    ct = camera_tuple(camera, settings.width, settings.height)
+    p = plan(mode, rank, world, settings.width, settings.height, settings.passes)
+    frame = render_frame(p, gpu_shard_renderer(sc, ct, settings, device), group)
+    if frame is None:
+        return None
+    f = frame.double().cpu().numpy()
+    return AccumBuffer(f[..., :3], f[..., 3], settings.samples_per_pixel)

@@ -306,3 +306,20 @@ def test_errors_are_loud():
         sc.render((0,) * 14, 0, 10)
     with pytest.raises(ValueError):
         DeviceScene(np.zeros((2, 3)), np.zeros((3, 6)), np.zeros(2))
+
+
+@pytest.mark.parametrize("mode", ["tiles", "samples"])
+def test_render_distributed_single_rank_equals_render(mode):
+    """multi_gpu.render_distributed without a process group (one rank) is the
+    plain render() frame."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.multi_gpu import render_distributed
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(4_000, seed=8, sh_degree=2)
+    st = RenderSettings(width=50, height=34, spp=6, multisample=2, seed=4)
+    got = render_distributed(a, front_camera(), st, mode=mode)
+    want = render(a, front_camera(), st)
+    np.testing.assert_allclose(got.rgb, want.rgb, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(got.opacity, want.opacity, rtol=1e-6, atol=1e-6)
+    assert got.spp == want.spp

@@ -1,0 +1,122 @@
+"""Multi-GPU driver host logic (paper_2504_06598_b200/multi_gpu.py), run on CPU:
+tile ownership, compact-buffer pixel order, pass ranges, assembly, and a
+world_size-2 gloo run of the same gather the NCCL path does.  The per-rank
+renderer here is the CPU oracle (checker), standing in for libsrt."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import S2
+from paper_2504_06598_b200 import multi_gpu as mg
+
+
+@pytest.mark.parametrize("w,h,world", [(64, 64, 2), (70, 50, 3), (1920, 1080, 8), (17, 5, 4)])
+def test_tiles_partition_the_frame(w, h, world):
+    seen = np.zeros((h, w), np.int64)
+    for r in range(world):
+        px, py, ok = mg.compact_pixels(w, h, r, world)
+        assert px.shape[0] <= mg.max_shard_tiles(w, h, world) * 256
+        np.add.at(seen, (py[ok], px[ok]), 1)
+    assert np.all(seen == 1)
+
+
+def test_assemble_roundtrip():
+    rs = np.random.default_rng(0)
+    w, h, world = 70, 50, 3
+    frame = rs.random((h, w, 4)).astype(np.float32)
+    bufs = []
+    n = mg.max_shard_tiles(w, h, world) * 256
+    for r in range(world):
+        px, py, ok = mg.compact_pixels(w, h, r, world)
+        b = np.zeros((n, 4), np.float32)
+        b[: px.shape[0]][ok] = frame[py[ok], px[ok]]
+        bufs.append(b)
+    np.testing.assert_array_equal(mg.assemble_tiles(bufs, w, h), frame)
+
+
+def test_pass_ranges_and_combine():
+    for passes in (1, 7, 1024):
+        for world in (1, 2, 3, 8):
+            rngs = [mg.pass_range(passes, r, world) for r in range(world)]
+            assert rngs[0][0] == 0 and rngs[-1][1] == passes
+            assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+    means = [np.full(3, 1.0), np.full(3, 4.0)]
+    np.testing.assert_allclose(mg.combine_samples(means, [1, 3]), np.full(3, 3.25))
+    with pytest.raises(ValueError):
+        mg.plan("rows", 0, 1, 4, 4, 1)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, mode, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2504_06598_b200.synthetic import front_camera, random_cloud
+
+        asset = random_cloud(800, seed=4, sh_degree=1)
+        pk = asset.packed
+        lo, hi = asset.aabb_arrays(np.sqrt(S2))
+        b = O.sah_build(lo, hi)
+        w, h, passes = 40, 24, 5
+        cam = front_camera()
+        ct = O.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, w, h)
+
+        def shard_render(p):
+            if p.mode == "tiles" and p.world == 1:
+                full = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=passes, s2=S2,
+                                seed=3, rng="counter")
+                return torch.from_numpy(np.dstack([full["rgb"], full["opacity"]]).astype(np.float32).reshape(-1, 4))
+            if p.mode == "tiles":
+                full = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=passes, s2=S2,
+                                seed=3, rng="counter")
+                rgba = np.dstack([full["rgb"], full["opacity"]]).astype(np.float32)
+                px, py, ok = mg.compact_pixels(w, h, p.rank, p.world)
+                buf = np.zeros((p.buffer_pixels, 4), np.float32)
+                buf[: px.shape[0]][ok] = rgba[py[ok], px[ok]]
+                return torch.from_numpy(buf)
+            part = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=p.local_passes,
+                            pass0=p.pass0, s2=S2, seed=3, rng="counter")
+            return torch.from_numpy(np.dstack([part["rgb"], part["opacity"]]).astype(np.float32).reshape(-1, 4))
+
+        p = mg.plan(mode, rank, world, w, h, passes)
+        frame = mg.render_frame(p, shard_render)
+        if rank == 0:
+            ref = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=passes, s2=S2, seed=3,
+                           rng="counter")
+            want = np.dstack([ref["rgb"], ref["opacity"]])
+            q.put(float(np.abs(frame.numpy() - want).max()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["tiles", "samples"])
+def test_gloo_world2_gather_matches_single_render(mode):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+        assert pr.exitcode == 0
+    err = q.get(timeout=5)
+    assert err <= 1e-6, err
