@@ -280,7 +280,7 @@ def run_ours(args) -> None:
                "h2d_bytes_per_step": 192, "d2h_bytes_per_step": int(buf.rgb.nbytes + buf.opacity.nbytes),
                "ms_per_frame": statistics.median(e2e_t) * 1e3,
                "path": "paper_2504_06598_b200.render() -> srt_render (C ABI): trace+shade+fp64 resolve on the GPU, "
-                       "AccumBuffer (H,W,3)+(H,W) float64 copied to pageable host memory; h2d = camera + settings "
+                       "AccumBuffer (H,W,3)+(H,W) float64 copied into pooled page-locked host memory; h2d = camera + settings "
                        "kernel parameters (SrtCamera 112 B + SrtRenderParams 80 B), scene resident"}
 
     cpu = None

@@ -95,6 +95,11 @@ const char *srt_last_error(void);      /* thread-local message of the last failu
 const char *srt_version(void);
 int32_t srt_device_count(void);
 
+/* Page-locked host memory (cudaHostAlloc) for host outputs: device->host
+ * copies into it run at full link speed.  srt_host_free releases it. */
+srt_status srt_host_alloc(int64_t bytes, void **out);
+srt_status srt_host_free(void *ptr);
+
 /* ---- scene ------------------------------------------------------------- */
 /* Upload a packed scene to `device` (fp32 SoA records in HBM). */
 srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene **out);

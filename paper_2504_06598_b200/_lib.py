@@ -61,6 +61,8 @@ SYMBOLS = [
     ("srt_last_error", ctypes.c_char_p, []),
     ("srt_version", ctypes.c_char_p, []),
     ("srt_device_count", _i32, []),
+    ("srt_host_alloc", _i32, [_i64, ctypes.POINTER(_vp)]),
+    ("srt_host_free", _i32, [_vp]),
     ("srt_scene_create", _i32, [ctypes.POINTER(SrtSceneDesc), _i32, ctypes.POINTER(_vp)]),
     ("srt_scene_destroy", _i32, [_vp]),
     ("srt_bvh_build", _i32, [_vp, _f64]),

@@ -137,6 +137,20 @@ int32_t srt_device_count(void) {
     return n;
 }
 
+srt_status srt_host_alloc(int64_t bytes, void **out) {
+    if (!out || bytes < 0) {
+        set_error("invalid host allocation");
+        return SRT_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    return cuda_status(cudaHostAlloc(out, (size_t)(bytes ? bytes : 1), cudaHostAllocPortable), "cudaHostAlloc");
+}
+
+srt_status srt_host_free(void *ptr) {
+    if (!ptr) return SRT_OK;
+    return cuda_status(cudaFreeHost(ptr), "cudaFreeHost");
+}
+
 srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene **out) {
     if (!desc || !out || desc->n < 0 || desc->sh_degree < 0 || desc->sh_degree > 3 ||
         (desc->n > 0 && (!desc->means || !desc->cov_inv6 || !desc->opacities))) {

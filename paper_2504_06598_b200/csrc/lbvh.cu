@@ -466,7 +466,33 @@ __global__ void k_collapse4(const Node2 *__restrict__ n2, const int2 *__restrict
     o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
     o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
     o.kids = make_int4(kids[0], kids[1], kids[2], kids[3]);
-    o.pad = make_int4(cnt, 0, 0, 0);
+    // traversal hints: valid / leaf child masks and, for each of the 8 ray
+    // direction octants, the children ordered near-to-far along that octant's
+    // diagonal (2 bits per child, 8 bits per octant)
+    unsigned validm = 0, leafm = 0;
+    float ctr[4][3];
+    for (int k = 0; k < 4; ++k) {
+        if (kids[k] != kLeafEmpty) validm |= 1u << k;
+        if (kids[k] < 0 && kids[k] != kLeafEmpty) leafm |= 1u << k;
+        for (int a = 0; a < 3; ++a) ctr[k][a] = 0.5f * (lo[a][k] + hi[a][k]);
+    }
+    unsigned ord[2] = {0, 0};
+    for (int oc = 0; oc < 8; ++oc) {
+        float dir[3] = {(oc & 1) ? -1.f : 1.f, (oc & 2) ? -1.f : 1.f, (oc & 4) ? -1.f : 1.f};
+        float key[4];
+        int idx[4] = {0, 1, 2, 3};
+        for (int k = 0; k < 4; ++k)
+            key[k] = (validm >> k) & 1u ? ctr[k][0] * dir[0] + ctr[k][1] * dir[1] + ctr[k][2] * dir[2] : 3.0e38f;
+        for (int i = 1; i < 4; ++i)  // insertion sort of 4
+            for (int j = i; j > 0 && key[idx[j]] < key[idx[j - 1]]; --j) {
+                int t = idx[j];
+                idx[j] = idx[j - 1];
+                idx[j - 1] = t;
+            }
+        unsigned byte = idx[0] | (idx[1] << 2) | (idx[2] << 4) | (idx[3] << 6);
+        ord[oc >> 2] |= byte << ((oc & 3) * 8);
+    }
+    o.pad = make_int4((int)(validm | (leafm << 4)), (int)ord[0], (int)ord[1], cnt);
     n4[w.y] = o;
 }
 

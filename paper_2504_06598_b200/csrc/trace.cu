@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
 // ---------------------------------------------------------------------------
 // BATCH: leaf jobs are run once at least BATCH are queued; MINB: minimum
 // resident blocks per SM requested from the register allocator.
-template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1>
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1, int ORDER = 1>
 __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
                                                                        int *overflow, unsigned long long *stats) {
     constexpr int W = kTraceThreads / 32;
@@ -679,6 +679,14 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
         }
         int sp = 0;
         int njobs = 0;  // leaf jobs queued for the warp (processed in batches of >= 32)
+        int oct = 0;    // direction octant of the packet (child order hint)
+        {
+            unsigned vm = __ballot_sync(FULL, valid);
+            int rep = vm ? __ffs(vm) - 1 : 0;
+            float ex = __shfl_sync(FULL, r.fdx, rep), ey = __shfl_sync(FULL, r.fdy, rep),
+                  ez = __shfl_sync(FULL, r.fdz, rep);
+            oct = (ex < 0.f ? 1 : 0) | (ey < 0.f ? 2 : 0) | (ez < 0.f ? 4 : 0);
+        }
         int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
         auto run_jobs = [&]() {
             sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
@@ -712,10 +720,57 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             if (lane == 0) ct.add(0, 1);
             int4 kids;
             int key[4];
-            unsigned hitm = slab4<true>(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
+            const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
+            unsigned hitm = slab4<true>(r, np, far, kids, key);
+            const unsigned lt = (1u << lane) - 1u;
+            node = kDone;
+            if (ORDER == 1) {
+                // octant order precomputed per node (lbvh.cu): one OR-reduce gives the
+                // children any lane hits; leaves are compacted, inner children pushed
+                // far-to-near along the packet's direction octant
+                int4 hint = __ldg(reinterpret_cast<const int4 *>(np + 7));
+                unsigned anyhit = __reduce_or_sync(FULL, hitm);
+                unsigned leafm = ((unsigned)hint.x >> 4) & 15u;
+                unsigned lhit = anyhit & leafm;
+                while (lhit) {
+                    int k = __ffs(lhit) - 1;
+                    lhit &= lhit - 1;
+                    bool h = (hitm >> k) & 1u;
+                    unsigned bm = __ballot_sync(FULL, h);
+                    if (h) {
+                        int o = njobs + __popc(bm & lt);
+                        sjob[wid][o] = ~pick(kids, k);
+                        sown[wid][o] = (unsigned char)lane;
+                    }
+                    njobs += __popc(bm);
+                }
+                if (njobs >= BATCH) run_jobs();
+                unsigned ihit = anyhit & ~leafm;
+                if (ihit) {
+                    unsigned ordb = ((unsigned)(oct < 4 ? hint.y : hint.z) >> ((oct & 3) * 8)) & 0xFFu;
+                    int order[4], n = 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        int c = (ordb >> (2 * j)) & 3;
+                        if ((ihit >> c) & 1u) order[n++] = c;
+                    }
+                    if (sp + n - 1 > PSTACK) {
+                        if (lane == 0) atomicExch(overflow, 1);
+                        break;
+                    }
+                    if (lane == 0)
+                        for (int j = n - 1; j >= 1; --j) {
+                            sstk_node[wid][sp] = pick(kids, order[j]);
+                            sstk_key[wid][sp] = 0;
+                            ++sp;
+                        }
+                    else
+                        sp += n - 1;
+                    node = pick(kids, order[0]);
+                }
+            } else {
             // Child codes are warp-uniform, so leaf/inner is a uniform branch per
             // child: one collective each (ballot for leaves, min-reduce for inner).
-            const unsigned lt = (1u << lane) - 1u;
             int wkey[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -741,7 +796,6 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             // ---- inner children: warp-uniform order by the warp-min entry ----
             int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
                       (wkey[3] != 0x7FFFFFFF);
-            node = kDone;
             if (nin > 0) {
 #define SRT_CX(a, b)                      \
     {                                     \
@@ -766,6 +820,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 }
                 sp += nin - 1;
                 node = pick(kids, wkey[0] & 3);
+            }
             }
             if (node == kDone) {
                 if (sp == 0 && njobs) run_jobs();
@@ -863,12 +918,12 @@ static int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH, int MINB>
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH, int MINB, int ORDER = 1>
 static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>, kTraceThreads, 0);
+            &blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>, kTraceThreads, 0);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     if (!g_num_sms) {
@@ -881,7 +936,7 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
-    k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>
+    k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>
         <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
 }
@@ -890,15 +945,17 @@ static int env_int(const char *name, int dflt);
 
 template <int NS, int MODE, int RNG, class Src, bool STATS>
 static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
-    // SRT_PACKET_CFG (experiments, N=1 mean-depth only): 0 batch 32 (default),
-    // 1 batch 64, 2 batch 32 + 8 blocks/SM, 3 batch 64 + 8 blocks/SM
+    // SRT_PACKET_CFG (experiments, N=1 mean-depth only): 0 batch 32, entry-
+    // sorted children (default), 1 batch 64, 2 batch 32 + 8 blocks/SM, 3 batch
+    // 64 + 8 blocks/SM, 4 octant-ordered children
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
     if constexpr (NS == 1 && MODE == 0 && !STATS) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
+        if (cfg == 4) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 1>(s, src, w, st);
     }
-    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1>(s, src, w, st);
+    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 0>(s, src, w, st);
 }
 
 template <int NS, int MODE, int RNG, class Src>

@@ -13,10 +13,14 @@ cached on the asset, keyed by device and cutoff, like the reference caches
 
 from __future__ import annotations
 
+import ctypes
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
+
+from . import _lib
 
 from .config import CameraConfig, RenderSettings
 from .sampling import pixel_jitter
@@ -47,6 +51,48 @@ class AccumBuffer:
     @property
     def height(self) -> int:
         return int(self.rgb.shape[0])
+
+
+class _PinnedBlock:
+    """Page-locked host block exposed to numpy; returned to the pool when the
+    last array viewing it is collected."""
+
+    def __init__(self, pool, ptr: int, nbytes: int):
+        self._pool, self._ptr, self._nbytes = pool, ptr, nbytes
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            self._pool.release(self._ptr, self._nbytes)
+        except Exception:
+            pass
+
+
+class PinnedPool:
+    """Reuses cudaHostAlloc blocks (srt_host_alloc) for render() outputs, so the
+    device->host copy of the AccumBuffer runs at link speed."""
+
+    def __init__(self):
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+
+    def array(self, shape, dtype=np.float64) -> np.ndarray:
+        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        with self._lock:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = ctypes.c_void_p()
+            _lib.check(_lib.load().srt_host_alloc(nbytes, ctypes.byref(p)))
+            ptr = p.value
+        return np.asarray(_PinnedBlock(self, ptr, nbytes)).view(dtype).reshape(shape)
+
+    def release(self, ptr: int, nbytes: int) -> None:
+        with self._lock:
+            self._free.setdefault(nbytes, []).append(ptr)
+
+
+_PINNED = PinnedPool()
 
 
 def camera_basis(camera: CameraConfig):
@@ -112,8 +158,10 @@ def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, thre
     sc = prepare(asset, settings, bvh, device)
     cam = camera_tuple(camera, settings.width, settings.height)
     mode = 0 if settings.depth_mode == "mean" else 1
-    rgb, op, _ = sc.render(cam, settings.width, settings.height, settings.passes, settings.multisample, mode,
-                           settings.cutoff_s * settings.cutoff_s, True, settings.seed, settings.background)
+    h, w = settings.height, settings.width
+    rgb, op, _ = sc.render(cam, w, h, settings.passes, settings.multisample, mode,
+                           settings.cutoff_s * settings.cutoff_s, True, settings.seed, settings.background,
+                           out_rgb=_PINNED.array((h, w, 3)), out_op=_PINNED.array((h, w)))
     return AccumBuffer(rgb, op, settings.samples_per_pixel)
 
 

@@ -21,7 +21,7 @@ import os
 if os.environ.get("SRT_SAH") == "1":
     from oracle import oracle as O
     lo, hi = asset.aabb_arrays(st.cutoff_s)
-    sc.upload_bvh(O.sah_build(lo, hi))
+    sc.upload_bvh(O.sah_build(lo, hi, leaf_size=int(os.environ.get("SRT_SAH_LEAF", "1"))))
 cam = make_camera(camera_tuple(front_camera(), W, H))
 prm = make_render_params(W, H, st.passes, N, 0, st.cutoff_s ** 2)
 t = shard_tiles(W, H)
