@@ -41,6 +41,9 @@ typedef int32_t srt_status;
 /* acceptance-draw generators (kernels.py:354 is the reference's trig hash) */
 #define SRT_RNG_COUNTER 1 /* u = U24(mix(seed, ray_id, sample, prim)) */
 #define SRT_RNG_TABLE 2   /* u = table[prim * table_slots + slot] (scripted tests) */
+#define SRT_RNG_TRIG64 3  /* the reference's own draw: trig hash of the fp64 hit position,
+                             fp64 candidate in the reference's expression order
+                             (kernels.py:47-60,139-189); parity mode, one ray per thread */
 
 typedef struct SrtScene SrtScene;
 
@@ -75,6 +78,7 @@ typedef struct {
     double background[3];
     int32_t shard_index; /* image-tile sharding: this rank renders 16x16 tiles */
     int32_t shard_count; /* t with t % shard_count == shard_index (1 = all)   */
+    int32_t rng;         /* 0 or SRT_RNG_COUNTER (default), SRT_RNG_TRIG64 */
 } SrtRenderParams;
 
 typedef struct {
@@ -82,7 +86,7 @@ typedef struct {
     int32_t mode;
     int32_t clip;
     double s2;
-    int32_t rng;             /* SRT_RNG_COUNTER or SRT_RNG_TABLE */
+    int32_t rng;             /* SRT_RNG_COUNTER, SRT_RNG_TABLE or SRT_RNG_TRIG64 */
     uint32_t seed;
     uint32_t ray_id0;        /* ray i uses ray_id = ray_id0 + i */
     uint32_t sample0;        /* slot k uses sample = sample0 + k */

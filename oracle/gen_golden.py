@@ -110,6 +110,16 @@ def main() -> None:
     buf2 = R.render(a2, cam, st2)
     np.savez_compressed(OUT / "render_small.npz", rgb=buf.rgb, opacity=buf.opacity, spp=buf.spp,
                         rgb_center=buf2.rgb, opacity_center=buf2.opacity)
+
+    # 6. configs[0] (C1): random_cloud(10k, seed 0, SH0) as-is, 64x64, 1 spp,
+    #    and the same frame at 4 passes x N=2 with SH degree 3
+    a = synthetic.random_cloud(10_000, seed=0, sh_degree=0)
+    c1 = R.render(a, cam, RenderSettings(width=64, height=64, spp=1))
+    a3 = synthetic.random_cloud(10_000, seed=0, sh_degree=3)
+    c1b = R.render(a3, cam, RenderSettings(width=48, height=40, spp=8, multisample=2, seed=7,
+                                           background=[0.05, 0.1, 0.2]))
+    np.savez_compressed(OUT / "render_c1.npz", rgb=c1.rgb, opacity=c1.opacity,
+                        rgb_ms=c1b.rgb, opacity_ms=c1b.opacity)
     print("golden fixtures written to", OUT)
 
 

@@ -17,6 +17,7 @@ LIB_PATH = _HERE / "libsrt.so"
 SRT_OK = 0
 SRT_RNG_COUNTER = 1
 SRT_RNG_TABLE = 2
+SRT_RNG_TRIG64 = 3
 _STATUS_NAMES = {1: "invalid argument", 2: "CUDA error", 3: "out of device memory", 4: "no BVH",
                  5: "stack overflow", 6: "unsupported"}
 
@@ -42,7 +43,7 @@ class SrtRenderParams(ctypes.Structure):
                 ("nslots", ctypes.c_int32), ("mode", ctypes.c_int32), ("clip", ctypes.c_int32),
                 ("s2", ctypes.c_double), ("seed", ctypes.c_uint32), ("pass0", ctypes.c_int32),
                 ("background", ctypes.c_double * 3), ("shard_index", ctypes.c_int32),
-                ("shard_count", ctypes.c_int32)]
+                ("shard_count", ctypes.c_int32), ("rng", ctypes.c_int32)]
 
 
 class SrtTraceParams(ctypes.Structure):

@@ -61,6 +61,7 @@ RenderArgs make_render_args(const SrtRenderParams *p) {
     a.mode = p->mode;
     a.clip = p->clip;
     a.s2 = (float)p->s2;
+    a.s2d = p->s2;
     a.seed = p->seed;
     a.pass0 = p->pass0;
     for (int k = 0; k < 3; ++k) a.bg[k] = (float)p->background[k];
@@ -68,6 +69,7 @@ RenderArgs make_render_args(const SrtRenderParams *p) {
     a.shard_index = p->shard_count < 1 ? 0 : p->shard_index;
     a.tiles_x = (p->width + 15) / 16;
     a.local_tiles = shard_tiles(p->width, p->height, a.shard_index, a.shard_count);
+    a.rng = p->rng;
     return a;
 }
 
@@ -108,7 +110,8 @@ static srt_status validate_render(const SrtScene *s, const SrtRenderParams *p) {
         return SRT_ERR_NO_BVH;
     }
     if (!p || p->width < 1 || p->height < 1 || p->passes < 1 || p->nslots < 1 || p->nslots > 256 ||
-        (p->mode != 0 && p->mode != 1) || !(p->s2 > 0.0) || p->pass0 < 0) {
+        (p->mode != 0 && p->mode != 1) || !(p->s2 > 0.0) || p->pass0 < 0 ||
+        (p->rng != 0 && p->rng != SRT_RNG_COUNTER && p->rng != SRT_RNG_TRIG64)) {
         set_error("invalid render parameters");
         return SRT_ERR_INVALID_ARG;
     }
@@ -495,7 +498,7 @@ srt_status srt_bvh_download(const SrtScene *s, float *node_lo, float *node_hi, i
 
 static srt_status validate_trace(const SrtScene *s, const SrtTraceParams *p, int64_t R, int32_t nslots) {
     if (!s || !p || R < 0 || nslots < 1 || nslots > 256 || (p->mode != 0 && p->mode != 1) || !(p->s2 > 0.0) ||
-        (p->rng != SRT_RNG_COUNTER && p->rng != SRT_RNG_TABLE) ||
+        (p->rng != SRT_RNG_COUNTER && p->rng != SRT_RNG_TABLE && p->rng != SRT_RNG_TRIG64) ||
         (p->rng == SRT_RNG_TABLE && (!p->table || p->table_slots < nslots))) {
         set_error("invalid trace parameters");
         return SRT_ERR_INVALID_ARG;
@@ -511,8 +514,8 @@ srt_status srt_trace_rays_device(const SrtScene *s, const SrtTraceParams *p, con
                                  int32_t nslots, float *d_t, int32_t *d_id, void *stream) {
     srt_status rc = validate_trace(s, p, R, nslots);
     if (rc) return rc;
-    if (p->rng == SRT_RNG_TABLE) {
-        set_error("table RNG needs the host entry point (srt_trace_rays)");
+    if (p->rng == SRT_RNG_TABLE || p->rng == SRT_RNG_TRIG64) {
+        set_error("table / trig64 RNG need the host entry point (srt_trace_rays)");
         return SRT_ERR_INVALID_ARG;
     }
     DeviceGuard g(s->device);
@@ -528,7 +531,7 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
     size_t ray_bytes = sizeof(double) * R * 6;
-    size_t out_bytes = (sizeof(float) + sizeof(int32_t)) * R * nslots;
+    size_t out_bytes = (sizeof(double) + sizeof(int32_t)) * R * nslots;
     size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
     rc = scratch_reserve(s, ray_bytes + out_bytes + table_bytes + 256);
     if (rc) return rc;
@@ -547,7 +550,23 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
     if (!rc && d_table)
         rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
-    if (!rc) rc = launch_trace_rays(s, p, d_rays, R, nslots, d_table, d_t, d_id, st);
+    double *d_t64 = (double *)(base + ray_bytes);
+    if (p->rng == SRT_RNG_TRIG64) d_id = (int32_t *)(base + ray_bytes + sizeof(double) * R * nslots);
+    if (!rc) {
+        if (p->rng == SRT_RNG_TRIG64)
+            rc = launch_trace_rays_trig64(s, p, d_rays, R, nslots, d_t64, d_id, st);
+        else
+            rc = launch_trace_rays(s, p, d_rays, R, nslots, d_table, d_t, d_id, st);
+    }
+    if (!rc && p->rng == SRT_RNG_TRIG64) {
+        std::vector<int32_t> hid((size_t)R * nslots);
+        rc = cuda_status(cudaMemcpyAsync(out_t, d_t64, sizeof(double) * hid.size(), cudaMemcpyDeviceToHost, st), "t");
+        if (!rc) rc = cuda_status(cudaMemcpyAsync(hid.data(), d_id, sizeof(int32_t) * hid.size(), cudaMemcpyDeviceToHost, st), "id");
+        if (!rc) rc = check_flag(s, st);
+        if (rc) return rc;
+        for (size_t i = 0; i < hid.size(); ++i) out_id[i] = hid[i];
+        return SRT_OK;
+    }
     std::vector<float> ht((size_t)R * nslots);
     std::vector<int32_t> hid((size_t)R * nslots);
     if (!rc) rc = cuda_status(cudaMemcpyAsync(ht.data(), d_t, sizeof(float) * ht.size(), cudaMemcpyDeviceToHost, st), "t download");

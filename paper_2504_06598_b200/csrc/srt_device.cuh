@@ -41,6 +41,9 @@ struct __align__(16) Geom {
 };
 
 struct SceneView {
+    const double *means64;  // fp64 records in original id order (trig64 bridge mode)
+    const double *cov64;
+    const double *opac64;
     const Node2 *nodes;
     const Node4 *nodes4;
     int32_t num_nodes4;

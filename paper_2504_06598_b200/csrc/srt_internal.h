@@ -36,6 +36,9 @@ struct SrtScene {
     int64_t *slot_prim_host = nullptr;  // unused placeholder
     srt::SceneView view() const {
         srt::SceneView v;
+        v.means64 = d_means;
+        v.cov64 = d_cov6;
+        v.opac64 = d_opac;
         v.nodes = d_nodes;
         v.nodes4 = d_nodes4;
         v.num_nodes4 = num_nodes4;
@@ -81,12 +84,14 @@ srt_status scratch_reserve(SrtScene *s, size_t bytes);
 struct RenderArgs {
     int width, height, passes, nslots, mode, clip;
     float s2;
+    double s2d;
     uint32_t seed;
     int pass0;
     float bg[3];
     int shard_index, shard_count;
     int tiles_x;
     int64_t local_tiles;
+    int rng;
 };
 RenderArgs make_render_args(const SrtRenderParams *p);
 CamD make_cam(const SrtCamera *c);
@@ -98,6 +103,10 @@ srt_status launch_shade_pass(const SrtScene *s, const CamD &cam, const RenderArg
                              cudaStream_t st);
 srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R,
                              int nslots, const double *d_table, float *d_t, int32_t *d_id, cudaStream_t st);
+srt_status launch_trace_rays_trig64(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R,
+                                    int nslots, double *d_t, int32_t *d_id, cudaStream_t st);
+srt_status launch_trace_pass_trig64(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, double s2,
+                                    int32_t *d_hits, cudaStream_t st);
 srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max,
                                 int mode, double s2, double *d_out, cudaStream_t st);
 srt_status launch_resolve_f64(const RenderArgs &a, const float4 *d_out, double *d_rgb, double *d_op,

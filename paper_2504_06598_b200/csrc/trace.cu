@@ -998,6 +998,7 @@ static srt_status dispatch(const SrtScene *s, const Src &src, const WalkCfg &w, 
 
 srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
                              cudaStream_t st) {
+    if (a.rng == SRT_RNG_TRIG64) return launch_trace_pass_trig64(s, cam, a, pass, (double)a.s2d, d_hits, st);
     CameraSource src;
     src.cam = cam;
     src.a = a;

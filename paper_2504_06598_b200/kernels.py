@@ -7,7 +7,8 @@ outputs written in place, None returned.  Pointing the reference's callers
 (``render.py:166-173``, ``validate.py:106,177``, its acceptance tests) at
 this module swaps its numba CPU loops for libsrt.  Keyword-only extras
 select the counter stream (seed / ray_id0 / sample0), a scripted ``table``
-of uniforms, and the device.
+of uniforms, ``rng="trig64"`` (the reference's own trig-hash draw in fp64,
+for direct comparison with the unmodified reference), and the device.
 
 Differences from the reference, by construction:
 * the acceptance draw is the counter RNG (or a table), not the trig hash of
@@ -67,14 +68,14 @@ def render_stochastic(node_lo, node_hi, node_left, node_right, node_count, prim_
                       means, cov6, opac, sh, deg,
                       ex, ey, ez, rx, ry, rz, ux, uy, uz, fx, fy, fz, half_w, half_h,
                       width, height, passes, nslots, mode, s2, clip, seed,
-                      bgr, bgg, bgb, out_rgb, out_op, *, device=0):
+                      bgr, bgg, bgb, out_rgb, out_op, *, device=0, rng="counter"):
     """kernels.py:622-673: per-pixel means over passes x nslots samples."""
     sc = _scene((node_lo, node_hi, node_left, node_right, node_count, prim_order, prim_lo, prim_hi),
                 means, cov6, opac, sh, int(deg), device)
     try:
         rgb, op, _ = sc.render((ex, ey, ez, rx, ry, rz, ux, uy, uz, fx, fy, fz, half_w, half_h), int(width),
                                int(height), int(passes), int(nslots), int(mode), float(s2), bool(clip), int(seed),
-                               (bgr, bgg, bgb))
+                               (bgr, bgg, bgb), rng=rng)
     finally:
         sc.close()
     out_rgb[...] = rgb

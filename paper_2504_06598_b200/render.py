@@ -145,12 +145,13 @@ def prepare(asset, settings: RenderSettings, bvh=None, device: int = 0) -> Devic
 
 
 def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, threads: int | None = None,
-           device: int = 0) -> AccumBuffer:
+           device: int = 0, rng: str = "counter") -> AccumBuffer:
     """Render a frame on the GPU (render.py:125-174).
 
     ``threads`` is accepted for signature compatibility (the reference's CPU
-    thread count); it has no effect on the GPU.  ``reference_mode`` (exact
-    sorted compositing) is not on the GPU yet and raises.
+    thread count); it has no effect on the GPU.  ``rng="trig64"`` draws the
+    reference's own trig-hash stream in fp64 (parity mode, slower).
+    ``reference_mode`` (exact sorted compositing) is not on the GPU yet.
     """
     del threads
     if settings.reference_mode:
@@ -161,7 +162,7 @@ def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, thre
     h, w = settings.height, settings.width
     rgb, op, _ = sc.render(cam, w, h, settings.passes, settings.multisample, mode,
                            settings.cutoff_s * settings.cutoff_s, True, settings.seed, settings.background,
-                           out_rgb=_PINNED.array((h, w, 3)), out_op=_PINNED.array((h, w)))
+                           out_rgb=_PINNED.array((h, w, 3)), out_op=_PINNED.array((h, w)), rng=rng)
     return AccumBuffer(rgb, op, settings.samples_per_pixel)
 
 

@@ -17,7 +17,7 @@ from . import _lib
 from ._lib import SrtCamera, SrtRenderParams, SrtSceneDesc, SrtTraceParams, check
 
 TMAX = float(np.finfo(np.float64).max)
-RNG = {"counter": _lib.SRT_RNG_COUNTER, "table": _lib.SRT_RNG_TABLE}
+RNG = {"counter": _lib.SRT_RNG_COUNTER, "table": _lib.SRT_RNG_TABLE, "trig64": _lib.SRT_RNG_TRIG64}
 
 
 def _ptr(a) -> ctypes.c_void_p:
@@ -47,7 +47,7 @@ def make_camera(cam) -> SrtCamera:
 
 
 def make_render_params(width, height, passes, nslots, mode, s2, clip=True, seed=0, background=(0.0, 0.0, 0.0),
-                       pass0=0, shard_index=0, shard_count=1) -> SrtRenderParams:
+                       pass0=0, shard_index=0, shard_count=1, rng="counter") -> SrtRenderParams:
     p = SrtRenderParams()
     p.width, p.height, p.passes, p.nslots = int(width), int(height), int(passes), int(nslots)
     p.mode, p.clip, p.s2 = int(mode), int(bool(clip)), float(s2)
@@ -56,6 +56,9 @@ def make_render_params(width, height, passes, nslots, mode, s2, clip=True, seed=
     for k in range(3):
         p.background[k] = float(background[k])
     p.shard_index, p.shard_count = int(shard_index), int(shard_count)
+    if rng not in ("counter", "trig64"):
+        raise ValueError(f"render rng must be 'counter' or 'trig64', got {rng!r}")
+    p.rng = RNG[rng]
     return p
 
 
@@ -149,6 +152,8 @@ class DeviceScene:
     def trace_rays(self, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0, clip=True, nslots=1,
                    rng="counter", seed=0, ray_id0=0, sample0=0, table=None):
         """kernels.trace_batch semantics (kernels.py:527-540) on the GPU.
+        rng: "counter" (default), "table" (explicit uniforms) or "trig64" (the
+        reference's own fp64 trig-hash draw, parity mode).
         Returns (out_t (R,N) f64, +inf on miss; out_id (R,N) i64, -1 on miss)."""
         o = _c64(origins).reshape(-1, 3)
         d = _c64(dirs).reshape(-1, 3)
@@ -179,11 +184,11 @@ class DeviceScene:
 
     # -- frames ----------------------------------------------------------------
     def render(self, cam, width, height, passes=1, nslots=1, mode=0, s2=8.0, clip=True, seed=0,
-               background=(0.0, 0.0, 0.0), pass0=0, want_ids=False, out_rgb=None, out_op=None):
+               background=(0.0, 0.0, 0.0), pass0=0, want_ids=False, out_rgb=None, out_op=None, rng="counter"):
         """kernels.render_stochastic semantics (kernels.py:622-673) on the GPU.
         Returns (rgb (H,W,3) f64, opacity (H,W) f64, ids (H,W,N) i64 of pass pass0 or None)."""
         camera = make_camera(cam)
-        prm = make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background, pass0)
+        prm = make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background, pass0, rng=rng)
         rgb = np.empty((height, width, 3)) if out_rgb is None else out_rgb
         op = np.empty((height, width)) if out_op is None else out_op
         ids = np.full((height, width, nslots), -1, np.int64) if want_ids else None

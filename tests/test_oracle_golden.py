@@ -139,3 +139,27 @@ def test_counter_rng_uniform_and_decorrelated(oracle):
     assert abs(u0.mean() - 0.5) < 0.005
     assert abs(np.corrcoef(u0[:-1], u0[1:])[0, 1]) < 0.01
     assert abs(np.corrcoef(u0, u1)[0, 1]) < 0.01
+
+
+def test_render_c1_bitwise(oracle, golden):
+    """configs[0] (C1) frames from the reference: 10k SH0 at 1 spp, and SH3 at
+    4 passes x N=2 with a background, bit for bit."""
+    from paper_2504_06598_b200.synthetic import front_camera, random_cloud
+
+    g = golden("render_c1")
+    cam = front_camera()
+    a = random_cloud(10_000, seed=0, sh_degree=0)
+    pk = a.packed
+    lo, hi = a.aabb_arrays(np.sqrt(S2))
+    b = oracle.sah_build(lo, hi)
+    ct = oracle.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, 64, 64)
+    out = oracle.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 0, ct, 64, 64, s2=S2, rng="trig")
+    np.testing.assert_array_equal(out["rgb"], g["rgb"])
+    np.testing.assert_array_equal(out["opacity"], g["opacity"])
+    a3 = random_cloud(10_000, seed=0, sh_degree=3)
+    pk3 = a3.packed
+    ct3 = oracle.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, 48, 40)
+    out3 = oracle.render(b, pk3.means, pk3.cov_inv6, pk3.opacities, pk3.sh, 3, ct3, 48, 40, passes=4, nslots=2,
+                         s2=S2, seed=7, rng="trig", background=[0.05, 0.1, 0.2])
+    np.testing.assert_array_equal(out3["rgb"], g["rgb_ms"])
+    np.testing.assert_array_equal(out3["opacity"], g["opacity_ms"])
