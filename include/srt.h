@@ -18,6 +18,8 @@
  *                                                      + srt_shade_pass_device
  *                                                      per pass)
  *   kernels.transmittance_batch kernels.py:544-557 -> srt_transmittance_rays
+ *   kernels.exact_batch        kernels.py:584-604  -> srt_exact_rays
+ *   kernels.render_exact       kernels.py:677-723  -> srt_render_exact
  *   (new) multi-GPU tile gather                    -> srt_unpack_tiles_device
  */
 #ifndef SRT_H
@@ -143,6 +145,19 @@ srt_status srt_trace_rays_device(const SrtScene *scene, const SrtTraceParams *pa
 srt_status srt_transmittance_rays(const SrtScene *scene, const double *origins,
                                   const double *dirs, int64_t num_rays, double t_min,
                                   double t_max, int32_t mode, double s2, double *out);
+
+/* ---- exact compositing (kernels.exact_batch / render_exact) -------------- */
+/* Every valid candidate along the ray, sorted by (t, prim id), composited
+ * front to back over `background` (kernels.py:441-475, 584-604).  out_rgb
+ * (R,3) f64, out_op (R,) f64. */
+srt_status srt_exact_rays(const SrtScene *scene, const double *origins, const double *dirs,
+                          int64_t num_rays, double t_min, double t_max, int32_t mode, double s2,
+                          const double *background, double *out_rgb, double *out_op);
+/* render_exact (kernels.py:677-723): per-pixel mean of the exact composite over
+ * params->passes jittered rays (passes pass0..pass0+passes-1).  Host outputs
+ * (H,W,3) and (H,W) f64. */
+srt_status srt_render_exact(const SrtScene *scene, const SrtCamera *camera,
+                            const SrtRenderParams *params, double *out_rgb, double *out_op);
 
 /* ---- full frames (kernels.render_stochastic) ----------------------------- */
 /* Host outputs out_rgb (H,W,3) f64 and out_op (H,W) f64 = per-pixel means.

@@ -120,6 +120,19 @@ def main() -> None:
                                            background=[0.05, 0.1, 0.2]))
     np.savez_compressed(OUT / "render_c1.npz", rgb=c1.rgb, opacity=c1.opacity,
                         rgb_ms=c1b.rgb, opacity_ms=c1b.opacity)
+
+    # 7. exact compositing (kernels.py:584-604, 677-723)
+    a = synthetic.random_cloud(500, seed=41, sh_degree=2)
+    pk = a.packed
+    bg = np.array([0.15, 0.25, 0.35])
+    ex_rgb = np.empty((n, 3))
+    ex_op = np.empty(n)
+    kernels.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, origins, dirs, 0.0, tmax, 0,
+                        s * s, bg[0], bg[1], bg[2], ex_rgb, ex_op)
+    fr = R.render(a, cam, RenderSettings(width=20, height=16, spp=3, seed=2, reference_mode=True,
+                                         background=bg))
+    np.savez_compressed(OUT / "exact_500.npz", rgb=ex_rgb, opacity=ex_op, frame_rgb=fr.rgb, frame_opacity=fr.opacity,
+                        frame_spp=fr.spp)
     print("golden fixtures written to", OUT)
 
 

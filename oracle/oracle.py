@@ -87,6 +87,12 @@ def lib() -> ctypes.CDLL:
         L.srt_oracle_transmittance.argtypes = bvh_args + [
             _f64p, _f64p, _f64p, _i64, _f64p, _f64p, _i64, _dbl, _dbl, _int, _dbl, _f64p, _int,
         ]
+        L.srt_oracle_exact_batch.restype = None
+        L.srt_oracle_exact_batch.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _i64, _f64p, _f64p, _i64, _dbl, _dbl,
+                                             _int, _dbl, _f64p, _f64p, _f64p, _int]
+        L.srt_oracle_render_exact.restype = None
+        L.srt_oracle_render_exact.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _i64, _f64p, _i64, _i64, _i64, _int,
+                                              _dbl, _i64, _f64p, _f64p, _f64p, _int]
         _lib = L
     return _lib
 
@@ -296,6 +302,35 @@ def render(bvh: OracleBvh, means, cov6, opac, sh, deg, cam, width, height, passe
     if counters:
         out["counters"] = dict(zip(COUNTER_NAMES, (int(v) for v in cnt)))
     return out
+
+
+def exact_batch(means, cov6, opac, sh, deg, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0,
+                background=(0.0, 0.0, 0.0), threads=0):
+    """kernels.exact_batch (kernels.py:584-604): brute-force sorted compositing."""
+    means, cov6, opac, sh = (_c(x, np.float64) for x in (means, cov6, opac, sh))
+    origins = _c(origins, np.float64).reshape(-1, 3)
+    dirs = _c(dirs, np.float64).reshape(-1, 3)
+    bg = _c(background, np.float64)
+    rgb = np.empty((origins.shape[0], 3))
+    op = np.empty(origins.shape[0])
+    lib().srt_oracle_exact_batch(_p(means), _p(cov6), _p(opac), _p(sh), means.shape[0], int(deg), _p(origins),
+                                 _p(dirs), origins.shape[0], float(t_min), float(t_max), int(mode), float(s2), _p(bg),
+                                 _p(rgb), _p(op), int(threads))
+    return rgb, op
+
+
+def render_exact(means, cov6, opac, sh, deg, cam, width, height, frames=1, mode=0, s2=8.0, seed=0,
+                 background=(0.0, 0.0, 0.0), threads=0):
+    """kernels.render_exact (kernels.py:677-723)."""
+    means, cov6, opac, sh = (_c(x, np.float64) for x in (means, cov6, opac, sh))
+    cam = _c(cam, np.float64)
+    bg = _c(background, np.float64)
+    rgb = np.zeros((height, width, 3))
+    op = np.zeros((height, width))
+    lib().srt_oracle_render_exact(_p(means), _p(cov6), _p(opac), _p(sh), means.shape[0], int(deg), _p(cam),
+                                  int(width), int(height), int(frames), int(mode), float(s2), int(seed), _p(bg),
+                                  _p(rgb), _p(op), int(threads))
+    return rgb, op
 
 
 def library_path() -> str:

@@ -834,3 +834,136 @@ int64_t srt_oracle_sah_build(const double *lo, const double *hi, int64_t n, int6
     free(B.suf_hi);
     return B.num_nodes;
 }
+
+/* ------------------------------------------------------------------------ */
+/* exact compositing (brute force, no BVH): kernels.py:441-475, 584-604,    */
+/* 677-723                                                                   */
+/* ------------------------------------------------------------------------ */
+
+/* stable merge sort of idx[0..m) by key (np.argsort kind="mergesort") */
+static void stable_argsort(const double *key, int64_t *idx, int64_t *tmp, int64_t m) {
+    for (int64_t i = 0; i < m; ++i) idx[i] = i;
+    for (int64_t width = 1; width < m; width *= 2) {
+        for (int64_t i = 0; i < m; i += 2 * width) {
+            int64_t a = i, am = i + width < m ? i + width : m, b = am, bm = i + 2 * width < m ? i + 2 * width : m;
+            int64_t o = i;
+            while (a < am && b < bm) tmp[o++] = key[idx[b]] < key[idx[a]] ? idx[b++] : idx[a++];
+            while (a < am) tmp[o++] = idx[a++];
+            while (b < bm) tmp[o++] = idx[b++];
+        }
+        memcpy(idx, tmp, sizeof(int64_t) * (size_t)m);
+    }
+}
+
+/* kernels.py:441-475 */
+static void exact_ray(const Scene *sc, double ox, double oy, double oz, double dx, double dy, double dz,
+                      double t_min, double t_max, int mode, double s2, const double *bg, double *t_buf,
+                      double *a_buf, int64_t *id_buf, int64_t *order, int64_t *tmp, double *out4) {
+    int64_t m = 0;
+    for (int64_t pid = 0; pid < sc->n; ++pid) {
+        double t = 0, resid = 0, hx, hy, hz;
+        if (candidate(sc, pid, ox, oy, oz, dx, dy, dz, mode, s2, &t, &resid, &hx, &hy, &hz) && t > t_min &&
+            t < t_max) {
+            t_buf[m] = t;
+            a_buf[m] = sc->opac[pid] * exp(-0.5 * resid);
+            id_buf[m] = pid;
+            m++;
+        }
+    }
+    stable_argsort(t_buf, order, tmp, m);
+    double r = 0.0, g = 0.0, b = 0.0, trans = 1.0;
+    for (int64_t i = 0; i < m; ++i) {
+        int64_t j = order[i];
+        double alpha = a_buf[j], col[3];
+        srt_oracle_sh_color(sc->sh, sc->deg, id_buf[j], dx, dy, dz, col);
+        double w = trans * alpha;
+        r += w * col[0];
+        g += w * col[1];
+        b += w * col[2];
+        trans *= 1.0 - alpha;
+    }
+    r += trans * bg[0];
+    g += trans * bg[1];
+    b += trans * bg[2];
+    out4[0] = r;
+    out4[1] = g;
+    out4[2] = b;
+    out4[3] = 1.0 - trans;
+}
+
+/* kernels.py:584-604 */
+void srt_oracle_exact_batch(const double *means, const double *cov6, const double *opac, const double *sh,
+                            int64_t n, int64_t deg, const double *origins, const double *dirs, int64_t R,
+                            double t_min, double t_max, int mode, double s2, const double *bg, double *out_rgb,
+                            double *out_op, int threads) {
+    Scene sc = {means, cov6, opac, sh, n, deg};
+    set_threads(threads);
+#pragma omp parallel
+    {
+        size_t cap = (size_t)(n > 0 ? n : 1);
+        double *t_buf = (double *)malloc(sizeof(double) * cap), *a_buf = (double *)malloc(sizeof(double) * cap);
+        int64_t *id_buf = (int64_t *)malloc(sizeof(int64_t) * cap), *order = (int64_t *)malloc(sizeof(int64_t) * cap),
+                *tmp = (int64_t *)malloc(sizeof(int64_t) * cap);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < R; ++i) {
+            double o4[4];
+            exact_ray(&sc, origins[i * 3], origins[i * 3 + 1], origins[i * 3 + 2], dirs[i * 3], dirs[i * 3 + 1],
+                      dirs[i * 3 + 2], t_min, t_max, mode, s2, bg, t_buf, a_buf, id_buf, order, tmp, o4);
+            out_rgb[i * 3] = o4[0];
+            out_rgb[i * 3 + 1] = o4[1];
+            out_rgb[i * 3 + 2] = o4[2];
+            out_op[i] = o4[3];
+        }
+        free(t_buf);
+        free(a_buf);
+        free(id_buf);
+        free(order);
+        free(tmp);
+    }
+}
+
+/* kernels.py:677-723 (render_exact): per-pixel mean over `frames` jittered rays */
+void srt_oracle_render_exact(const double *means, const double *cov6, const double *opac, const double *sh,
+                             int64_t n, int64_t deg, const double *cam, int64_t width, int64_t height,
+                             int64_t frames, int mode, double s2, int64_t seed, const double *bg, double *out_rgb,
+                             double *out_op, int threads) {
+    Scene sc = {means, cov6, opac, sh, n, deg};
+    int64_t tiles_x = (width + 15) / 16, tiles_y = (height + 15) / 16;
+    sobol_init();
+    set_threads(threads);
+#pragma omp parallel
+    {
+        size_t cap = (size_t)(n > 0 ? n : 1);
+        double *t_buf = (double *)malloc(sizeof(double) * cap), *a_buf = (double *)malloc(sizeof(double) * cap);
+        int64_t *id_buf = (int64_t *)malloc(sizeof(int64_t) * cap), *order = (int64_t *)malloc(sizeof(int64_t) * cap),
+                *tmp = (int64_t *)malloc(sizeof(int64_t) * cap);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t tile = 0; tile < tiles_x * tiles_y; ++tile) {
+            int64_t ty = tile / tiles_x, tx = tile % tiles_x;
+            int64_t y_end = (ty + 1) * 16 < height ? (ty + 1) * 16 : height;
+            int64_t x_end = (tx + 1) * 16 < width ? (tx + 1) * 16 : width;
+            for (int64_t py = ty * 16; py < y_end; ++py)
+                for (int64_t px = tx * 16; px < x_end; ++px) {
+                    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                    for (int64_t f = 0; f < frames; ++f) {
+                        double jx, jy, dx, dy, dz, o4[4];
+                        srt_oracle_pixel_jitter(px, py, f, seed, &jx, &jy);
+                        double u = 2.0 * ((double)px + jx) / (double)width - 1.0;
+                        double v = 1.0 - 2.0 * ((double)py + jy) / (double)height;
+                        camera_dir(cam, u, v, &dx, &dy, &dz);
+                        exact_ray(&sc, cam[0], cam[1], cam[2], dx, dy, dz, 0.0, DBL_MAX, mode, s2, bg, t_buf, a_buf,
+                                  id_buf, order, tmp, o4);
+                        for (int c = 0; c < 4; ++c) acc[c] += o4[c];
+                    }
+                    double inv = 1.0 / (double)frames;
+                    for (int c = 0; c < 3; ++c) out_rgb[(py * width + px) * 3 + c] = acc[c] * inv;
+                    out_op[py * width + px] = acc[3] * inv;
+                }
+        }
+        free(t_buf);
+        free(a_buf);
+        free(id_buf);
+        free(order);
+        free(tmp);
+    }
+}

@@ -12,7 +12,8 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libsrt.so"
+# SRT_LIBSRT_PATH overrides the in-tree library (A/B timing of two builds)
+LIB_PATH = Path(os.environ.get("SRT_LIBSRT_PATH", _HERE / "libsrt.so"))
 
 SRT_OK = 0
 SRT_RNG_COUNTER = 1
@@ -74,6 +75,8 @@ SYMBOLS = [
     ("srt_trace_rays", _i32, [_vp, ctypes.POINTER(SrtTraceParams), _vp, _vp, _i64, _i32, _vp, _vp]),
     ("srt_trace_rays_device", _i32, [_vp, ctypes.POINTER(SrtTraceParams), _vp, _i64, _i32, _vp, _vp, _vp]),
     ("srt_transmittance_rays", _i32, [_vp, _vp, _vp, _i64, _f64, _f64, _i32, _f64, _vp]),
+    ("srt_exact_rays", _i32, [_vp, _vp, _vp, _i64, _f64, _f64, _i32, _f64, _vp, _vp, _vp]),
+    ("srt_render_exact", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp]),
     ("srt_render", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp]),
     ("srt_trace_pass_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _i32, _vp,
                                      _vp]),

@@ -94,7 +94,7 @@ srt_status check_flag(const SrtScene *s, cudaStream_t st) {
     if (rc) return rc;
     if (flag) {
         cudaMemsetAsync(s->d_flag, 0, sizeof(int), st);
-        set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
+        set_error("traversal stack overflow (BVH deeper than the 128-entry stack, or more than 512 exact candidates)");
         return SRT_ERR_STACK_OVERFLOW;
     }
     return SRT_OK;
@@ -608,6 +608,64 @@ srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, con
     rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
     if (!rc) rc = launch_transmittance(s, d_rays, R, t_min, t_max, mode, s2, d_out, st);
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out, d_out, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "download");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const double *dirs, int64_t R, double t_min,
+                          double t_max, int32_t mode, double s2, const double *background, double *out_rgb,
+                          double *out_op) {
+    if (!sc || R < 0 || (mode != 0 && mode != 1) || !(s2 > 0.0) || !background || (R > 0 && (!out_rgb || !out_op))) {
+        set_error("invalid exact-compositing parameters");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (!sc->has_bvh) {
+        set_error("scene has no BVH");
+        return SRT_ERR_NO_BVH;
+    }
+    if (R == 0) return SRT_OK;
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    size_t ray_bytes = sizeof(double) * R * 6;
+    srt_status rc = scratch_reserve(s, ray_bytes + sizeof(double) * R * 4);
+    if (rc) return rc;
+    double *d_rays = (double *)s->d_scratch;
+    double *d_rgb = d_rays + R * 6;
+    double *d_op = d_rgb + R * 3;
+    std::vector<double> packed((size_t)R * 6);
+    for (int64_t i = 0; i < R; ++i)
+        for (int k = 0; k < 3; ++k) {
+            packed[i * 6 + k] = origins[i * 3 + k];
+            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
+        }
+    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    if (!rc) rc = launch_exact_rays(s, d_rays, R, t_min, t_max, mode, s2, background, d_rgb, d_op, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * R * 3, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "op");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+srt_status srt_render_exact(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
+                            double *out_op) {
+    srt_status rc = validate_render(sc, p);
+    if (rc) return rc;
+    if (!camera || !out_rgb || !out_op) {
+        set_error("null camera or output");
+        return SRT_ERR_INVALID_ARG;
+    }
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    const int64_t npix = (int64_t)p->width * p->height;
+    rc = scratch_reserve(s, sizeof(double) * npix * 4);
+    if (rc) return rc;
+    double *d_rgb = (double *)s->d_scratch;
+    double *d_op = d_rgb + npix * 3;
+    rc = launch_exact_frame(s, make_cam(camera), make_render_args(p), d_rgb, d_op, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "op");
     if (!rc) rc = check_flag(s, st);
     return rc;
 }

@@ -82,4 +82,36 @@ def render_stochastic(node_lo, node_hi, node_left, node_right, node_count, prim_
     out_op[...] = op
 
 
-__all__ = ["render_stochastic", "trace_batch", "transmittance_batch", "np"]
+def _lbvh_scene(means, cov6, opac, sh, deg, s2, device) -> DeviceScene:
+    sc = DeviceScene(means, cov6, opac, sh, deg, device)
+    sc.build_bvh(float(np.sqrt(s2)))  # boxes at the cutoff radius the validity test uses
+    return sc
+
+
+def exact_batch(means, cov6, opac, sh, deg, origins, directions, t_min, t_max, mode, s2, bgr, bgg, bgb,
+                out_rgb, out_op, *, device=0):
+    """kernels.py:584-604: exact sorted compositing per explicit ray (the
+    reference brute-forces all primitives; here a GPU LBVH collects them)."""
+    sc = _lbvh_scene(means, cov6, opac, sh, int(deg), s2, device)
+    try:
+        rgb, op = sc.exact_rays(origins, directions, t_min, t_max, int(mode), float(s2), (bgr, bgg, bgb))
+    finally:
+        sc.close()
+    out_rgb[...] = rgb
+    out_op[...] = op
+
+
+def render_exact(means, cov6, opac, sh, deg, ex, ey, ez, rx, ry, rz, ux, uy, uz, fx, fy, fz, half_w, half_h,
+                 width, height, frames, mode, s2, seed, bgr, bgg, bgb, out_rgb, out_op, *, device=0):
+    """kernels.py:677-723: per-pixel exact composite averaged over `frames` jittered rays."""
+    sc = _lbvh_scene(means, cov6, opac, sh, int(deg), s2, device)
+    try:
+        rgb, op = sc.render_exact((ex, ey, ez, rx, ry, rz, ux, uy, uz, fx, fy, fz, half_w, half_h), int(width),
+                                  int(height), int(frames), int(mode), float(s2), int(seed), (bgr, bgg, bgb))
+    finally:
+        sc.close()
+    out_rgb[...] = rgb
+    out_op[...] = op
+
+
+__all__ = ["exact_batch", "render_exact", "render_stochastic", "trace_batch", "transmittance_batch", "np"]

@@ -151,15 +151,20 @@ def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, thre
     ``threads`` is accepted for signature compatibility (the reference's CPU
     thread count); it has no effect on the GPU.  ``rng="trig64"`` draws the
     reference's own trig-hash stream in fp64 (parity mode, slower).
-    ``reference_mode`` (exact sorted compositing) is not on the GPU yet.
+    ``settings.reference_mode`` renders exact sorted compositing instead
+    (render_exact, kernels.py:677-723), with ``spp = passes``.
     """
     del threads
-    if settings.reference_mode:
-        raise NotImplementedError("reference_mode (exact compositing) is not implemented on the GPU yet")
     sc = prepare(asset, settings, bvh, device)
     cam = camera_tuple(camera, settings.width, settings.height)
     mode = 0 if settings.depth_mode == "mean" else 1
     h, w = settings.height, settings.width
+    if settings.reference_mode:
+        # exact sorted compositing averaged over the same jittered rays (render.py:156-163)
+        rgb, op = sc.render_exact(cam, w, h, settings.passes, mode, settings.cutoff_s * settings.cutoff_s,
+                                  settings.seed, settings.background, out_rgb=_PINNED.array((h, w, 3)),
+                                  out_op=_PINNED.array((h, w)))
+        return AccumBuffer(rgb, op, settings.passes)
     rgb, op, _ = sc.render(cam, w, h, settings.passes, settings.multisample, mode,
                            settings.cutoff_s * settings.cutoff_s, True, settings.seed, settings.background,
                            out_rgb=_PINNED.array((h, w, 3)), out_op=_PINNED.array((h, w)), rng=rng)

@@ -182,6 +182,28 @@ class DeviceScene:
                                                  float(t_max), int(mode), float(s2), _ptr(out)))
         return out
 
+    def exact_rays(self, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0, background=(0.0, 0.0, 0.0)):
+        """kernels.exact_batch semantics (kernels.py:584-604): sorted compositing
+        of every valid candidate.  Returns (rgb (R,3) f64, opacity (R,) f64)."""
+        o = _c64(origins).reshape(-1, 3)
+        d = _c64(dirs).reshape(-1, 3)
+        bg = _c64(background).reshape(3)
+        rgb = np.empty((o.shape[0], 3))
+        op = np.empty(o.shape[0])
+        check(_lib.load().srt_exact_rays(self.handle, _ptr(o), _ptr(d), o.shape[0], float(t_min), float(t_max),
+                                         int(mode), float(s2), _ptr(bg), _ptr(rgb), _ptr(op)))
+        return rgb, op
+
+    def render_exact(self, cam, width, height, frames=1, mode=0, s2=8.0, seed=0, background=(0.0, 0.0, 0.0),
+                     out_rgb=None, out_op=None):
+        """kernels.render_exact semantics (kernels.py:677-723)."""
+        camera = make_camera(cam)
+        prm = make_render_params(width, height, frames, 1, mode, s2, True, seed, background)
+        rgb = np.empty((height, width, 3)) if out_rgb is None else out_rgb
+        op = np.empty((height, width)) if out_op is None else out_op
+        check(_lib.load().srt_render_exact(self.handle, ctypes.byref(camera), ctypes.byref(prm), _ptr(rgb), _ptr(op)))
+        return rgb, op
+
     # -- frames ----------------------------------------------------------------
     def render(self, cam, width, height, passes=1, nslots=1, mode=0, s2=8.0, clip=True, seed=0,
                background=(0.0, 0.0, 0.0), pass0=0, want_ids=False, out_rgb=None, out_op=None, rng="counter"):

@@ -1,0 +1,97 @@
+"""Exact sorted compositing on the GPU (render_exact / exact_batch,
+kernels.py:441-475, 584-604, 677-723) against the reference's own outputs
+(tests/golden/exact_500.npz) and the oracle.  fp32 alphas and colours: 1e-5
+relative; a pixel whose two candidates lie within fp32 resolution in depth
+may composite in swapped order, so a small fraction may deviate more."""
+
+import numpy as np
+import pytest
+
+from conftest import S2, random_rays
+
+pytestmark = pytest.mark.gpu
+RTOL, ATOL = 2e-5, 2e-6
+
+
+def _close_fraction(a, b):
+    ok = np.abs(a - b) <= RTOL * np.abs(b) + ATOL
+    return float(np.mean(ok.reshape(ok.shape[0], -1).all(axis=1) if ok.ndim > 1 else ok))
+
+
+def test_exact_batch_matches_reference(golden):
+    from paper_2504_06598_b200 import kernels
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    g = golden("exact_500")
+    t = golden("trace_400")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    pk = a.packed
+    n = t["origins"].shape[0]
+    rgb = np.empty((n, 3))
+    op = np.empty(n)
+    kernels.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, t["origins"], t["dirs"], 0.0,
+                        float(np.finfo(np.float64).max), 0, S2, 0.15, 0.25, 0.35, rgb, op)
+    assert _close_fraction(rgb, g["rgb"]) >= 0.995
+    assert _close_fraction(op, g["opacity"]) >= 0.995
+
+
+def test_render_reference_mode_matches_reference(golden):
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    g = golden("exact_500")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    buf = render(a, front_camera(), RenderSettings(width=20, height=16, spp=3, seed=2, reference_mode=True,
+                                                   background=[0.15, 0.25, 0.35]))
+    assert buf.spp == 3
+    assert _close_fraction(buf.rgb.reshape(-1, 3), g["frame_rgb"].reshape(-1, 3)) >= 0.995
+    assert _close_fraction(buf.opacity.reshape(-1), g["frame_opacity"].reshape(-1)) >= 0.995
+
+
+def test_exact_vs_oracle_larger(oracle):
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(5_000, seed=3, sh_degree=3)
+    pk = a.packed
+    o, d = random_rays(np.random.default_rng(4), 4_000)
+    sc = DeviceScene.from_packed(pk)
+    sc.build_bvh(np.sqrt(S2))
+    rgb, op = sc.exact_rays(o, d, s2=S2, background=(0.1, 0.0, 0.2))
+    want_rgb, want_op = oracle.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 3, o, d, s2=S2,
+                                           background=(0.1, 0.0, 0.2))
+    assert _close_fraction(rgb, want_rgb) >= 0.995
+    assert _close_fraction(op, want_op) >= 0.995
+
+
+def test_exact_closed_forms():
+    """tests/test_render.py:113-124 and tests/test_kernels.py:163-175 of the reference."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, kernels, pancake_stack, render, two_layer_scene
+
+    buf = render(two_layer_scene(), front_camera(), RenderSettings(width=8, height=8, spp=4, reference_mode=True))
+    np.testing.assert_allclose(buf.rgb[..., 0], 0.5, atol=1e-6)
+    np.testing.assert_allclose(buf.rgb[..., 1], 0.0, atol=1e-6)
+    np.testing.assert_allclose(buf.rgb[..., 2], 0.25, atol=1e-6)
+    np.testing.assert_allclose(buf.opacity, 0.75, atol=1e-6)
+    assert buf.spp == 4
+    tie = pancake_stack([0.5, 0.5], [[1, 0, 0], [0, 0, 1]], spacing=0.0)  # equal depths: id order
+    pk = tie.packed
+    rgb = np.empty((1, 3))
+    op = np.empty(1)
+    kernels.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 0, np.array([[0.1, 0.0, 0.0]]),
+                        np.array([[0.0, 0.0, 1.0]]), 0.0, float(np.finfo(np.float64).max), 0, S2, 0.0, 0.0, 0.0, rgb, op)
+    np.testing.assert_allclose(rgb[0], [0.5, 0.0, 0.25], atol=1e-6)
+
+
+def test_stochastic_mean_approaches_exact():
+    """tests/test_kernels.py:255-266: the estimator's mean closes in on the exact image."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(100, seed=59)
+    errs = {}
+    for spp in (1, 512):
+        exact = render(a, front_camera(), RenderSettings(width=8, height=8, spp=spp, seed=5, reference_mode=True))
+        noisy = render(a, front_camera(), RenderSettings(width=8, height=8, spp=spp, seed=5))
+        errs[spp] = float(np.mean((noisy.rgb - exact.rgb) ** 2))
+    assert errs[512] < errs[1] / 20

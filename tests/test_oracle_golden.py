@@ -163,3 +163,26 @@ def test_render_c1_bitwise(oracle, golden):
                          s2=S2, seed=7, rng="trig", background=[0.05, 0.1, 0.2])
     np.testing.assert_array_equal(out3["rgb"], g["rgb_ms"])
     np.testing.assert_array_equal(out3["opacity"], g["opacity_ms"])
+
+
+def test_exact_compositing_matches_reference(oracle, golden):
+    """kernels.exact_batch and render(reference_mode=True) (kernels.py:584-604,
+    677-723) restated: bit for bit against the reference's outputs."""
+    from paper_2504_06598_b200.synthetic import front_camera, random_cloud
+
+    g = golden("exact_500")
+    t = golden("trace_400")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    pk = a.packed
+    bg = [0.15, 0.25, 0.35]
+    rgb, op = oracle.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 2, t["origins"], t["dirs"], s2=S2,
+                                 background=bg)
+    np.testing.assert_array_equal(rgb, g["rgb"])
+    np.testing.assert_array_equal(op, g["opacity"])
+    cam = front_camera()
+    ct = oracle.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, 20, 16)
+    frgb, fop = oracle.render_exact(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 2, ct, 20, 16, frames=3, s2=S2, seed=2,
+                                    background=bg)
+    np.testing.assert_array_equal(frgb, g["frame_rgb"])
+    np.testing.assert_array_equal(fop, g["frame_opacity"])
+    assert int(g["frame_spp"]) == 3
