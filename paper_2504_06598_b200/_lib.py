@@ -100,7 +100,10 @@ def load() -> ctypes.CDLL:
             raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
                               f"(there is no CPU fallback for the GPU renderer)")
         lib = ctypes.CDLL(os.fspath(LIB_PATH))
+        override = "SRT_LIBSRT_PATH" in os.environ
         for name, res, args in SYMBOLS:
+            if override and not hasattr(lib, name):
+                continue  # an older build under A/B comparison
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -206,44 +206,45 @@ struct Cand {
     int valid;
 };
 
-template <int MODE, class R>
+template <int MODE, class R, bool REFINE = true>
 __device__ __forceinline__ Cand candidate(const R &r, const float4 &m, const float4 &a, const float4 &b,
                                           float s2) {
     Cand c;
     double vx = (double)m.x - r.ox, vy = (double)m.y - r.oy, vz = (double)m.z - r.oz;  // mu - o
     double tc = vx * r.dx + vy * r.dy + vz * r.dz;  // (mu - o).d  == center depth (mode 1)
     double t0 = tc * r.inv_dd;
+    float wx = (float)(t0 * r.dx - vx), wy = (float)(t0 * r.dy - vy), wz = (float)(t0 * r.dz - vz);
     float a00 = a.x, a01 = a.y, a02 = a.z, a11 = a.w, a12 = b.x, a22 = b.y;
     float adx = a00 * r.fdx + a01 * r.fdy + a02 * r.fdz;
     float ady = a01 * r.fdx + a11 * r.fdy + a12 * r.fdz;
     float adz = a02 * r.fdx + a12 * r.fdy + a22 * r.fdz;
     float dad = r.fdx * adx + r.fdy * ady + r.fdz * adz;
-    float inv_dad = 1.0f / dad;
-    // Two re-centrings: first at the Euclidean projection of the mean, then
-    // at the resulting estimate of the peak.  At the peak d.A.w vanishes, so
-    // the residual w.A.w has no cancellation even for very anisotropic A.
-    double t1 = t0;
-    float wx, wy, wz, awx, awy, awz, daw, waw;
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-        wx = (float)(t1 * r.dx - vx);
-        wy = (float)(t1 * r.dy - vy);
-        wz = (float)(t1 * r.dz - vz);
+    float awx = a00 * wx + a01 * wy + a02 * wz;
+    float awy = a01 * wx + a11 * wy + a12 * wz;
+    float awz = a02 * wx + a12 * wy + a22 * wz;
+    float daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
+    float waw = wx * awx + wy * awy + wz * awz;
+    if (REFINE) {
+        // second re-centring, at the estimated peak: there d.A.w vanishes and
+        // w.A.w carries no cancellation even for very anisotropic A
+        t0 = t0 - (double)(daw / dad);
+        wx = (float)(t0 * r.dx - vx);
+        wy = (float)(t0 * r.dy - vy);
+        wz = (float)(t0 * r.dz - vz);
         awx = a00 * wx + a01 * wy + a02 * wz;
         awy = a01 * wx + a11 * wy + a12 * wz;
         awz = a02 * wx + a12 * wy + a22 * wz;
         daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
         waw = wx * awx + wy * awy + wz * awz;
-        if (it == 0) t1 = t1 - (double)(daw * inv_dad);
     }
-    float resid = fmaxf(waw - daw * daw * inv_dad, 0.0f);
+    float resid = fmaxf(waw - daw * daw / dad, 0.0f);
     float mah, t;
     if (MODE == 0) {
-        t = (float)(t1 - (double)(daw * inv_dad));
+        t = (float)(t0 - (double)(daw / dad));
         mah = resid;
     } else {
         t = (float)tc;
-        float s = (float)(tc - t1);
+        float s = (float)(tc - t0);
         float qx = wx + s * r.fdx, qy = wy + s * r.fdy, qz = wz + s * r.fdz;
         mah = qx * (a00 * qx + a01 * qy + a02 * qz) + qy * (a01 * qx + a11 * qy + a12 * qz) +
               qz * (a02 * qx + a12 * qy + a22 * qz);

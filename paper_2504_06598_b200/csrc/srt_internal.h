@@ -33,7 +33,6 @@ struct SrtScene {
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     cudaStream_t stream = nullptr;
-    int64_t *slot_prim_host = nullptr;  // unused placeholder
     srt::SceneView view() const {
         srt::SceneView v;
         v.means64 = d_means;

@@ -454,7 +454,9 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
     ct.add(3, 1);
     RayState r;
     init_ray(r, cam.e[0], cam.e[1], cam.e[2], dd[0], dd[1], dd[2], 0.0, DBL_MAX);
-    Cand c = candidate<MODE>(r, m, a, b, w.s2);
+    // one re-centring: the second (peak) re-centring only matters for extreme
+    // anisotropy and would raise this loop's register count by ~10
+    Cand c = candidate<MODE, RayState, false>(r, m, a, b, w.s2);
     if (!c.valid) return;
     unsigned long long key = pack_hit(c.t, pid);
 #pragma unroll
