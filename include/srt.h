@@ -96,6 +96,17 @@ typedef struct {
     int64_t table_slots;
 } SrtTraceParams;
 
+/* Raw splats (SplatAsset fields, assets.py:60-102) for on-device packing. */
+typedef struct {
+    int64_t n;
+    const double *means;     /* (n, 3) */
+    const double *rotations; /* (n, 4) unit quaternions (w, x, y, z) */
+    const double *scales;    /* (n, 3) > 0 */
+    const double *opacities; /* (n,) */
+    const double *sh;        /* (n, 3, K); may be NULL */
+    int32_t sh_degree;
+} SrtSplatDesc;
+
 /* ---- library ----------------------------------------------------------- */
 const char *srt_last_error(void);      /* thread-local message of the last failure */
 const char *srt_version(void);
@@ -110,6 +121,9 @@ srt_status srt_host_free(void *ptr);
 /* Upload a packed scene to `device` (fp32 SoA records in HBM). */
 srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene **out);
 srt_status srt_scene_destroy(SrtScene *scene);
+/* Upload raw splats and pack them on the device: A = R diag(1/s^2) R^T in
+ * fp64 per primitive (replaces SplatAsset.packed, assets.py:145-171). */
+srt_status srt_scene_create_from_splats(const SrtSplatDesc *desc, int32_t device, SrtScene **out);
 /* Build the GPU LBVH over each primitive's cutoff-ellipsoid AABB
  * (Mahalanobis radius cutoff_s; Morton codes, radix sort, Karras hierarchy,
  * atomic bottom-up refit).  Replaces bvh.build (bvh.py:87-193). */

@@ -133,6 +133,21 @@ def main() -> None:
                                          background=bg))
     np.savez_compressed(OUT / "exact_500.npz", rgb=ex_rgb, opacity=ex_op, frame_rgb=fr.rgb, frame_opacity=fr.opacity,
                         frame_spp=fr.spp)
+
+    # 8. PLY ingest (assets.py:257-370): files written by the reference and the
+    #    arrays its loader returns for them
+    from splatray.assets import load_ply, save_ply
+
+    a = synthetic.random_cloud(300, seed=5, sh_degree=3)
+    save_ply(a, OUT / "splats_300_sh3.ply", binary=True)
+    b = synthetic.random_cloud(60, seed=6, sh_degree=1)
+    save_ply(b, OUT / "splats_60_sh1_ascii.ply", binary=False)
+    out = {}
+    for tag, fname in (("bin", "splats_300_sh3.ply"), ("ascii", "splats_60_sh1_ascii.ply")):
+        got = load_ply(OUT / fname)
+        for f in ("means", "rotations", "scales", "opacities", "sh"):
+            out[f"{tag}_{f}"] = getattr(got, f)
+    np.savez_compressed(OUT / "ply_loaded.npz", **out)
     print("golden fixtures written to", OUT)
 
 

@@ -10,6 +10,7 @@ accumulate pass.  There is no CPU fallback.
 
 from .assets import EmptyAssetError, PackedScene, SplatAsset
 from .config import DEFAULT_CUTOFF, CameraConfig, ConfigError, RenderSettings
+from .ply import PlyFormatError, load_ply, save_ply
 from .render import AccumBuffer, camera_basis, generate_camera_ray, image_metrics, render
 from .sampling import counter_uniform, pixel_jitter
 from .scene import DeviceScene
@@ -20,7 +21,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "AccumBuffer", "CameraConfig", "ConfigError", "DEFAULT_CUTOFF", "DeviceScene", "EmptyAssetError",
-    "PackedScene", "RenderSettings", "SplatAsset", "anisotropic_sheets", "camera_basis", "counter_uniform",
-    "density_cloud", "front_camera", "generate_camera_ray", "image_metrics", "pancake_stack", "pixel_jitter",
-    "random_cloud", "render", "two_layer_scene",
+    "PackedScene", "PlyFormatError", "RenderSettings", "SplatAsset", "anisotropic_sheets", "camera_basis",
+    "counter_uniform", "density_cloud", "front_camera", "generate_camera_ray", "image_metrics", "load_ply",
+    "pancake_stack", "pixel_jitter", "random_cloud", "render", "save_ply", "two_layer_scene",
 ]

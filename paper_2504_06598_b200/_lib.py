@@ -34,6 +34,12 @@ class SrtSceneDesc(ctypes.Structure):
                 ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p), ("sh_degree", ctypes.c_int32)]
 
 
+class SrtSplatDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("means", ctypes.c_void_p), ("rotations", ctypes.c_void_p),
+                ("scales", ctypes.c_void_p), ("opacities", ctypes.c_void_p), ("sh", ctypes.c_void_p),
+                ("sh_degree", ctypes.c_int32)]
+
+
 class SrtCamera(ctypes.Structure):
     _fields_ = [("position", ctypes.c_double * 3), ("right", ctypes.c_double * 3), ("up", ctypes.c_double * 3),
                 ("forward", ctypes.c_double * 3), ("half_w", ctypes.c_double), ("half_h", ctypes.c_double)]
@@ -67,6 +73,7 @@ SYMBOLS = [
     ("srt_host_free", _i32, [_vp]),
     ("srt_scene_create", _i32, [ctypes.POINTER(SrtSceneDesc), _i32, ctypes.POINTER(_vp)]),
     ("srt_scene_destroy", _i32, [_vp]),
+    ("srt_scene_create_from_splats", _i32, [ctypes.POINTER(SrtSplatDesc), _i32, ctypes.POINTER(_vp)]),
     ("srt_bvh_build", _i32, [_vp, _f64]),
     ("srt_bvh_upload", _i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("srt_bvh_info", _i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),

@@ -182,19 +182,24 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 8), "stats alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 8), "stats init");
     if (!rc && n > 0) {
+        // uploads are ordered on the scene's stream: cudaMemcpy from pageable
+        // memory may return before the DMA lands, and the scene's stream does
+        // not synchronise with the legacy default stream
+        cudaStream_t st = s->stream;
         rc = cuda_status(cudaMalloc(&s->d_means, sizeof(double) * n * 3), "means alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_cov6, sizeof(double) * n * 6), "cov alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_opac, sizeof(double) * n), "opacity alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_sh, sizeof(float) * n * 3 * s->sh_k), "sh alloc");
-        if (!rc) rc = cuda_status(cudaMemcpy(s->d_means, desc->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice), "means upload");
-        if (!rc) rc = cuda_status(cudaMemcpy(s->d_cov6, desc->cov_inv6, sizeof(double) * n * 6, cudaMemcpyHostToDevice), "cov upload");
-        if (!rc) rc = cuda_status(cudaMemcpy(s->d_opac, desc->opacities, sizeof(double) * n, cudaMemcpyHostToDevice), "opacity upload");
+        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_means, desc->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st), "means upload");
+        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_cov6, desc->cov_inv6, sizeof(double) * n * 6, cudaMemcpyHostToDevice, st), "cov upload");
+        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_opac, desc->opacities, sizeof(double) * n, cudaMemcpyHostToDevice, st), "opacity upload");
         if (!rc) {
             shf.assign((size_t)n * 3 * s->sh_k, 0.0f);
             if (desc->sh)
                 for (size_t i = 0; i < shf.size(); ++i) shf[i] = (float)desc->sh[i];
-            rc = cuda_status(cudaMemcpy(s->d_sh, shf.data(), sizeof(float) * shf.size(), cudaMemcpyHostToDevice), "sh upload");
+            rc = cuda_status(cudaMemcpyAsync(s->d_sh, shf.data(), sizeof(float) * shf.size(), cudaMemcpyHostToDevice, st), "sh upload");
         }
+        if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "scene upload");
     }
     if (rc) {
         srt_scene_destroy(s);
@@ -202,6 +207,36 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     }
     *out = s;
     return SRT_OK;
+}
+
+srt_status srt_scene_create_from_splats(const SrtSplatDesc *desc, int32_t device, SrtScene **out) {
+    if (!desc || !out || desc->n < 0 || (desc->n > 0 && (!desc->means || !desc->rotations || !desc->scales ||
+                                                         !desc->opacities))) {
+        set_error("invalid splat description");
+        return SRT_ERR_INVALID_ARG;
+    }
+    const int64_t n = desc->n;
+    // create with a placeholder covariance, then pack on the device
+    std::vector<double> zero6((size_t)(n > 0 ? n : 1) * 6, 0.0);
+    SrtSceneDesc d{n, desc->means, zero6.data(), desc->opacities, desc->sh, desc->sh_degree};
+    srt_status rc = srt_scene_create(&d, device, out);
+    if (rc || n == 0) return rc;
+    SrtScene *s = *out;
+    DeviceGuard g(s->device);
+    double *d_q = nullptr, *d_s = nullptr;
+    rc = cuda_status(cudaMalloc(&d_q, sizeof(double) * n * 4), "quaternion alloc");
+    if (!rc) rc = cuda_status(cudaMalloc(&d_s, sizeof(double) * n * 3), "scale alloc");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(d_q, desc->rotations, sizeof(double) * n * 4, cudaMemcpyHostToDevice, s->stream), "q upload");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(d_s, desc->scales, sizeof(double) * n * 3, cudaMemcpyHostToDevice, s->stream), "s upload");
+    if (!rc) rc = launch_pack_splats(n, d_q, d_s, s->d_cov6, s->stream);
+    if (!rc) rc = cuda_status(cudaStreamSynchronize(s->stream), "pack");
+    cudaFree(d_q);
+    cudaFree(d_s);
+    if (rc) {
+        srt_scene_destroy(s);
+        *out = nullptr;
+    }
+    return rc;
 }
 
 srt_status srt_scene_destroy(SrtScene *s) {
@@ -351,8 +386,10 @@ srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const d
     if (!nodes.empty()) {
         rc = cuda_status(cudaMalloc(&s->d_nodes, sizeof(Node2) * nodes.size()), "node alloc");
         if (!rc)
-            rc = cuda_status(cudaMemcpy(s->d_nodes, nodes.data(), sizeof(Node2) * nodes.size(), cudaMemcpyHostToDevice),
+            rc = cuda_status(cudaMemcpyAsync(s->d_nodes, nodes.data(), sizeof(Node2) * nodes.size(),
+                                             cudaMemcpyHostToDevice, s->stream),
                              "node upload");
+        if (!rc) rc = cuda_status(cudaStreamSynchronize(s->stream), "node upload");
     }
     if (!rc && n > 0) {
         // gather the fp64 records on the host in slot order, convert on device
@@ -381,7 +418,11 @@ srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const d
                 gg.b = make_float4((float)cc[4], (float)cc[5], pf, (float)(std::sqrt(tr) * 1.0000002));
             }
             rc = cuda_status(cudaMalloc(&s->d_geom, sizeof(Geom) * n), "geom alloc");
-            if (!rc) rc = cuda_status(cudaMemcpy(s->d_geom, geom.data(), sizeof(Geom) * n, cudaMemcpyHostToDevice), "geom upload");
+            if (!rc)
+                rc = cuda_status(cudaMemcpyAsync(s->d_geom, geom.data(), sizeof(Geom) * n, cudaMemcpyHostToDevice,
+                                                 s->stream),
+                                 "geom upload");
+            if (!rc) rc = cuda_status(cudaStreamSynchronize(s->stream), "geom upload");
         }
     }
     if (rc) return rc;

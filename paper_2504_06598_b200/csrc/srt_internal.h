@@ -79,6 +79,7 @@ float box_hi_f32(double x);
 srt_status lbvh_build(SrtScene *s, double cutoff_s);
 srt_status collapse4(SrtScene *s);
 srt_status scratch_reserve(SrtScene *s, size_t bytes);
+srt_status launch_pack_splats(int64_t n, const double *d_q, const double *d_scales, double *d_cov6, cudaStream_t st);
 
 struct RenderArgs {
     int width, height, passes, nslots, mode, clip;

@@ -90,6 +90,28 @@ class DeviceScene:
     def from_packed(cls, pack, device: int = 0) -> "DeviceScene":
         return cls(pack.means, pack.cov_inv6, pack.opacities, pack.sh, pack.sh_degree, device)
 
+    @classmethod
+    def from_splats(cls, asset, device: int = 0) -> "DeviceScene":
+        """Upload a SplatAsset's raw fields and pack the inverse covariances on
+        the GPU (srt_scene_create_from_splats) instead of via asset.packed."""
+        from ._lib import SrtSplatDesc
+
+        L = _lib.load()
+        _lib.require_device()
+        means, rot, sc = _c64(asset.means), _c64(asset.rotations), _c64(asset.scales)
+        opac, sh = _c64(asset.opacities), _c64(asset.sh)
+        desc = SrtSplatDesc(means.shape[0], means.ctypes.data, rot.ctypes.data, sc.ctypes.data, opac.ctypes.data,
+                            sh.ctypes.data, int(asset.sh_degree))
+        h = ctypes.c_void_p()
+        check(L.srt_scene_create_from_splats(ctypes.byref(desc), int(device), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.n = means.shape[0]
+        self.sh_degree = int(asset.sh_degree)
+        self.device = int(device)
+        self.bvh_key = None
+        return self
+
     # -- lifetime ----------------------------------------------------------
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
