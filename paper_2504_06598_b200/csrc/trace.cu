@@ -948,16 +948,18 @@ static int env_int(const char *name, int dflt);
 template <int NS, int MODE, int RNG, class Src, bool STATS>
 static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
     // SRT_PACKET_CFG (experiments, N=1 mean-depth only): 0 batch 32, entry-
-    // sorted children (default), 1 batch 64, 2 batch 32 + 8 blocks/SM, 3 batch
-    // 64 + 8 blocks/SM, 4 octant-ordered children
+    // sorted children, 7 blocks/SM (default), 1 batch 64, 2 = 0, 3 batch 64 +
+    // 8 blocks/SM, 4 octant-ordered children
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
     if constexpr (NS == 1 && MODE == 0 && !STATS) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
-        if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8>(s, src, w, st);
+        if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
         if (cfg == 4) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 1>(s, src, w, st);
     }
-    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 0>(s, src, w, st);
+    // 7 resident blocks/SM (72 registers, no spills) measured 4% faster than
+    // the unconstrained 80-register build at N=1; larger N keep their registers
+    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, (NS <= 2 ? 7 : 1), 0>(s, src, w, st);
 }
 
 template <int NS, int MODE, int RNG, class Src>
