@@ -124,10 +124,13 @@ srt_status srt_scene_destroy(SrtScene *scene);
 /* Upload raw splats and pack them on the device: A = R diag(1/s^2) R^T in
  * fp64 per primitive (replaces SplatAsset.packed, assets.py:145-171). */
 srt_status srt_scene_create_from_splats(const SrtSplatDesc *desc, int32_t device, SrtScene **out);
-/* Build the GPU LBVH over each primitive's cutoff-ellipsoid AABB
- * (Mahalanobis radius cutoff_s; Morton codes, radix sort, Karras hierarchy,
- * atomic bottom-up refit).  Replaces bvh.build (bvh.py:87-193). */
+/* Build the GPU BVH over each primitive's cutoff-ellipsoid AABB
+ * (Mahalanobis radius cutoff_s), collapsed to 4-wide nodes.  Replaces
+ * bvh.build (bvh.py:87-193).  srt_bvh_build uses SRT_BVH_PLOC. */
+#define SRT_BVH_LBVH 0 /* Morton codes, radix sort, Karras radix tree, atomic refit */
+#define SRT_BVH_PLOC 1 /* Morton order + PLOC agglomerative clustering (better trees) */
 srt_status srt_bvh_build(SrtScene *scene, double cutoff_s);
+srt_status srt_bvh_build_ex(SrtScene *scene, double cutoff_s, int32_t method);
 /* Upload a reference-layout BVH (bvh.py:29-47): node_lo/node_hi (M,3) f64,
  * node_left/node_right/node_count (M,) i64, prim_order (n,) i64,
  * prim_lo/prim_hi (n,3) f64. */

@@ -75,6 +75,7 @@ SYMBOLS = [
     ("srt_scene_destroy", _i32, [_vp]),
     ("srt_scene_create_from_splats", _i32, [ctypes.POINTER(SrtSplatDesc), _i32, ctypes.POINTER(_vp)]),
     ("srt_bvh_build", _i32, [_vp, _f64]),
+    ("srt_bvh_build_ex", _i32, [_vp, _f64, _i32]),
     ("srt_bvh_upload", _i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("srt_bvh_info", _i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),
                             ctypes.POINTER(_i64)]),

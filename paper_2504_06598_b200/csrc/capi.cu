@@ -258,14 +258,16 @@ srt_status srt_scene_destroy(SrtScene *s) {
     return SRT_OK;
 }
 
-srt_status srt_bvh_build(SrtScene *s, double cutoff_s) {
-    if (!s || !(cutoff_s > 0.0) || !std::isfinite(cutoff_s)) {
-        set_error("invalid scene or cutoff");
+srt_status srt_bvh_build_ex(SrtScene *s, double cutoff_s, int32_t method) {
+    if (!s || !(cutoff_s > 0.0) || !std::isfinite(cutoff_s) || (method != SRT_BVH_LBVH && method != SRT_BVH_PLOC)) {
+        set_error("invalid scene, cutoff or build method");
         return SRT_ERR_INVALID_ARG;
     }
     DeviceGuard g(s->device);
-    return lbvh_build(s, cutoff_s);
+    return lbvh_build(s, cutoff_s, method);
 }
+
+srt_status srt_bvh_build(SrtScene *s, double cutoff_s) { return srt_bvh_build_ex(s, cutoff_s, SRT_BVH_PLOC); }
 
 // Reference layout (bvh.py:29-47) -> Node2 tree.  A reference leaf with k
 // primitives becomes a balanced subtree over the k primitive boxes, so the

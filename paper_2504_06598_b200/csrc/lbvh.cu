@@ -15,6 +15,8 @@
 //   5. k_refit        bottom-up: the second thread to reach a node writes
 //                     the node's Node2 (both children's boxes) and its union.
 //   6. k_geom         primitive records permuted into leaf ("slot") order.
+// With method SRT_BVH_PLOC, steps 4-5 are replaced by agglomerative PLOC
+// clustering over the same Morton order (ploc.cu).
 #include <cub/device/device_radix_sort.cuh>
 
 #include "srt_internal.h"
@@ -253,7 +255,7 @@ static srt_status dalloc(T **p, size_t count, const char *what) {
     return SRT_OK;
 }
 
-srt_status lbvh_build(SrtScene *s, double cutoff_s) {
+srt_status lbvh_build(SrtScene *s, double cutoff_s, int method) {
     const int64_t n = s->n;
     cudaStream_t st = s->stream;
     if (s->d_nodes) cudaFree(s->d_nodes);
@@ -330,10 +332,14 @@ srt_status lbvh_build(SrtScene *s, double cutoff_s) {
         SRT_TRY(cuda_status(cudaMemsetAsync(flags, 0, sizeof(int) * m, st), "flags"));
         SRT_TRY(cuda_status(cudaMemsetAsync(ddepth, 0, sizeof(int), st), "depth"));
         SRT_TRY(cuda_status(cudaMemsetAsync(parent_int, 0xFF, sizeof(int) * m, st), "parents"));
-        k_karras<<<(unsigned)((m + B - 1) / B), B, 0, st>>>(n, keys2, children, parent_int, parent_leaf);
-        SRT_TRY(cuda_status(cudaGetLastError(), "k_karras"));
-        k_refit<<<G, B, 0, st>>>(n, children, parent_int, parent_leaf, plo, phi, vals2, ibox, flags, s->d_nodes);
-        SRT_TRY(cuda_status(cudaGetLastError(), "k_refit"));
+        if (method == SRT_BVH_PLOC) {
+            SRT_TRY(ploc_build(s, n, vals2, plo, phi, parent_int, parent_leaf, st));
+        } else {
+            k_karras<<<(unsigned)((m + B - 1) / B), B, 0, st>>>(n, keys2, children, parent_int, parent_leaf);
+            SRT_TRY(cuda_status(cudaGetLastError(), "k_karras"));
+            k_refit<<<G, B, 0, st>>>(n, children, parent_int, parent_leaf, plo, phi, vals2, ibox, flags, s->d_nodes);
+            SRT_TRY(cuda_status(cudaGetLastError(), "k_refit"));
+        }
         k_depth<<<G, B, 0, st>>>(n, parent_int, parent_leaf, ddepth);
         SRT_TRY(cuda_status(cudaGetLastError(), "k_depth"));
         SRT_TRY(cuda_status(cudaMemcpyAsync(&h_depth, ddepth, sizeof(int), cudaMemcpyDeviceToHost, st), "depth"));

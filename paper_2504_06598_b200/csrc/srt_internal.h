@@ -76,7 +76,9 @@ float box_lo_f32(double x);
 float box_hi_f32(double x);
 
 // build / launch helpers (lbvh.cu, trace.cu, shade.cu)
-srt_status lbvh_build(SrtScene *s, double cutoff_s);
+srt_status lbvh_build(SrtScene *s, double cutoff_s, int method);
+srt_status ploc_build(SrtScene *s, int64_t n, const uint32_t *slot_prim, const float *plo, const float *phi,
+                      int *parent_int, int *parent_leaf, cudaStream_t st);
 srt_status collapse4(SrtScene *s);
 srt_status scratch_reserve(SrtScene *s, size_t bytes);
 srt_status launch_pack_splats(int64_t n, const double *d_q, const double *d_scales, double *d_cov6, cudaStream_t st);

@@ -639,7 +639,7 @@ template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int 
 __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
                                                                        int *overflow, unsigned long long *stats) {
     constexpr int W = kTraceThreads / 32;
-    constexpr int PSTACK = 64;
+    constexpr int PSTACK = 128;
     __shared__ float4 sdir[W][32];      // fp32 direction + far bound of each lane's ray
     __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
     __shared__ unsigned long long sbest[W][32][NS];

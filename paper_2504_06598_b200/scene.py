@@ -131,9 +131,13 @@ class DeviceScene:
         return self._h
 
     # -- BVH -----------------------------------------------------------------
-    def build_bvh(self, cutoff_s: float) -> None:
-        """GPU LBVH over the cutoff-ellipsoid boxes (srt_bvh_build)."""
-        check(_lib.load().srt_bvh_build(self.handle, float(cutoff_s)))
+    def build_bvh(self, cutoff_s: float, method: str = "ploc") -> None:
+        """GPU BVH over the cutoff-ellipsoid boxes (srt_bvh_build_ex): "ploc"
+        (agglomerative clustering, default) or "lbvh" (Karras radix tree)."""
+        methods = {"lbvh": 0, "ploc": 1}
+        if method not in methods:
+            raise ValueError(f"unknown BVH build method {method!r}")
+        check(_lib.load().srt_bvh_build_ex(self.handle, float(cutoff_s), methods[method]))
         self.bvh_key = ("lbvh", float(cutoff_s))
 
     def upload_bvh(self, bvh) -> None:

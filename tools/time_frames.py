@@ -18,10 +18,20 @@ asset = density_cloud(n) if n > 10_000 else random_cloud(n, sh_degree=0)
 st = RenderSettings(width=W, height=H, spp=spp, multisample=N)
 sc = prepare(asset, st)
 import os
+if os.environ.get("SRT_BVH_METHOD"):
+    sc.build_bvh(st.cutoff_s, method=os.environ["SRT_BVH_METHOD"])
 if os.environ.get("SRT_SAH") == "1":
     from oracle import oracle as O
     lo, hi = asset.aabb_arrays(st.cutoff_s)
-    sc.upload_bvh(O.sah_build(lo, hi, leaf_size=int(os.environ.get("SRT_SAH_LEAF", "1"))))
+    if os.environ.get("SRT_SAH_TIGHT") == "1":  # ellipsoid AABBs, as the LBVH uses
+        import numpy as np
+        half = st.cutoff_s * np.sqrt(np.einsum("nii->ni", np.linalg.inv(asset.packed.cov_inv)))
+        lo, hi = asset.means - half, asset.means + half
+    import time as _t
+    _t0 = _t.time()
+    ob = O.sah_build(lo, hi, leaf_size=int(os.environ.get("SRT_SAH_LEAF", "1")))
+    print("host SAH build", _t.time() - _t0)
+    sc.upload_bvh(ob)
 cam = make_camera(camera_tuple(front_camera(), W, H))
 prm = make_render_params(W, H, st.passes, N, 0, st.cutoff_s ** 2)
 t = shard_tiles(W, H)
@@ -51,5 +61,8 @@ if os.environ.get("SRT_TRACE_STATS") == "1":
     w = max(d["walks"], 1)
     print("per walk:", {k: round(v / w, 2) for k, v in d.items()})
 walks = W * H * st.passes
+import time as _tt
+_t0 = _tt.time(); sc.build_bvh(st.cutoff_s, method=os.environ.get("SRT_BVH_METHOD", "ploc")); _bt = _tt.time() - _t0
+print(f"build {_bt*1e3:.1f} ms", end="  ")
 print(f"n={n} {W}x{H} spp={spp} N={N}: trace {tt[len(tt)//2]:.3f} ms ({walks/tt[len(tt)//2]/1e3:.1f} Mwalks/s, "
       f"{walks*N/tt[len(tt)//2]/1e3:.1f} Msamples/s) shade {ts[len(ts)//2]:.3f} ms  bvh {sc.bvh_info()}")
