@@ -213,11 +213,10 @@ def run_ours(args) -> None:
         if ev is not None:
             ev[0].record(stream)
         for f in range(st.passes):
-            sc.trace_pass_device(cam, prm, f, hits.data_ptr(), sp)
-            if ev is not None and f == st.passes - 1:
-                ev[1].record(stream)
-            sc.shade_pass_device(cam, prm, f, hits.data_ptr(), acc.data_ptr(), f == 0, f == st.passes - 1,
-                                 out.data_ptr(), sp)
+            # one fused kernel per pass: packet walk + SH shade + accumulate
+            sc.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), sp)
+        if ev is not None:
+            ev[1].record(stream)
         if world > 1:
             dist.gather(out, gathered if rank == 0 else None, dst=0)
             if rank == 0:
@@ -306,12 +305,12 @@ def run_ours(args) -> None:
                        "ms_per_frame": ms_per_step, "wall_s_timed_region": wall},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic_per_launch(),
-                         "kernel": "k_trace_pass", "kernel_ms": trace_avg_ms,
+                         "kernel": "k_trace_packet (fused walk + SH shade + accumulate)", "kernel_ms": trace_avg_ms,
                          "algorithmic_bytes_per_walk": BYTES_PER_WALK, "walks_per_launch": walks_per_launch,
                          "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * st.passes * 2 + (args.steps if world > 1 else 0),
+            "gpu_launches": args.steps * st.passes + (args.steps if world > 1 else 0),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

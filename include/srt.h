@@ -196,6 +196,12 @@ srt_status srt_shade_pass_device(const SrtScene *scene, const SrtCamera *camera,
                                  const SrtRenderParams *params, int32_t pass,
                                  const int32_t *d_hits, float *d_accum, int32_t first,
                                  int32_t last, float *d_out, void *stream);
+/* One pass traced AND shaded by a single kernel (the walk's hits are
+ * SH-shaded and accumulated in place; no hit buffer).  Same d_accum/first/
+ * last/d_out contract as srt_shade_pass_device. */
+srt_status srt_render_pass_device(const SrtScene *scene, const SrtCamera *camera,
+                                  const SrtRenderParams *params, int32_t pass, float *d_accum,
+                                  int32_t first, int32_t last, float *d_out, void *stream);
 /* Whole frame on device: all passes, d_out (H*W) float4 rgba means. */
 srt_status srt_render_device(const SrtScene *scene, const SrtCamera *camera,
                              const SrtRenderParams *params, int32_t *d_hits, float *d_accum,

@@ -745,6 +745,23 @@ srt_status srt_shade_pass_device(const SrtScene *s, const SrtCamera *camera, con
                              last != 0, (float4 *)d_out, (cudaStream_t)stream);
 }
 
+srt_status srt_render_pass_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t pass,
+                                  float *d_accum, int32_t first, int32_t last, float *d_out, void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_accum || (last && !d_out)) {
+        set_error("null camera or buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (p->rng == SRT_RNG_TRIG64) {
+        set_error("the fused pass draws the counter stream; use the trace/shade entry points for trig64");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return launch_render_pass_fused(s, make_cam(camera), make_render_args(p), pass, (float4 *)d_accum, first != 0,
+                                    last != 0, (float4 *)d_out, (cudaStream_t)stream);
+}
+
 srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t *d_hits,
                              float *d_accum, float *d_out, void *stream) {
     srt_status rc = validate_render(s, p);
@@ -759,10 +776,15 @@ srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const S
     cudaStream_t st = (cudaStream_t)stream;
     for (int f = 0; f < p->passes && !rc; ++f) {
         int pass = p->pass0 + f;
-        rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
-        if (!rc)
-            rc = launch_shade_pass(s, cam, a, pass, d_hits, (float4 *)d_accum, f == 0, f == p->passes - 1,
-                                   (float4 *)d_out, st);
+        if (a.rng == SRT_RNG_TRIG64) {
+            rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
+            if (!rc)
+                rc = launch_shade_pass(s, cam, a, pass, d_hits, (float4 *)d_accum, f == 0, f == p->passes - 1,
+                                       (float4 *)d_out, st);
+        } else {
+            rc = launch_render_pass_fused(s, cam, a, pass, (float4 *)d_accum, f == 0, f == p->passes - 1,
+                                          (float4 *)d_out, st);
+        }
     }
     return rc;
 }
@@ -801,6 +823,10 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     double *d_op = d_rgb + npix * 3;
     for (int f = 0; f < p->passes && !rc; ++f) {
         int pass = p->pass0 + f;
+        if (a.rng != SRT_RNG_TRIG64 && !(out_ids && f == 0)) {
+            rc = launch_render_pass_fused(s, cam, a, pass, d_acc, f == 0, f == p->passes - 1, d_out, st);
+            continue;
+        }
         rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
         if (!rc && out_ids && f == 0) {
             // slot ids of the first pass, un-tiled on the host

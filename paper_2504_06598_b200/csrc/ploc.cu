@@ -8,13 +8,15 @@
 // better than the Karras radix tree for traversal.
 // Node2 records are written as the merges happen (both child boxes are known),
 // so no refit pass is needed; the last merge becomes node 0, the root.
+#include <cstdlib>
+
 #include <cub/device/device_scan.cuh>
 
 #include "srt_internal.h"
 
 namespace srt {
 
-constexpr int kPlocRadius = 16;
+constexpr int kPlocRadius = 16;  // neighbourhood half-width (SRT_PLOC_RADIUS overrides, experiments)
 
 __device__ __forceinline__ float half_area(float4 lo, float4 hi) {
     float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
@@ -31,13 +33,13 @@ __global__ void k_ploc_init(int64_t n, const uint32_t *__restrict__ slot_prim, c
     hi[j] = make_float4(phi[p * 3], phi[p * 3 + 1], phi[p * 3 + 2], 0.f);
 }
 
-__global__ void k_ploc_nn(int nc, const float4 *__restrict__ lo, const float4 *__restrict__ hi, int *nn) {
+__global__ void k_ploc_nn(int nc, int radius, const float4 *__restrict__ lo, const float4 *__restrict__ hi, int *nn) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nc) return;
     float4 l = lo[i], h = hi[i];
     float best = INFINITY;
     int bj = (i ^ 1) < nc ? (i ^ 1) : i - 1;
-    int j0 = max(0, i - kPlocRadius), j1 = min(nc - 1, i + kPlocRadius);
+    int j0 = max(0, i - radius), j1 = min(nc - 1, i + radius);
     for (int j = j0; j <= j1; ++j) {
         if (j == i) continue;
         float4 l2 = lo[j], h2 = hi[j];
@@ -110,6 +112,8 @@ srt_status ploc_build(SrtScene *s, int64_t n, const uint32_t *slot_prim, const f
     size_t temp_bytes = 0;
     int nc = (int)n;
     const int B = 256;
+    const char *env = getenv("SRT_PLOC_RADIUS");
+    const int radius = env ? max(1, atoi(env)) : kPlocRadius;
     rc = cuda_status(cudaMalloc(&code, sizeof(int) * n), "ploc alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&code2, sizeof(int) * n), "ploc alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&nn, sizeof(int) * n), "ploc alloc");
@@ -129,7 +133,7 @@ srt_status ploc_build(SrtScene *s, int64_t n, const uint32_t *slot_prim, const f
     }
     while (!rc && nc > 1) {
         unsigned g = (unsigned)((nc + B - 1) / B);
-        k_ploc_nn<<<g, B, 0, st>>>(nc, lo, hi, nn);
+        k_ploc_nn<<<g, B, 0, st>>>(nc, radius, lo, hi, nn);
         k_ploc_merge<<<g, B, 0, st>>>(nc, n, nn, code, lo, hi, code2, lo2, hi2, keep, counter, s->d_nodes,
                                      parent_int, parent_leaf);
         rc = cuda_status(cudaMemsetAsync(keep + nc, 0, sizeof(int), st), "ploc keep tail");

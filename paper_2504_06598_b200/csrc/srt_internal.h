@@ -100,6 +100,9 @@ CamD make_cam(const SrtCamera *c);
 
 srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
                              cudaStream_t st);
+srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
+                                   float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
+                                   int32_t *d_hits = nullptr);
 srt_status launch_shade_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                              const int32_t *d_hits, float4 *d_accum, bool first, bool last, float4 *d_out,
                              cudaStream_t st);

@@ -285,12 +285,56 @@ struct CameraSource {
         for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, (uint32_t)pass * (uint32_t)a.nslots + k);
         return true;
     }
+    // fused shading (hits == nullptr): accumulate straight from the walk
+    float4 *accum;
+    float4 *out;
+    int first, last;
     template <int NS>
     __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
         int32_t *h = hits + (int64_t)idx * a.nslots;
 #pragma unroll
         for (int k = 0; k < NS; ++k)
             if (k < a.nslots) h[k] = sl.id[k];
+    }
+    // Walk result -> either the hit buffer (split trace/shade) or, fused, the
+    // SH colour of every slot's hit on this ray's direction plus background
+    // for misses, accumulated exactly as k_shade_pass does (kernels.py:657-673).
+    template <int NS>
+    __device__ __forceinline__ void finish_shaded(uint32_t idx, const Slots<NS> &sl, const SceneView &s, float fx,
+                                                  float fy, float fz) const {
+        if (hits) {
+            finish<NS>(idx, sl);
+            return;
+        }
+        float r = 0.f, g = 0.f, b = 0.f, o = 0.f;
+        for (int k = 0; k < NS && k < a.nslots; ++k) {
+            int pid = sl.id[k];
+            if (pid >= 0) {
+                float3 c = sh_color(s.sh, s.sh_k, s.sh_deg, pid, fx, fy, fz);
+                r += c.x;
+                g += c.y;
+                b += c.z;
+                o += 1.0f;
+            } else {
+                r += a.bg[0];
+                g += a.bg[1];
+                b += a.bg[2];
+            }
+        }
+        float4 acc = first ? make_float4(0.f, 0.f, 0.f, 0.f) : accum[idx];
+        acc.x += r;
+        acc.y += g;
+        acc.z += b;
+        acc.w += o;
+        if (last) {
+            float inv = 1.0f / ((float)a.passes * (float)a.nslots);
+            int px, py;
+            tile_pixel(a, idx >> 8, idx & 255, px, py);
+            int64_t oidx = a.shard_count > 1 ? (int64_t)idx : (int64_t)py * a.width + px;
+            out[oidx] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        } else {
+            accum[idx] = acc;
+        }
     }
 };
 
@@ -321,6 +365,11 @@ struct ArraySource {
                 out_t[(int64_t)idx * nslots + k] = sl.id[k] >= 0 ? sl.t[k] : INFINITY;
                 out_id[(int64_t)idx * nslots + k] = sl.id[k];
             }
+    }
+    template <int NS>
+    __device__ __forceinline__ void finish_shaded(uint32_t idx, const Slots<NS> &sl, const SceneView &, float, float,
+                                                  float) const {
+        finish<NS>(idx, sl);
     }
 };
 
@@ -371,7 +420,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace(SceneView s, Src src, W
             if (wk.next >= 0) wk.next = visit_node<NS, MODE, RNG, STATS>(s, r, w, wk, sl, wk.next, overflow, ct);
             if (wk.next < 0) {
                 ct.add(7, 1);
-                src.template finish<NS>(idx, sl);
+                src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz);
                 active = false;
             }
         }
@@ -615,7 +664,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
                     sl.id[k] = (int)(unsigned)v;
                     sl.t[k] = unpack_t(v);
                 }
-                src.template finish<NS>(idx, sl);
+                src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz);
                 ct.add(7, 1);
                 active = false;
             }
@@ -851,7 +900,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 sl.id[k] = (int)(unsigned)v;
                 sl.t[k] = unpack_t(v);
             }
-            src.template finish<NS>(idx, sl);
+            src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz);
         }
         __syncwarp();
     }
@@ -1003,7 +1052,19 @@ static srt_status dispatch(const SrtScene *s, const Src &src, const WalkCfg &w, 
 srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, int32_t *d_hits,
                              cudaStream_t st) {
     if (a.rng == SRT_RNG_TRIG64) return launch_trace_pass_trig64(s, cam, a, pass, (double)a.s2d, d_hits, st);
+    return launch_render_pass_fused(s, cam, a, pass, nullptr, false, false, nullptr, st, d_hits);
+}
+
+// One pass traced AND shaded by the packet kernel (d_hits == nullptr), or
+// traced into d_hits for a separate k_shade_pass.
+srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
+                                   float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
+                                   int32_t *d_hits) {
     CameraSource src;
+    src.accum = d_accum;
+    src.out = d_out;
+    src.first = first ? 1 : 0;
+    src.last = last ? 1 : 0;
     src.cam = cam;
     src.a = a;
     src.pass = pass;

@@ -263,6 +263,12 @@ class DeviceScene:
                                                 int(bool(first)), int(bool(last)), ctypes.c_void_p(d_out),
                                                 ctypes.c_void_p(stream)))
 
+    def render_pass_device(self, camera, prm, pass_index, d_accum, first, last, d_out, stream) -> None:
+        """One pass traced and shaded by a single kernel (srt_render_pass_device)."""
+        check(_lib.load().srt_render_pass_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),
+                                                 int(pass_index), ctypes.c_void_p(d_accum), int(bool(first)),
+                                                 int(bool(last)), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)))
+
     def render_device(self, camera, prm, d_hits, d_accum, d_out, stream) -> None:
         check(_lib.load().srt_render_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),
                                             ctypes.c_void_p(d_hits), ctypes.c_void_p(d_accum),

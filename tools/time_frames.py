@@ -44,13 +44,19 @@ for _ in range(3):
     sc.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(), s)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 tt, ts = [], []
+fused = os.environ.get("SRT_SPLIT") != "1"
 for _ in range(reps):
     flush.fill_(1)
     ev[0].record()
-    for f in range(st.passes):
-        sc.trace_pass_device(cam, prm, f, hits.data_ptr(), s)
-    ev[1].record()
-    sc.shade_pass_device(cam, prm, 0, hits.data_ptr(), acc.data_ptr(), True, True, out.data_ptr(), s)
+    if fused:
+        for f in range(st.passes):
+            sc.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), s)
+        ev[1].record()
+    else:
+        for f in range(st.passes):
+            sc.trace_pass_device(cam, prm, f, hits.data_ptr(), s)
+        ev[1].record()
+        sc.shade_pass_device(cam, prm, 0, hits.data_ptr(), acc.data_ptr(), True, True, out.data_ptr(), s)
     ev[2].record()
     torch.cuda.synchronize()
     tt.append(ev[0].elapsed_time(ev[1]))
