@@ -323,3 +323,17 @@ def test_render_distributed_single_rank_equals_render(mode):
     np.testing.assert_allclose(got.rgb, want.rgb, rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(got.opacity, want.opacity, rtol=1e-6, atol=1e-6)
     assert got.spp == want.spp
+
+
+@pytest.mark.slow
+def test_c5_scale_6m_vs_oracle(oracle):
+    """configs[4] scale (6M density-preserving SH3 Gaussians, 1080p): ids of a
+    16x16-strided sample (8,100 rays) against the oracle; PLOC build of 6M."""
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    asset = density_cloud(6_000_000)
+    (rgb, op, ids), ref = _render_both(oracle, asset, 1920, 1080, spp=1, stride=(16, 16))
+    sub = (slice(None, None, 16), slice(None, None, 16))
+    agree = ids[sub] == ref["ids"][sub]
+    assert agree.mean() >= ID_AGREE, agree.mean()
+    _check_colours(rgb[sub], ref["rgb"][sub], np.all(agree, axis=2))
