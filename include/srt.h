@@ -20,6 +20,8 @@
  *   kernels.transmittance_batch kernels.py:544-557 -> srt_transmittance_rays
  *   kernels.exact_batch        kernels.py:584-604  -> srt_exact_rays
  *   kernels.render_exact       kernels.py:677-723  -> srt_render_exact
+ *   kernels.biased_batch       kernels.py:561-580  -> srt_biased_rays
+ *   cli._biased_frame          cli.py:164-203      -> srt_render_biased
  *   (new) multi-GPU tile gather                    -> srt_unpack_tiles_device
  */
 #ifndef SRT_H
@@ -175,6 +177,24 @@ srt_status srt_exact_rays(const SrtScene *scene, const double *origins, const do
  * (H,W,3) and (H,W) f64. */
 srt_status srt_render_exact(const SrtScene *scene, const SrtCamera *camera,
                             const SrtRenderParams *params, double *out_rgb, double *out_op);
+
+/* ---- biased k-nearest composite (kernels.biased_batch) ------------------- */
+/* One acceptance draw per candidate (slot 0 of the ray's stream: counter key
+ * (seed, ray_id0+i, sample0), table column 0, or the reference trig hash with
+ * SRT_RNG_TRIG64); the kk nearest accepted candidates, sorted by (t, prim id),
+ * are composited front to back with their own alphas over `background`
+ * (kernels.py:479-518, 561-580).  kk >= 1; params->nslots/clip are ignored.
+ * out_rgb (R,3) f64.  More than 256 accepted with kk > 256 ->
+ * SRT_ERR_STACK_OVERFLOW. */
+srt_status srt_biased_rays(const SrtScene *scene, const SrtTraceParams *params, const double *origins,
+                           const double *dirs, int64_t num_rays, int32_t kk, const double *background,
+                           double *out_rgb);
+/* The cli's --compare-biased frame (cli.py:164-203): per-pixel mean over
+ * params->passes jittered camera rays of the biased composite.  Counter draw
+ * of pixel (px,py), pass f: (seed, py*W+px, f); params->rng SRT_RNG_TRIG64
+ * uses the reference hash.  Host output (H,W,3) f64. */
+srt_status srt_render_biased(const SrtScene *scene, const SrtCamera *camera, const SrtRenderParams *params,
+                             int32_t kk, double *out_rgb);
 
 /* ---- full frames (kernels.render_stochastic) ----------------------------- */
 /* Host outputs out_rgb (H,W,3) f64 and out_op (H,W) f64 = per-pixel means.

@@ -148,8 +148,41 @@ def main() -> None:
         for f in ("means", "rotations", "scales", "opacities", "sh"):
             out[f"{tag}_{f}"] = getattr(got, f)
     np.savez_compressed(OUT / "ply_loaded.npz", **out)
+    biased()
     print("golden fixtures written to", OUT)
 
 
+def biased() -> None:
+    """9. biased k-nearest composite (kernels.py:479-518, 561-580): the
+    reference's `--compare-biased` baseline on the trace_400 rays."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, REF)
+    from splatray import kernels, synthetic
+
+    tmax = float(np.finfo(np.float64).max)
+    s2 = 8.0
+    t = np.load(OUT / "trace_400.npz")
+    origins, dirs = t["origins"], t["dirs"]
+    a = synthetic.random_cloud(500, seed=41, sh_degree=2)
+    pk = a.packed
+    bg = np.array([0.15, 0.25, 0.35])
+    res = {}
+    for mode in (0, 1):
+        for kk in (1, 2, 5):
+            out = np.empty((origins.shape[0], 3))
+            kernels.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, origins, dirs, 0.0, tmax,
+                                 mode, s2, kk, bg[0], bg[1], bg[2], out)
+            res[f"rgb_m{mode}_k{kk}"] = out
+    # the cli's frame-level baseline (cli.py:164-203) on a small frame
+    from splatray import cli
+    from splatray.config import RenderSettings
+
+    cam = synthetic.front_camera()
+    for kk in (1, 3):
+        st = RenderSettings(width=20, height=16, spp=2, seed=5, background=bg)
+        res[f"frame_k{kk}"] = cli._biased_frame(a, cam, st, kk)
+    np.savez_compressed(OUT / "biased_500.npz", **res)
+
+
 if __name__ == "__main__":
-    main()
+    biased() if sys.argv[1:] == ["biased"] else main()

@@ -90,6 +90,10 @@ def lib() -> ctypes.CDLL:
         L.srt_oracle_exact_batch.restype = None
         L.srt_oracle_exact_batch.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _i64, _f64p, _f64p, _i64, _dbl, _dbl,
                                              _int, _dbl, _f64p, _f64p, _f64p, _int]
+        L.srt_oracle_biased_batch.restype = None
+        L.srt_oracle_biased_batch.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _i64, _f64p, _f64p, _i64, _dbl, _dbl,
+                                              _int, _dbl, _i64, _f64p, _int, ctypes.c_uint32, ctypes.c_uint32,
+                                              ctypes.c_uint32, _f64p, _i64, _f64p, _int]
         L.srt_oracle_render_exact.restype = None
         L.srt_oracle_render_exact.argtypes = [_f64p, _f64p, _f64p, _f64p, _i64, _i64, _f64p, _i64, _i64, _i64, _int,
                                               _dbl, _i64, _f64p, _f64p, _f64p, _int]
@@ -317,6 +321,25 @@ def exact_batch(means, cov6, opac, sh, deg, origins, dirs, t_min=0.0, t_max=TMAX
                                  _p(dirs), origins.shape[0], float(t_min), float(t_max), int(mode), float(s2), _p(bg),
                                  _p(rgb), _p(op), int(threads))
     return rgb, op
+
+
+def biased_batch(means, cov6, opac, sh, deg, origins, dirs, kk, t_min=0.0, t_max=TMAX, mode=0, s2=8.0,
+                 background=(0.0, 0.0, 0.0), rng="trig", seed=0, ray_id0=0, sample0=0, table=None, threads=0):
+    """kernels.biased_batch (kernels.py:561-580): brute force, one draw per
+    candidate, kk nearest accepted composited.  rng "trig" is the reference."""
+    means, cov6, opac, sh = (_c(x, np.float64) for x in (means, cov6, opac, sh))
+    origins = _c(origins, np.float64).reshape(-1, 3)
+    dirs = _c(dirs, np.float64).reshape(-1, 3)
+    bg = _c(background, np.float64)
+    tab = _c(table if table is not None else np.zeros((1, 1)), np.float64)
+    if tab.ndim == 1:
+        tab = tab.reshape(-1, 1)
+    rgb = np.empty((origins.shape[0], 3))
+    lib().srt_oracle_biased_batch(_p(means), _p(cov6), _p(opac), _p(sh), means.shape[0], int(deg), _p(origins),
+                                  _p(dirs), origins.shape[0], float(t_min), float(t_max), int(mode), float(s2),
+                                  int(kk), _p(bg), RNG_MODES[rng], seed & 0xFFFFFFFF, ray_id0 & 0xFFFFFFFF,
+                                  sample0 & 0xFFFFFFFF, _p(tab), tab.shape[1], _p(rgb), int(threads))
+    return rgb
 
 
 def render_exact(means, cov6, opac, sh, deg, cam, width, height, frames=1, mode=0, s2=8.0, seed=0,

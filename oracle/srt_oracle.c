@@ -922,6 +922,76 @@ void srt_oracle_exact_batch(const double *means, const double *cov6, const doubl
     }
 }
 
+/* kernels.py:479-518 (_biased_ray): one draw per valid candidate (slot 0),
+ * the kk nearest accepted composited with their own alphas.  rng selects the
+ * draw: SRT_RNG_TRIG (the reference's hash), COUNTER (key from seed,
+ * ray_id0 + i, sample0) or TABLE (table[pid * table_slots]). */
+static void biased_ray(const Scene *sc, double ox, double oy, double oz, double dx, double dy, double dz,
+                       double t_min, double t_max, int mode, double s2, int64_t kk, const double *bg,
+                       const TraceCfg *cfg, uint32_t key, double *t_buf, double *a_buf, int64_t *id_buf,
+                       int64_t *order, int64_t *tmp, double *out3) {
+    int64_t m = 0;
+    for (int64_t pid = 0; pid < sc->n; ++pid) {
+        double t = 0, resid = 0, hx, hy, hz;
+        if (!candidate(sc, pid, ox, oy, oz, dx, dy, dz, mode, s2, &t, &resid, &hx, &hy, &hz) || t <= t_min ||
+            t >= t_max)
+            continue;
+        double alpha = sc->opac[pid] * exp(-0.5 * resid);
+        if (draw(cfg, pid, 0, hx, hy, hz, &key) < alpha) {
+            t_buf[m] = t;
+            a_buf[m] = alpha;
+            id_buf[m] = pid;
+            m++;
+        }
+    }
+    stable_argsort(t_buf, order, tmp, m);
+    double r = 0.0, g = 0.0, b = 0.0, trans = 1.0;
+    int64_t take = m < kk ? m : kk;
+    for (int64_t i = 0; i < take; ++i) {
+        int64_t j = order[i];
+        double alpha = a_buf[j], col[3];
+        srt_oracle_sh_color(sc->sh, sc->deg, id_buf[j], dx, dy, dz, col);
+        double w = trans * alpha;
+        r += w * col[0];
+        g += w * col[1];
+        b += w * col[2];
+        trans *= 1.0 - alpha;
+    }
+    out3[0] = r + trans * bg[0];
+    out3[1] = g + trans * bg[1];
+    out3[2] = b + trans * bg[2];
+}
+
+/* kernels.py:561-580 */
+void srt_oracle_biased_batch(const double *means, const double *cov6, const double *opac, const double *sh,
+                             int64_t n, int64_t deg, const double *origins, const double *dirs, int64_t R,
+                             double t_min, double t_max, int mode, double s2, int64_t kk, const double *bg,
+                             int rng, uint32_t seed, uint32_t ray_id0, uint32_t sample0, const double *table,
+                             int64_t table_slots, double *out_rgb, int threads) {
+    Scene sc = {means, cov6, opac, sh, n, deg};
+    TraceCfg cfg = {mode, s2, 0, rng, seed, table, table_slots};
+    set_threads(threads);
+#pragma omp parallel
+    {
+        size_t cap = (size_t)(n > 0 ? n : 1);
+        double *t_buf = (double *)malloc(sizeof(double) * cap), *a_buf = (double *)malloc(sizeof(double) * cap);
+        int64_t *id_buf = (int64_t *)malloc(sizeof(int64_t) * cap), *order = (int64_t *)malloc(sizeof(int64_t) * cap),
+                *tmp = (int64_t *)malloc(sizeof(int64_t) * cap);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < R; ++i) {
+            uint32_t key = srt_oracle_walk_key(seed, ray_id0 + (uint32_t)i, sample0);
+            biased_ray(&sc, origins[i * 3], origins[i * 3 + 1], origins[i * 3 + 2], dirs[i * 3], dirs[i * 3 + 1],
+                       dirs[i * 3 + 2], t_min, t_max, mode, s2, kk, bg, &cfg, key, t_buf, a_buf, id_buf, order, tmp,
+                       out_rgb + i * 3);
+        }
+        free(t_buf);
+        free(a_buf);
+        free(id_buf);
+        free(order);
+        free(tmp);
+    }
+}
+
 /* kernels.py:677-723 (render_exact): per-pixel mean over `frames` jittered rays */
 void srt_oracle_render_exact(const double *means, const double *cov6, const double *opac, const double *sh,
                              int64_t n, int64_t deg, const double *cam, int64_t width, int64_t height,

@@ -11,7 +11,7 @@ accumulate pass.  There is no CPU fallback.
 from .assets import EmptyAssetError, PackedScene, SplatAsset
 from .config import DEFAULT_CUTOFF, CameraConfig, ConfigError, RenderSettings
 from .ply import PlyFormatError, load_ply, save_ply
-from .render import AccumBuffer, camera_basis, generate_camera_ray, image_metrics, render
+from .render import AccumBuffer, camera_basis, generate_camera_ray, image_metrics, render, render_biased
 from .sampling import counter_uniform, pixel_jitter
 from .scene import DeviceScene
 from .synthetic import (anisotropic_sheets, density_cloud, front_camera, pancake_stack, random_cloud,
@@ -23,5 +23,5 @@ __all__ = [
     "AccumBuffer", "CameraConfig", "ConfigError", "DEFAULT_CUTOFF", "DeviceScene", "EmptyAssetError",
     "PackedScene", "PlyFormatError", "RenderSettings", "SplatAsset", "anisotropic_sheets", "camera_basis",
     "counter_uniform", "density_cloud", "front_camera", "generate_camera_ray", "image_metrics", "load_ply",
-    "pancake_stack", "pixel_jitter", "random_cloud", "render", "save_ply", "two_layer_scene",
+    "pancake_stack", "pixel_jitter", "random_cloud", "render", "render_biased", "save_ply", "two_layer_scene",
 ]

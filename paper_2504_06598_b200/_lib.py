@@ -84,6 +84,8 @@ SYMBOLS = [
     ("srt_trace_rays_device", _i32, [_vp, ctypes.POINTER(SrtTraceParams), _vp, _i64, _i32, _vp, _vp, _vp]),
     ("srt_transmittance_rays", _i32, [_vp, _vp, _vp, _i64, _f64, _f64, _i32, _f64, _vp]),
     ("srt_exact_rays", _i32, [_vp, _vp, _vp, _i64, _f64, _f64, _i32, _f64, _vp, _vp, _vp]),
+    ("srt_biased_rays", _i32, [_vp, ctypes.POINTER(SrtTraceParams), _vp, _vp, _i64, _i32, _vp, _vp]),
+    ("srt_render_biased", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _i32, _vp]),
     ("srt_render_exact", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp]),
     ("srt_render", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp]),
     ("srt_trace_pass_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _i32, _vp,

@@ -690,6 +690,62 @@ srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const doubl
     return rc;
 }
 
+srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const double *origins, const double *dirs,
+                           int64_t R, int32_t kk, const double *background, double *out_rgb) {
+    srt_status rc = validate_trace(sc, p, R, 1);
+    if (rc) return rc;
+    if (kk < 1 || !background || (R > 0 && (!origins || !dirs || !out_rgb))) {
+        set_error("invalid biased-composite parameters (k must be >= 1)");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (R == 0) return SRT_OK;
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    size_t ray_bytes = sizeof(double) * R * 6;
+    size_t rgb_bytes = sizeof(double) * R * 3;
+    size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
+    rc = scratch_reserve(s, ray_bytes + rgb_bytes + table_bytes);
+    if (rc) return rc;
+    double *d_rays = (double *)s->d_scratch;
+    double *d_rgb = d_rays + R * 6;
+    double *d_table = table_bytes ? d_rgb + R * 3 : nullptr;
+    std::vector<double> packed((size_t)R * 6);
+    for (int64_t i = 0; i < R; ++i)
+        for (int k = 0; k < 3; ++k) {
+            packed[i * 6 + k] = origins[i * 3 + k];
+            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
+        }
+    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    if (!rc && d_table)
+        rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
+    if (!rc) rc = launch_biased_rays(s, p, d_rays, R, kk, background, d_table, d_rgb, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, rgb_bytes, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
+srt_status srt_render_biased(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, int32_t kk,
+                             double *out_rgb) {
+    srt_status rc = validate_render(sc, p);
+    if (rc) return rc;
+    if (!camera || !out_rgb || kk < 1 || p->rng == SRT_RNG_TABLE) {
+        set_error("invalid biased-frame parameters (k >= 1; counter or trig64 draws)");
+        return SRT_ERR_INVALID_ARG;
+    }
+    SrtScene *s = const_cast<SrtScene *>(sc);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream;
+    const int64_t npix = (int64_t)p->width * p->height;
+    rc = scratch_reserve(s, sizeof(double) * npix * 3);
+    if (rc) return rc;
+    double *d_rgb = (double *)s->d_scratch;
+    rc = launch_biased_frame(s, make_cam(camera), p, kk, d_rgb, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = check_flag(s, st);
+    return rc;
+}
+
 srt_status srt_render_exact(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
                             double *out_op) {
     srt_status rc = validate_render(sc, p);

@@ -10,10 +10,51 @@
 #include <cfloat>
 
 #include "srt_internal.h"
+#include "srt_trig64.cuh"
 
 namespace srt {
 
 constexpr int kExactCap = 512;  // candidates per ray (overflow -> SRT_ERR_STACK_OVERFLOW)
+
+// Every leaf primitive whose conservative box the ray crosses inside
+// [t_min, t_max0], in no particular order: visit(slot, gm, ga, gb).
+template <class Visit>
+__device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState &r, int *overflow, Visit &&visit) {
+    if (s.num_nodes4 == 0) return;
+    int stk[kStackSize];
+    int sp = 0, node = 0;
+    while (node >= 0) {
+        const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
+        float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3), loz = __ldg(np + 4),
+               hiz = __ldg(np + 5);
+        int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+        float lx[4] = {lox.x, lox.y, lox.z, lox.w}, hx[4] = {hix.x, hix.y, hix.z, hix.w};
+        float ly[4] = {loy.x, loy.y, loy.z, loy.w}, hy[4] = {hiy.x, hiy.y, hiy.z, hiy.w};
+        float lz[4] = {loz.x, loz.y, loz.z, loz.w}, hz[4] = {hiz.x, hiz.y, hiz.z, hiz.w};
+        int kid[4] = {kids.x, kids.y, kids.z, kids.w};
+        node = -1;
+        for (int k = 0; k < 4; ++k) {
+            if (kid[k] == kLeafEmpty) continue;
+            float xa = fmaf(lx[k], r.idx, -r.oidx), xb = fmaf(hx[k], r.idx, -r.oidx);
+            float ya = fmaf(ly[k], r.idy, -r.oidy), yb = fmaf(hy[k], r.idy, -r.oidy);
+            float za = fmaf(lz[k], r.idz, -r.oidz), zb = fmaf(hz[k], r.idz, -r.oidz);
+            float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
+            float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), r.t_max0));
+            if (!(tn <= tf)) continue;
+            if (kid[k] >= 0) {
+                if (sp >= kStackSize) {
+                    atomicExch(overflow, 1);
+                    return;
+                }
+                stk[sp++] = kid[k];
+                continue;
+            }
+            const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~kid[k]);
+            visit(__ldg(g), __ldg(g + 1), __ldg(g + 2));
+        }
+        if (sp > 0) node = stk[--sp];
+    }
+}
 
 template <int MODE>
 __device__ void exact_ray(const SceneView &s, const RayState &r, float s2, const float *bg, double out[4],
@@ -22,51 +63,18 @@ __device__ void exact_ray(const SceneView &s, const RayState &r, float s2, const
     float ca[kExactCap];
     int cid[kExactCap];
     int m = 0;
-    if (s.num_nodes4 > 0) {
-        int stk[kStackSize];
-        int sp = 0, node = 0;
-        while (node >= 0) {
-            const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
-            float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3),
-                   loz = __ldg(np + 4), hiz = __ldg(np + 5);
-            int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
-            float lx[4] = {lox.x, lox.y, lox.z, lox.w}, hx[4] = {hix.x, hix.y, hix.z, hix.w};
-            float ly[4] = {loy.x, loy.y, loy.z, loy.w}, hy[4] = {hiy.x, hiy.y, hiy.z, hiy.w};
-            float lz[4] = {loz.x, loz.y, loz.z, loz.w}, hz[4] = {hiz.x, hiz.y, hiz.z, hiz.w};
-            int kid[4] = {kids.x, kids.y, kids.z, kids.w};
-            node = -1;
-            for (int k = 0; k < 4; ++k) {
-                if (kid[k] == kLeafEmpty) continue;
-                float xa = fmaf(lx[k], r.idx, -r.oidx), xb = fmaf(hx[k], r.idx, -r.oidx);
-                float ya = fmaf(ly[k], r.idy, -r.oidy), yb = fmaf(hy[k], r.idy, -r.oidy);
-                float za = fmaf(lz[k], r.idz, -r.oidz), zb = fmaf(hz[k], r.idz, -r.oidz);
-                float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
-                float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), r.t_max0));
-                if (!(tn <= tf)) continue;
-                if (kid[k] >= 0) {
-                    if (sp >= kStackSize) {
-                        atomicExch(overflow, 1);
-                        break;
-                    }
-                    stk[sp++] = kid[k];
-                    continue;
-                }
-                const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~kid[k]);
-                float4 gm = __ldg(g), ga = __ldg(g + 1), gb = __ldg(g + 2);
-                Cand c = candidate<MODE>(r, gm, ga, gb, s2);
-                if (!c.valid) continue;
-                if (m >= kExactCap) {
-                    atomicExch(overflow, 1);
-                    continue;
-                }
-                ct[m] = c.t;
-                ca[m] = c.alpha;
-                cid[m] = __float_as_int(gb.z);
-                ++m;
-            }
-            if (sp > 0) node = stk[--sp];
+    for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+        Cand c = candidate<MODE>(r, gm, ga, gb, s2);
+        if (!c.valid) return;
+        if (m >= kExactCap) {
+            atomicExch(overflow, 1);
+            return;
         }
-    }
+        ct[m] = c.t;
+        ca[m] = c.alpha;
+        cid[m] = __float_as_int(gb.z);
+        ++m;
+    });
     // insertion sort by (t, prim id)
     for (int i = 1; i < m; ++i) {
         float t = ct[i], a = ca[i];
@@ -138,6 +146,194 @@ __global__ void __launch_bounds__(128) k_exact_frame(SceneView s, CamD cam, Rend
     rgb[i * 3 + 1] = acc[1] * inv;
     rgb[i * 3 + 2] = acc[2] * inv;
     op[i] = acc[3] * inv;
+}
+
+// ---------------------------------------------------------------------------
+// Biased k-nearest composite (kernels.py:479-518, 561-580; tracer.py:305-343):
+// every valid candidate in (t_min, t_max) is accepted with ONE draw (slot 0 of
+// the ray's stream), and only the kk nearest accepted are composited with
+// their original alphas, background behind.  The kk nearest are kept as a
+// sorted list while walking, so memory is O(min(kk, cap)), not O(accepted).
+//   RNG counter: u = counter_u(walk_key(frame_key(seed), ray_id0+i, sample0), pid)
+//   RNG table:   u = table[pid * table_slots + 0]
+//   RNG trig64:  u = the reference's trig hash of the fp64 hit (kernels.py:55-60)
+// ---------------------------------------------------------------------------
+constexpr int kBiasedCap = 256;
+
+struct BiasedArgs {
+    double t_min, t_max, s2;
+    int mode, kk;
+    float3 bg;
+    uint32_t fkey, ray_id0, sample0;
+    const double *table;
+    int64_t tstride;
+};
+
+template <int MODE, int RNG>
+__device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, const BiasedArgs &a, double out[3],
+                           int *overflow) {
+    RayState r;
+    init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], a.t_min, a.t_max);
+    const t64::Ray64 r64{q[0], q[1], q[2], q[3], q[4], q[5], a.t_min, a.t_max};
+    const int keep = a.kk < 1 ? 1 : (a.kk < kBiasedCap ? a.kk : kBiasedCap);
+    double bt[kBiasedCap], ba[kBiasedCap];
+    int bid[kBiasedCap];
+    bt[0] = INFINITY;  // (keep >= 1; silences a maybe-uninitialised diagnostic)
+    ba[0] = 0.0;
+    bid[0] = 0;
+    int m = 0;            // kept (<= keep), sorted by (t, pid)
+    bool dropped = false; // an accepted candidate fell off the kept list
+    const float s2f = (float)a.s2;
+    for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+        const int pid = __float_as_int(gb.z);
+        double t, alpha;
+        bool acc;
+        if (RNG == SRT_RNG_TRIG64) {
+            double resid, hx, hy, hz;
+            if (!t64::candidate<MODE>(r64, s.means64 + (int64_t)pid * 3, s.cov64 + (int64_t)pid * 6, a.s2, t, resid,
+                                      hx, hy, hz))
+                return;
+            if (t <= a.t_min || t >= a.t_max) return;
+            alpha = t64::mul(s.opac64[pid], exp(t64::mul(-0.5, resid)));
+            acc = t64::hash_position(hx, hy, hz, 0) < alpha;
+        } else {
+            Cand c = candidate<MODE>(r, gm, ga, gb, s2f);
+            if (!c.valid) return;
+            t = c.t;
+            alpha = c.alpha;
+            if (RNG == SRT_RNG_TABLE)
+                acc = __ldg(a.table + (int64_t)pid * a.tstride) < alpha;
+            else
+                acc = counter_u(key, (uint32_t)pid) < c.alpha;
+        }
+        if (!acc) return;
+        // insert into the sorted kept list, dropping the farthest when full
+        int j = m;
+        if (m == keep) {
+            if (!(t < bt[m - 1] || (t == bt[m - 1] && pid < bid[m - 1]))) {
+                dropped = true;
+                return;
+            }
+            dropped = true;
+            --j;
+        } else {
+            ++m;
+        }
+        while (j > 0 && (bt[j - 1] > t || (bt[j - 1] == t && bid[j - 1] > pid))) {
+            bt[j] = bt[j - 1];
+            ba[j] = ba[j - 1];
+            bid[j] = bid[j - 1];
+            --j;
+        }
+        bt[j] = t;
+        ba[j] = alpha;
+        bid[j] = pid;
+    });
+    if (dropped && keep < a.kk) atomicExch(overflow, 1);  // kk > cap and more accepted than the cap
+    double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
+    for (int k = 0; k < m; ++k) {
+        float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, bid[k], r.fdx, r.fdy, r.fdz);
+        double w = trans * ba[k];
+        rr += w * col.x;
+        gg += w * col.y;
+        bb += w * col.z;
+        trans *= 1.0 - ba[k];
+    }
+    out[0] = rr + trans * a.bg.x;
+    out[1] = gg + trans * a.bg.y;
+    out[2] = bb + trans * a.bg.z;
+}
+
+template <int MODE, int RNG>
+__global__ void __launch_bounds__(128) k_biased_rays(SceneView s, const double *__restrict__ rays, int64_t R,
+                                                     BiasedArgs a, double *rgb, int *overflow) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R) return;
+    biased_ray<MODE, RNG>(s, rays + i * 6, walk_key(a.fkey, a.ray_id0 + (uint32_t)i, a.sample0), a, rgb + i * 3,
+                          overflow);
+}
+
+// The cli's --compare-biased frame (cli.py:164-203): per pixel, the mean
+// over passes of the biased composite of the jittered camera ray of that
+// pass; the counter draw of pixel (px,py), pass f is (seed, py*W+px, f).
+template <int MODE, int RNG>
+__global__ void __launch_bounds__(128) k_biased_frame(SceneView s, CamD cam, BiasedArgs a, int width, int height,
+                                                      int passes, int pass0, uint32_t seed, double *rgb,
+                                                      int *overflow) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)width * height) return;
+    int px = (int)(i % width), py = (int)(i / width);
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int f = 0; f < passes; ++f) {
+        double q[6] = {cam.e[0], cam.e[1], cam.e[2], 0.0, 0.0, 0.0};
+        camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)(pass0 + f), seed, width, height, q[3], q[4], q[5]);
+        double o[3];
+        biased_ray<MODE, RNG>(s, q, walk_key(a.fkey, (uint32_t)i, (uint32_t)(pass0 + f)), a, o, overflow);
+        for (int c = 0; c < 3; ++c) acc[c] += o[c];
+    }
+    double inv = 1.0 / (double)passes;
+    for (int c = 0; c < 3; ++c) rgb[i * 3 + c] = acc[c] * inv;
+}
+
+static BiasedArgs biased_args(double t_min, double t_max, double s2, int mode, int kk, const double *bg,
+                              uint32_t seed, uint32_t ray_id0, uint32_t sample0, const double *table,
+                              int64_t tstride) {
+    BiasedArgs a;
+    a.t_min = t_min;
+    a.t_max = t_max;
+    a.s2 = s2;
+    a.mode = mode;
+    a.kk = kk;
+    a.bg = make_float3((float)bg[0], (float)bg[1], (float)bg[2]);
+    uint32_t x = seed ^ 0x9E3779B9u;  // frame_key on the host
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    a.fkey = x;
+    a.ray_id0 = ray_id0;
+    a.sample0 = sample0;
+    a.table = table;
+    a.tstride = tstride;
+    return a;
+}
+
+#define SRT_BIASED_DISPATCH(RNGV, MODEV, LAUNCH)                         \
+    if ((RNGV) == SRT_RNG_TRIG64) {                                      \
+        if ((MODEV) == 0) LAUNCH(0, SRT_RNG_TRIG64); else LAUNCH(1, SRT_RNG_TRIG64); \
+    } else if ((RNGV) == SRT_RNG_TABLE) {                                \
+        if ((MODEV) == 0) LAUNCH(0, SRT_RNG_TABLE); else LAUNCH(1, SRT_RNG_TABLE);   \
+    } else {                                                             \
+        if ((MODEV) == 0) LAUNCH(0, SRT_RNG_COUNTER); else LAUNCH(1, SRT_RNG_COUNTER); \
+    }
+
+srt_status launch_biased_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int kk,
+                              const double *bg, const double *d_table, double *d_rgb, cudaStream_t st) {
+    unsigned blocks = (unsigned)((R + 127) / 128);
+    if (blocks == 0) return SRT_OK;
+    BiasedArgs a = biased_args(p->t_min, p->t_max, p->s2, p->mode, kk, bg, p->seed, p->ray_id0, p->sample0, d_table,
+                               p->table_slots);
+    SceneView v = s->view();
+#define SRT_B(M, G) k_biased_rays<M, G><<<blocks, 128, 0, st>>>(v, d_rays, R, a, d_rgb, s->d_flag)
+    SRT_BIASED_DISPATCH(p->rng, p->mode, SRT_B)
+#undef SRT_B
+    return cuda_status(cudaGetLastError(), "k_biased_rays launch");
+}
+
+srt_status launch_biased_frame(const SrtScene *s, const CamD &cam, const SrtRenderParams *p, int kk,
+                               double *d_rgb, cudaStream_t st) {
+    int64_t n = (int64_t)p->width * p->height;
+    unsigned blocks = (unsigned)((n + 127) / 128);
+    if (blocks == 0) return SRT_OK;
+    BiasedArgs a = biased_args(0.0, DBL_MAX, p->s2, p->mode, kk, p->background, p->seed, 0, 0, nullptr, 0);
+    SceneView v = s->view();
+#define SRT_B(M, G)                                                                                          \
+    k_biased_frame<M, G><<<blocks, 128, 0, st>>>(v, cam, a, p->width, p->height, p->passes, p->pass0, p->seed, \
+                                                 d_rgb, s->d_flag)
+    SRT_BIASED_DISPATCH(p->rng, p->mode, SRT_B)
+#undef SRT_B
+    return cuda_status(cudaGetLastError(), "k_biased_frame launch");
 }
 
 srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max, int mode,

@@ -112,6 +112,10 @@ srt_status launch_trace_rays_trig64(const SrtScene *s, const SrtTraceParams *p, 
                                     int nslots, double *d_t, int32_t *d_id, cudaStream_t st);
 srt_status launch_trace_pass_trig64(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, double s2,
                                     int32_t *d_hits, cudaStream_t st);
+srt_status launch_biased_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int kk,
+                              const double *bg, const double *d_table, double *d_rgb, cudaStream_t st);
+srt_status launch_biased_frame(const SrtScene *s, const CamD &cam, const SrtRenderParams *p, int kk,
+                               double *d_rgb, cudaStream_t st);
 srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max, int mode,
                              double s2, const double *bg, double *d_rgb, double *d_op, cudaStream_t st);
 srt_status launch_exact_frame(const SrtScene *s, const CamD &cam, const RenderArgs &a, double *d_rgb, double *d_op,

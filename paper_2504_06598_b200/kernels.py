@@ -101,6 +101,22 @@ def exact_batch(means, cov6, opac, sh, deg, origins, directions, t_min, t_max, m
     out_op[...] = op
 
 
+def biased_batch(means, cov6, opac, sh, deg, origins, directions, t_min, t_max, mode, s2, kk, bgr, bgg, bgb,
+                 out_rgb, *, seed=0, ray_id0=0, sample0=0, rng="counter", table=None, device=0):
+    """kernels.py:561-580 (the `--compare-biased` baseline, cli.py:164-203):
+    per ray, one acceptance draw per valid candidate, then the kk nearest
+    accepted composited front to back with their original alphas."""
+    if int(kk) < 1:
+        raise ValueError(f"k must be >= 1, got {kk}")  # tracer.py:325-326
+    sc = _lbvh_scene(means, cov6, opac, sh, int(deg), s2, device)
+    try:
+        rgb = sc.biased_rays(origins, directions, int(kk), t_min, t_max, int(mode), float(s2), (bgr, bgg, bgb), rng,
+                             seed, ray_id0, sample0, table)
+    finally:
+        sc.close()
+    out_rgb[...] = rgb
+
+
 def render_exact(means, cov6, opac, sh, deg, ex, ey, ez, rx, ry, rz, ux, uy, uz, fx, fy, fz, half_w, half_h,
                  width, height, frames, mode, s2, seed, bgr, bgg, bgb, out_rgb, out_op, *, device=0):
     """kernels.py:677-723: per-pixel exact composite averaged over `frames` jittered rays."""
@@ -114,4 +130,4 @@ def render_exact(means, cov6, opac, sh, deg, ex, ey, ez, rx, ry, rz, ux, uy, uz,
     out_op[...] = op
 
 
-__all__ = ["exact_batch", "render_exact", "render_stochastic", "trace_batch", "transmittance_batch", "np"]
+__all__ = ["biased_batch", "exact_batch", "render_exact", "render_stochastic", "trace_batch", "transmittance_batch", "np"]

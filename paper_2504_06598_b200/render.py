@@ -171,6 +171,20 @@ def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, thre
     return AccumBuffer(rgb, op, settings.samples_per_pixel)
 
 
+def render_biased(asset, camera: CameraConfig, settings: RenderSettings, k: int, bvh=None, device: int = 0,
+                  rng: str = "counter") -> np.ndarray:
+    """The bench's ``--compare-biased K`` frame (cli.py:164-203) on the GPU:
+    per pixel, the mean over ``settings.passes`` jittered rays of the biased
+    k-nearest composite (kernels.py:479-518).  Returns (H, W, 3) f64."""
+    if int(k) < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    sc = prepare(asset, settings, bvh, device)
+    cam = camera_tuple(camera, settings.width, settings.height)
+    mode = 0 if settings.depth_mode == "mean" else 1
+    return sc.render_biased(cam, settings.width, settings.height, int(k), settings.passes, mode,
+                            settings.cutoff_s * settings.cutoff_s, settings.seed, settings.background, rng=rng)
+
+
 def image_metrics(image: AccumBuffer, reference: AccumBuffer) -> dict:
     """MSE / PSNR (peak = max(1, reference max)) and mean |opacity error| (render.py:177-195)."""
     if image.rgb.shape != reference.rgb.shape:

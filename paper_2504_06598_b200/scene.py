@@ -220,6 +220,45 @@ class DeviceScene:
                                          int(mode), float(s2), _ptr(bg), _ptr(rgb), _ptr(op)))
         return rgb, op
 
+    def biased_rays(self, origins, dirs, kk, t_min=0.0, t_max=TMAX, mode=0, s2=8.0, background=(0.0, 0.0, 0.0),
+                    rng="counter", seed=0, ray_id0=0, sample0=0, table=None):
+        """kernels.biased_batch semantics (kernels.py:479-518, 561-580): one
+        acceptance draw per candidate (slot 0 of the ray's stream), the kk
+        nearest accepted composited with their own alphas.  Returns rgb (R,3)."""
+        if int(kk) < 1:
+            raise ValueError(f"k must be >= 1, got {kk}")
+        o = _c64(origins).reshape(-1, 3)
+        d = _c64(dirs).reshape(-1, 3)
+        bg = _c64(background).reshape(3)
+        p = SrtTraceParams()
+        p.t_min, p.t_max, p.mode, p.clip, p.s2 = float(t_min), float(t_max), int(mode), 0, float(s2)
+        p.rng = RNG[rng]
+        p.seed, p.ray_id0, p.sample0 = seed & 0xFFFFFFFF, ray_id0 & 0xFFFFFFFF, sample0 & 0xFFFFFFFF
+        tab = None
+        if rng == "table":
+            tab = _c64(table)
+            if tab.ndim == 1:
+                tab = tab.reshape(-1, 1)
+            if tab.ndim != 2 or tab.shape[0] != self.n:
+                raise ValueError("table must be (n,) or (n, slots)")
+            p.table, p.table_slots = tab.ctypes.data, tab.shape[1]
+        rgb = np.empty((o.shape[0], 3))
+        check(_lib.load().srt_biased_rays(self.handle, ctypes.byref(p), _ptr(o), _ptr(d), o.shape[0], int(kk),
+                                          _ptr(bg), _ptr(rgb)))
+        return rgb
+
+    def render_biased(self, cam, width, height, kk, passes=1, mode=0, s2=8.0, seed=0, background=(0.0, 0.0, 0.0),
+                      pass0=0, rng="counter", out_rgb=None):
+        """cli._biased_frame semantics (cli.py:164-203): per-pixel mean over
+        `passes` jittered rays of the biased k-nearest composite."""
+        if int(kk) < 1:
+            raise ValueError(f"k must be >= 1, got {kk}")
+        camera = make_camera(cam)
+        prm = make_render_params(width, height, passes, 1, mode, s2, False, seed, background, pass0, rng=rng)
+        rgb = np.empty((height, width, 3)) if out_rgb is None else out_rgb
+        check(_lib.load().srt_render_biased(self.handle, ctypes.byref(camera), ctypes.byref(prm), int(kk), _ptr(rgb)))
+        return rgb
+
     def render_exact(self, cam, width, height, frames=1, mode=0, s2=8.0, seed=0, background=(0.0, 0.0, 0.0),
                      out_rgb=None, out_op=None):
         """kernels.render_exact semantics (kernels.py:677-723)."""

@@ -74,3 +74,38 @@ def test_small_frames_match_reference(golden):
     assert _pixel_agreement(got, g["rgb"], g["opacity"]) >= 0.99
     got2 = _render(anisotropic_sheets(60, seed=3), 16, 12, 3, seed=11, mode="center")
     assert _pixel_agreement(got2, g["rgb_center"], g["opacity_center"]) >= 0.99
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("kk", [1, 2, 5])
+def test_biased_batch_matches_reference(golden, mode, kk):
+    """kernels.biased_batch of the reference (the cli's --compare-biased
+    baseline, kernels.py:479-518) through the trig64 draw: fp64 alphas and
+    fp32 SH colours, so per-ray rgb to 1e-5 except at draw ties."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    g = golden("biased_500")
+    t = golden("trace_400")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    sc = DeviceScene.from_packed(a.packed)
+    sc.build_bvh(CUTOFF)
+    rgb = sc.biased_rays(t["origins"], t["dirs"], kk, 0.0, TMAX, mode, S2, (0.15, 0.25, 0.35), rng="trig64")
+    sc.close()
+    ok = np.all(np.abs(rgb - g[f"rgb_m{mode}_k{kk}"]) <= 1e-5, axis=1)
+    assert ok.mean() >= 0.995
+
+
+@pytest.mark.parametrize("kk", [1, 3])
+def test_biased_frame_matches_reference_cli(golden, kk):
+    """The reference bench's --compare-biased frame (cli.py:164-203; 20x16,
+    2 passes) against render_biased with the trig64 draw."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render_biased
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    g = golden("biased_500")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    st = RenderSettings(width=20, height=16, spp=2, seed=5, background=[0.15, 0.25, 0.35])
+    rgb = render_biased(a, front_camera(), st, kk, rng="trig64")
+    ok = np.all(np.abs(rgb - g[f"frame_k{kk}"]) <= 1e-5, axis=2)
+    assert ok.mean() >= 0.99

@@ -172,3 +172,13 @@ def test_two_layer_closed_form():
     assert len(a) == 2 and a.sh_degree == 0
     cam = front_camera()
     assert cam.fov_deg == 45.0
+
+
+def test_biased_k_must_be_positive():
+    """tracer.py:325-326: k < 1 is a ValueError, raised before any device work."""
+    from paper_2504_06598_b200 import kernels
+
+    z = np.zeros((1, 3))
+    with pytest.raises(ValueError, match="k"):
+        kernels.biased_batch(z, np.zeros((1, 6)), np.zeros(1), np.zeros((1, 3, 1)), 0, z, z + [0, 0, 1], 0.0, 1.0,
+                             0, 8.0, 0, 0.0, 0.0, 0.0, np.zeros((1, 3)))

@@ -186,3 +186,19 @@ def test_exact_compositing_matches_reference(oracle, golden):
     np.testing.assert_array_equal(frgb, g["frame_rgb"])
     np.testing.assert_array_equal(fop, g["frame_opacity"])
     assert int(g["frame_spp"]) == 3
+
+
+def test_biased_batch_bitwise(oracle, golden):
+    """kernels.biased_batch (kernels.py:479-518, 561-580) with the reference's
+    trig draw: bit-identical for k in {1, 2, 5}, both depth modes."""
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    g = golden("biased_500")
+    t = golden("trace_400")
+    a = random_cloud(500, seed=41, sh_degree=2)
+    pk = a.packed
+    for mode in (0, 1):
+        for kk in (1, 2, 5):
+            rgb = oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 2, t["origins"], t["dirs"], kk,
+                                      mode=mode, s2=S2, background=[0.15, 0.25, 0.35], rng="trig")
+            np.testing.assert_array_equal(rgb, g[f"rgb_m{mode}_k{kk}"])

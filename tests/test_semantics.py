@@ -34,6 +34,16 @@ class OracleBackend:
         b = self.O.sah_build(lo, hi)
         return self.O.transmittance(b, pk.means, pk.cov_inv6, pk.opacities, origins, dirs, 0.0, TMAX, 0, S2)
 
+    def biased(self, asset, origins, dirs, kk, rng="counter", table=None, seed=0, mode=0, background=(0, 0, 0)):
+        pk = asset.packed
+        return self.O.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, origins, dirs, kk,
+                                   mode=mode, s2=S2, background=background, rng=rng, seed=seed, table=table)
+
+    def exact(self, asset, origins, dirs, background=(0, 0, 0)):
+        pk = asset.packed
+        return self.O.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, origins, dirs, s2=S2,
+                                  background=background)[0]
+
 
 class GpuBackend:
     name = "gpu"
@@ -62,6 +72,20 @@ class GpuBackend:
         sc = self.scene(asset)
         try:
             return sc.transmittance(origins, dirs, 0.0, TMAX, 0, S2)
+        finally:
+            sc.close()
+
+    def biased(self, asset, origins, dirs, kk, rng="counter", table=None, seed=0, mode=0, background=(0, 0, 0)):
+        sc = self.scene(asset)
+        try:
+            return sc.biased_rays(origins, dirs, kk, 0.0, TMAX, mode, S2, background, rng, seed, 0, 0, table)
+        finally:
+            sc.close()
+
+    def exact(self, asset, origins, dirs, background=(0, 0, 0)):
+        sc = self.scene(asset)
+        try:
+            return sc.exact_rays(origins, dirs, 0.0, TMAX, 0, S2, background)[0]
         finally:
             sc.close()
 
@@ -212,3 +236,50 @@ def test_trace_batch_empty_and_miss(backend):
     assert t.shape == (0, 1)
     t, ids = backend.trace(a, [[0, 0, -10]], [[0, 0, -1]], 3)  # facing away
     assert np.all(ids == -1) and np.all(np.isinf(t))
+
+
+# ---- biased k-nearest composite (reference tests/test_tracer.py:270-299) -----
+
+def test_biased_truncation_composites_only_k_nearest(backend):
+    """Both layers accepted by script: k=1 shades only the red front layer,
+    k=2 adds blue with the compositing weight (test_tracer.py:271-283)."""
+    a = two_layer_scene()
+    table = np.array([[0.1], [0.1]])
+    k1 = backend.biased(a, [[0, 0, 0]], [[0, 0, 1]], 1, rng="table", table=table)
+    k2 = backend.biased(a, [[0, 0, 0]], [[0, 0, 1]], 2, rng="table", table=table)
+    np.testing.assert_allclose(k1[0], [0.5, 0.0, 0.0], atol=1e-6)
+    np.testing.assert_allclose(k2[0], [0.5, 0.0, 0.25], atol=1e-6)
+
+
+def test_biased_background_fills_the_rest(backend):
+    """Front accepted, back rejected, k=4: half red, half background (:285-291)."""
+    a = two_layer_scene()
+    out = backend.biased(a, [[0, 0, 0]], [[0, 0, 1]], 4, rng="table", table=np.array([[0.1], [0.9]]),
+                         background=(0.0, 1.0, 0.0))
+    np.testing.assert_allclose(out[0], [0.5, 0.5, 0.0], atol=1e-6)
+
+
+def test_biased_all_accepted_is_exact_composite(backend):
+    """Every candidate accepted (u = 0) and k above the candidate count: the
+    biased composite IS the exact sorted composite (kernels.py:441-518)."""
+    a = random_cloud(500, seed=41, sh_degree=2)
+    o, d = random_rays(np.random.default_rng(9), 300)
+    bg = (0.15, 0.25, 0.35)
+    got = backend.biased(a, o, d, 200, rng="table", table=np.zeros((500, 1)), background=bg)
+    want = backend.exact(a, o, d, background=bg)
+    np.testing.assert_allclose(got, want, atol=2e-5)
+
+
+def test_biased_counter_k_nesting(backend):
+    """One draw per candidate, independent of k: k composites a prefix of the
+    same accepted list, so a ray whose k=1 and k=8 results agree accepted at
+    most one candidate and every larger k gives the same colour."""
+    a = random_cloud(500, seed=41, sh_degree=0)
+    o, d = random_rays(np.random.default_rng(4), 300)
+    k1 = backend.biased(a, o, d, 1, seed=7)
+    k8 = backend.biased(a, o, d, 8, seed=7)
+    k99 = backend.biased(a, o, d, 99, seed=7)
+    same = np.all(np.isclose(k1, k8), axis=1)
+    assert np.isfinite(k99).all()
+    assert same.mean() < 1.0  # some rays accept more than one candidate
+    np.testing.assert_allclose(k8[same], k99[same], atol=1e-12)  # k1 == k8 -> at most one accepted
