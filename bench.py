@@ -278,9 +278,10 @@ def run_ours(args) -> None:
         e2e = {"value": rays_per_frame / statistics.median(e2e_t) / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": 192, "d2h_bytes_per_step": int(buf.rgb.nbytes + buf.opacity.nbytes),
                "ms_per_frame": statistics.median(e2e_t) * 1e3,
-               "path": "paper_2504_06598_b200.render() -> srt_render (C ABI): trace+shade+fp64 resolve on the GPU, "
-                       "AccumBuffer (H,W,3)+(H,W) float64 copied into pooled page-locked host memory; h2d = camera + settings "
-                       "kernel parameters (SrtCamera 112 B + SrtRenderParams 80 B), scene resident"}
+               "path": "paper_2504_06598_b200.render() -> srt_render (C ABI): fused trace+shade on the GPU; the last "
+                       "pass stores the AccumBuffer (H,W,3)+(H,W) float64 straight into pooled mapped page-locked host "
+                       "memory (device->host over PCIe during the walk), stream synchronised before render() returns; "
+                       "h2d = camera + settings kernel parameters (SrtCamera 112 B + SrtRenderParams 80 B), scene resident"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -140,13 +140,26 @@ int32_t srt_device_count(void) {
     return n;
 }
 
+// Device address of a mapped page-locked host buffer, or nullptr for
+// pageable / device memory.
+static double *mapped_host(double *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+    return (double *)at.devicePointer;
+}
+
 srt_status srt_host_alloc(int64_t bytes, void **out) {
     if (!out || bytes < 0) {
         set_error("invalid host allocation");
         return SRT_ERR_INVALID_ARG;
     }
     *out = nullptr;
-    return cuda_status(cudaHostAlloc(out, (size_t)(bytes ? bytes : 1), cudaHostAllocPortable), "cudaHostAlloc");
+    return cuda_status(cudaHostAlloc(out, (size_t)(bytes ? bytes : 1), cudaHostAllocPortable | cudaHostAllocMapped),
+                       "cudaHostAlloc");
 }
 
 srt_status srt_host_free(void *ptr) {
@@ -877,10 +890,17 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     float4 *d_out = (float4 *)(base + al(hits_bytes) + al(acc_bytes));
     double *d_rgb = (double *)(base + al(hits_bytes) + al(acc_bytes) + al(out_bytes));
     double *d_op = d_rgb + npix * 3;
+    // Outputs in mapped page-locked memory (srt_host_alloc): the last fused
+    // pass stores the f64 frame straight into them, so the device->host
+    // transfer overlaps the walk and no resolve kernel or copy follows.
+    double *m_rgb = mapped_host(out_rgb), *m_op = mapped_host(out_op);
+    const bool direct = m_rgb && m_op && a.rng != SRT_RNG_TRIG64 && !(out_ids && p->passes == 1);
     for (int f = 0; f < p->passes && !rc; ++f) {
         int pass = p->pass0 + f;
         if (a.rng != SRT_RNG_TRIG64 && !(out_ids && f == 0)) {
-            rc = launch_render_pass_fused(s, cam, a, pass, d_acc, f == 0, f == p->passes - 1, d_out, st);
+            const bool last = f == p->passes - 1;
+            rc = launch_render_pass_fused(s, cam, a, pass, d_acc, f == 0, last, d_out, st, nullptr,
+                                          last && direct ? m_rgb : nullptr, last && direct ? m_op : nullptr);
             continue;
         }
         rc = launch_trace_pass(s, cam, a, pass, d_hits, st);
@@ -904,6 +924,10 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
             }
         }
         if (!rc) rc = launch_shade_pass(s, cam, a, pass, d_hits, d_acc, f == 0, f == p->passes - 1, d_out, st);
+    }
+    if (direct) {
+        if (!rc) rc = check_flag(s, st);
+        return rc;
     }
     if (!rc) rc = launch_resolve_f64(a, d_out, d_rgb, d_op, st);
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb download");

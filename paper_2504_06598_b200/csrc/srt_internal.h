@@ -102,7 +102,7 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
                              cudaStream_t st);
 srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                                    float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
-                                   int32_t *d_hits = nullptr);
+                                   int32_t *d_hits = nullptr, double *d_rgb64 = nullptr, double *d_op64 = nullptr);
 srt_status launch_shade_pass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                              const int32_t *d_hits, float4 *d_accum, bool first, bool last, float4 *d_out,
                              cudaStream_t st);

@@ -288,6 +288,7 @@ struct CameraSource {
     // fused shading (hits == nullptr): accumulate straight from the walk
     float4 *accum;
     float4 *out;
+    double *rgb64, *op64;  // optional final f64 frame (e.g. mapped page-locked host memory)
     int first, last;
     template <int NS>
     __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
@@ -330,6 +331,17 @@ struct CameraSource {
             float inv = 1.0f / ((float)a.passes * (float)a.nslots);
             int px, py;
             tile_pixel(a, idx >> 8, idx & 255, px, py);
+            if (rgb64) {
+                // the resolved frame straight into its final (H,W,3)+(H,W) f64
+                // layout -- over PCIe when it is mapped host memory, so the
+                // device->host transfer overlaps the rest of the walk
+                int64_t pix = (int64_t)py * a.width + px;
+                rgb64[pix * 3 + 0] = (double)(acc.x * inv);
+                rgb64[pix * 3 + 1] = (double)(acc.y * inv);
+                rgb64[pix * 3 + 2] = (double)(acc.z * inv);
+                op64[pix] = (double)(acc.w * inv);
+                return;
+            }
             int64_t oidx = a.shard_count > 1 ? (int64_t)idx : (int64_t)py * a.width + px;
             out[oidx] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
         } else {
@@ -1059,10 +1071,12 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
 // traced into d_hits for a separate k_shade_pass.
 srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                                    float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
-                                   int32_t *d_hits) {
+                                   int32_t *d_hits, double *d_rgb64, double *d_op64) {
     CameraSource src;
     src.accum = d_accum;
     src.out = d_out;
+    src.rgb64 = d_rgb64;
+    src.op64 = d_op64;
     src.first = first ? 1 : 0;
     src.last = last ? 1 : 0;
     src.cam = cam;

@@ -337,3 +337,28 @@ def test_c5_scale_6m_vs_oracle(oracle):
     agree = ids[sub] == ref["ids"][sub]
     assert agree.mean() >= ID_AGREE, agree.mean()
     _check_colours(rgb[sub], ref["rgb"][sub], np.all(agree, axis=2))
+
+
+@pytest.mark.parametrize("passes,nslots", [(1, 1), (3, 2)])
+def test_mapped_host_output_equals_copy_path(passes, nslots):
+    """srt_render into mapped page-locked outputs (the last fused pass stores
+    the f64 frame over PCIe) equals the resolve-and-copy path into pageable
+    memory, bit for bit."""
+    from paper_2504_06598_b200 import front_camera
+    from paper_2504_06598_b200.render import PinnedPool
+    from paper_2504_06598_b200.scene import DeviceScene, camera_tuple
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(5_000, seed=12, sh_degree=2)
+    sc = DeviceScene.from_packed(a.packed)
+    sc.build_bvh(np.sqrt(S2))
+    W, H = 72, 40
+    cam = camera_tuple(front_camera(), W, H)
+    pool = PinnedPool()
+    prgb, pop = pool.array((H, W, 3)), pool.array((H, W))
+    rgb_m, op_m, _ = sc.render(cam, W, H, passes, nslots, 0, S2, True, 3, (0.1, 0.2, 0.3), out_rgb=prgb, out_op=pop)
+    rgb_c, op_c, _ = sc.render(cam, W, H, passes, nslots, 0, S2, True, 3, (0.1, 0.2, 0.3))
+    sc.close()
+    np.testing.assert_array_equal(rgb_m, rgb_c)
+    np.testing.assert_array_equal(op_m, op_c)
+    assert op_c.max() > 0
