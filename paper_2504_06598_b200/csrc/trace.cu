@@ -1017,6 +1017,8 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
         if (cfg == 4) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 1>(s, src, w, st);
+        if (cfg == 5) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8, 0>(s, src, w, st);
+        if (cfg == 6) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 16, 7, 0>(s, src, w, st);
     }
     // 7 resident blocks/SM (72 registers, no spills) measured 4% faster than
     // the unconstrained 80-register build at N=1; larger N keep their registers
