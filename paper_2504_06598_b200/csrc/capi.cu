@@ -126,6 +126,11 @@ static srt_status validate_render(const SrtScene *s, const SrtRenderParams *p) {
 
 using namespace srt;
 
+// serialise host entry points on one scene handle (null-safe)
+#define SRT_LOCK(sc)                              \
+    std::unique_lock<std::mutex> srt_lock_;       \
+    if (sc) srt_lock_ = std::unique_lock<std::mutex>((sc)->mu)
+
 extern "C" {
 
 const char *srt_last_error(void) { return g_last_error.c_str(); }
@@ -191,7 +196,7 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
-    if (!rc) rc = cuda_status(cudaMalloc(&s->d_work, sizeof(uint32_t) * 4), "work counter alloc");
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_work, sizeof(uint32_t) * 32 * SrtScene::kWorkRing), "work counter alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 8), "stats alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 8), "stats init");
     if (!rc && n > 0) {
@@ -272,6 +277,7 @@ srt_status srt_scene_destroy(SrtScene *s) {
 }
 
 srt_status srt_bvh_build_ex(SrtScene *s, double cutoff_s, int32_t method) {
+    SRT_LOCK(s);
     if (!s || !(cutoff_s > 0.0) || !std::isfinite(cutoff_s) || (method != SRT_BVH_LBVH && method != SRT_BVH_PLOC)) {
         set_error("invalid scene, cutoff or build method");
         return SRT_ERR_INVALID_ARG;
@@ -289,6 +295,7 @@ srt_status srt_bvh_build(SrtScene *s, double cutoff_s) { return srt_bvh_build_ex
 srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const double *node_hi, const int64_t *node_left,
                           const int64_t *node_right, const int64_t *node_count, const int64_t *prim_order,
                           const double *prim_lo, const double *prim_hi) {
+    SRT_LOCK(s);
     if (!s || M < 0 || (M > 0 && (!node_lo || !node_hi || !node_left || !node_right || !node_count || !prim_order ||
                                   !prim_lo || !prim_hi))) {
         set_error("invalid BVH arrays");
@@ -469,6 +476,7 @@ srt_status srt_bvh_info(const SrtScene *s, int64_t *num_nodes, int32_t *depth, i
 srt_status srt_bvh_download(const SrtScene *s, float *node_lo, float *node_hi, int64_t *node_left,
                             int64_t *node_right, int64_t *node_count, int64_t *prim_order, float *prim_lo,
                             float *prim_hi) {
+    SRT_LOCK(s);
     if (!s || !s->has_bvh) {
         set_error("scene has no BVH");
         return SRT_ERR_NO_BVH;
@@ -580,6 +588,7 @@ srt_status srt_trace_rays_device(const SrtScene *s, const SrtTraceParams *p, con
 
 srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const double *origins, const double *dirs,
                           int64_t R, int32_t nslots, double *out_t, int64_t *out_id) {
+    SRT_LOCK(sc);
     srt_status rc = validate_trace(sc, p, R, nslots);
     if (rc) return rc;
     if (R == 0) return SRT_OK;
@@ -638,6 +647,7 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
 
 srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, const double *dirs, int64_t R,
                                   double t_min, double t_max, int32_t mode, double s2, double *out) {
+    SRT_LOCK(sc);
     if (!sc || R < 0 || (mode != 0 && mode != 1) || !(s2 > 0.0)) {
         set_error("invalid transmittance parameters");
         return SRT_ERR_INVALID_ARG;
@@ -671,6 +681,7 @@ srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, con
 srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const double *dirs, int64_t R, double t_min,
                           double t_max, int32_t mode, double s2, const double *background, double *out_rgb,
                           double *out_op) {
+    SRT_LOCK(sc);
     if (!sc || R < 0 || (mode != 0 && mode != 1) || !(s2 > 0.0) || !background || (R > 0 && (!out_rgb || !out_op))) {
         set_error("invalid exact-compositing parameters");
         return SRT_ERR_INVALID_ARG;
@@ -705,6 +716,7 @@ srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const doubl
 
 srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const double *origins, const double *dirs,
                            int64_t R, int32_t kk, const double *background, double *out_rgb) {
+    SRT_LOCK(sc);
     srt_status rc = validate_trace(sc, p, R, 1);
     if (rc) return rc;
     if (kk < 1 || !background || (R > 0 && (!origins || !dirs || !out_rgb))) {
@@ -740,6 +752,7 @@ srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const do
 
 srt_status srt_render_biased(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, int32_t kk,
                              double *out_rgb) {
+    SRT_LOCK(sc);
     srt_status rc = validate_render(sc, p);
     if (rc) return rc;
     if (!camera || !out_rgb || kk < 1 || p->rng == SRT_RNG_TABLE) {
@@ -761,6 +774,7 @@ srt_status srt_render_biased(const SrtScene *sc, const SrtCamera *camera, const 
 
 srt_status srt_render_exact(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
                             double *out_op) {
+    SRT_LOCK(sc);
     srt_status rc = validate_render(sc, p);
     if (rc) return rc;
     if (!camera || !out_rgb || !out_op) {
@@ -860,6 +874,7 @@ srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const S
 
 srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
                       double *out_op, int64_t *out_ids) {
+    SRT_LOCK(sc);
     srt_status rc = validate_render(sc, p);
     if (rc) return rc;
     if (!camera || !out_rgb || !out_op) {

@@ -24,6 +24,7 @@ __device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState
     int stk[kStackSize];
     int sp = 0, node = 0;
     while (node >= 0) {
+        SRT_DCHECK(node >= 0 && node < s.num_nodes4);
         const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
         float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3), loz = __ldg(np + 4),
                hiz = __ldg(np + 5);
@@ -49,6 +50,7 @@ __device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState
                 stk[sp++] = kid[k];
                 continue;
             }
+            SRT_DCHECK(~kid[k] < s.n);
             const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~kid[k]);
             visit(__ldg(g), __ldg(g + 1), __ldg(g + 2));
         }
@@ -232,6 +234,7 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
     if (dropped && keep < a.kk) atomicExch(overflow, 1);  // kk > cap and more accepted than the cap
     double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
     for (int k = 0; k < m; ++k) {
+        SRT_DCHECK(bid[k] >= 0 && bid[k] < s.n);
         float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, bid[k], r.fdx, r.fdy, r.fdz);
         double w = trans * ba[k];
         rr += w * col.x;

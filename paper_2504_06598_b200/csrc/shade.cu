@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(256) k_shade_pass(SceneView s, CamD cam, Rende
     for (int k = 0; k < a.nslots; ++k) {
         int pid = __ldg(h + k);
         if (pid >= 0) {
+            SRT_DCHECK(pid < s.n);
             float3 c = sh_color(s.sh, s.sh_k, s.sh_deg, pid, fx, fy, fz);
             r += c.x;
             g += c.y;

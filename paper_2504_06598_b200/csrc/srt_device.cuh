@@ -11,6 +11,7 @@
 //   SH     K*12 B per primitive in ORIGINAL id order, channel major, fp32.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace srt {
@@ -39,6 +40,22 @@ struct __align__(16) Geom {
     float4 a;  // a00 a01 a02 a11
     float4 b;  // a12 a22, prim id (int bits), sqrt(sum |a_ij|) (screen error bound)
 };
+
+// Device-side invariant checks, compiled in only for the bounds-checked
+// debug library (make debug): a failed check prints and traps the context.
+#ifdef SRT_DEBUG
+#define SRT_DCHECK(c)                                                              \
+    do {                                                                           \
+        if (!(c)) {                                                                \
+            printf("SRT_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);       \
+            __trap();                                                              \
+        }                                                                          \
+    } while (0)
+#else
+#define SRT_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
 
 struct SceneView {
     const double *means64;  // fp64 records in original id order (trig64 bridge mode)

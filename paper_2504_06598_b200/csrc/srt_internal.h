@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -24,7 +26,7 @@ struct SrtScene {
     int32_t num_nodes = 0;
     srt::Node4 *d_nodes4 = nullptr; // (num_nodes4,) 4-wide tree traced by the kernels
     int32_t num_nodes4 = 0;
-    uint32_t *d_work = nullptr;     // persistent-kernel work counters
+    uint32_t *d_work = nullptr;     // ring of kWorkRing persistent-kernel work counters (128 B apart)
     unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
     bool has_bvh = false;
@@ -33,6 +35,14 @@ struct SrtScene {
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     cudaStream_t stream = nullptr;
+    // Host entry points that use the scene's stream and scratch serialise on
+    // `mu` (calls on one handle serialise).  Launches on
+    // caller streams (the *_device entry points) take a fresh work counter
+    // from the ring, so concurrent streams never share one.
+    mutable std::mutex mu;
+    static constexpr uint32_t kWorkRing = 64;
+    mutable std::atomic<uint32_t> work_next{0};
+    uint32_t *next_work() const { return d_work + 32u * (work_next.fetch_add(1u) % kWorkRing); }
     srt::SceneView view() const {
         srt::SceneView v;
         v.means64 = d_means;

@@ -80,6 +80,7 @@ template <int NS, int MODE, int RNG, bool STATS>
 __device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r, const WalkCfg &w, int slot,
                                            Slots<NS> &sl, float &far, Counters<STATS> &ct) {
     ct.add(1, 1);
+    SRT_DCHECK(slot >= 0 && slot < s.n);
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
     float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
     // stage 1: fp32 screen -- can this candidate be accepted by any slot?
@@ -200,6 +201,7 @@ __device__ __forceinline__ int visit_node(const SceneView &s, const RayState &r,
     ct.add(0, 1);
     int4 kids;
     int key[4];
+    SRT_DCHECK(node >= 0 && node < s.num_nodes4);
     unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), wk.far, kids, key);
     unsigned leafm = 0;
 #pragma unroll
@@ -311,6 +313,7 @@ struct CameraSource {
         for (int k = 0; k < NS && k < a.nslots; ++k) {
             int pid = sl.id[k];
             if (pid >= 0) {
+                SRT_DCHECK(pid < s.n);
                 float3 c = sh_color(s.sh, s.sh_k, s.sh_deg, pid, fx, fy, fz);
                 r += c.x;
                 g += c.y;
@@ -465,6 +468,7 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
                                          unsigned long long *best, const uint32_t *keys, float far,
                                          Counters<STATS> &ct) {
     ct.add(1, 1);
+    SRT_DCHECK(slot >= 0 && slot < s.n);
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
     float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
     Screen sc = screen<MODE>(r, m, a, b, w.s2, w.sqrt_s2, far);
@@ -501,6 +505,7 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
                                            const WalkCfg &w, int slot, unsigned long long *best,
                                            const uint32_t *keys, float far, Counters<STATS> &ct) {
     ct.add(1, 1);
+    SRT_DCHECK(slot >= 0 && slot < s.n);
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
     float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
     Screen sc = screen<MODE>(sr, m, a, b, w.s2, w.sqrt_s2, far);
@@ -783,6 +788,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             if (lane == 0) ct.add(0, 1);
             int4 kids;
             int key[4];
+            SRT_DCHECK(node >= 0 && node < s.num_nodes4);
             const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
             unsigned hitm = slab4<true>(r, np, far, kids, key);
             const unsigned lt = (1u << lane) - 1u;
@@ -802,6 +808,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     unsigned bm = __ballot_sync(FULL, h);
                     if (h) {
                         int o = njobs + __popc(bm & lt);
+                        SRT_DCHECK(o < BATCH + 128);
                         sjob[wid][o] = ~pick(kids, k);
                         sown[wid][o] = (unsigned char)lane;
                     }
@@ -823,6 +830,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     }
                     if (lane == 0)
                         for (int j = n - 1; j >= 1; --j) {
+                            SRT_DCHECK(sp < PSTACK);
                             sstk_node[wid][sp] = pick(kids, order[j]);
                             sstk_key[wid][sp] = 0;
                             ++sp;
@@ -845,6 +853,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     unsigned bm = __ballot_sync(FULL, h);
                     if (h) {
                         int o = njobs + __popc(bm & lt);
+                        SRT_DCHECK(o < BATCH + 128);
                         sjob[wid][o] = ~code;
                         sown[wid][o] = (unsigned char)lane;
                     }
@@ -877,6 +886,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
 #pragma unroll
                     for (int j = 3; j >= 1; --j)
                         if (j < nin) {
+                            SRT_DCHECK(sp + nin - 1 - j < PSTACK);
                             sstk_node[wid][sp + nin - 1 - j] = pick(kids, wkey[j] & 3);
                             sstk_key[wid][sp + nin - 1 - j] = wkey[j] & ~3;
                         }
@@ -896,6 +906,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                         if (lane == 0) ct.add(5, 1);
                         if (sstk_key[wid][sp] <= maxfar) {
                             node = sstk_node[wid][sp];
+                            SRT_DCHECK(node >= 0 && node < s.num_nodes4);
                             break;
                         }
                         if (lane == 0) ct.add(6, 1);
@@ -940,13 +951,14 @@ static srt_status launch_trace_v(const SrtScene *s, const Src &src, const WalkCf
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    uint32_t *work = s->next_work();
+    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace<NS, MODE, RNG, Src, REFILL, STATS>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace launch");
 }
 
@@ -963,13 +975,14 @@ static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const Wal
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    uint32_t *work = s->next_work();
+    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_coop<NS, MODE, RNG, Src, STATS>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_coop launch");
 }
 
@@ -994,13 +1007,14 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    srt_status rc = cuda_status(cudaMemsetAsync(s->d_work, 0, sizeof(uint32_t), st), "work counter reset");
+    uint32_t *work = s->next_work();
+    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, s->d_work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
 }
 
@@ -1149,6 +1163,7 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
     while (node != kDone) {
         int4 kids;
         int key[4];
+        SRT_DCHECK(node >= 0 && node < s.num_nodes4);
         unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), r.t_max0, kids, key);
         node = kDone;
         while (hitm) {
@@ -1156,6 +1171,7 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
             hitm &= hitm - 1;
             int code = pick(kids, k);
             if (code < 0) {
+                SRT_DCHECK(~code < s.n);
                 const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~code);
                 float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
                 Cand cd = candidate<MODE>(r, m, a, b, s2);

@@ -43,6 +43,7 @@ __device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, in
     int sp = 0;
     int node = 0;
     while (node >= 0) {
+        SRT_DCHECK(node >= 0 && node < s.num_nodes4);
         const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
         float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3),
                loz = __ldg(np + 4), hiz = __ldg(np + 5);
@@ -70,6 +71,7 @@ __device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, in
                 continue;
             }
             int slot = ~kid[k];
+            SRT_DCHECK(slot < s.n);
             int pid = __float_as_int(s.geom[slot].b.z);
             double t, resid, px, py, pz;
             if (!candidate<MODE>(r, s.means64 + (int64_t)pid * 3, s.cov64 + (int64_t)pid * 6, s2, t, resid, px, py,

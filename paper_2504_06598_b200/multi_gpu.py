@@ -228,3 +228,49 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
         return None
     f = frame.double().cpu().numpy()
     return AccumBuffer(f[..., :3], f[..., 3], settings.samples_per_pixel)
+
+
+def render_devices(asset, camera, settings, devices, rng: str = "counter"):
+    """Single-process multi-GPU render (SURVEY.md 8(b) "plus optional devices";
+    8(e) tile sharding): one host thread drives every device -- shard i of G
+    traces the interleaved tiles t % G == i on ``devices[i]`` into a
+    tile-compact buffer (async launches on per-device streams), the buffers
+    are copied to ``devices[0]`` (peer copies over NVLink) and unpacked there
+    by ``srt_unpack_tiles_device``.  The counter stream is keyed per pixel, so
+    the frame equals the single-GPU render bit for bit.  A device may appear
+    more than once (its shards then run back to back on one stream)."""
+    import torch
+
+    from .render import AccumBuffer, prepare
+    from .scene import camera_tuple, make_camera, make_render_params, shard_tiles, unpack_tiles_device
+
+    devices = [int(d) for d in devices]
+    G = len(devices)
+    if G == 0:
+        raise ValueError("devices must name at least one GPU")
+    W, H = settings.width, settings.height
+    cam = make_camera(camera_tuple(camera, W, H))
+    mode = 0 if settings.depth_mode == "mean" else 1
+    max_tiles = max_shard_tiles(W, H, G)
+    outs = []
+    for i, d in enumerate(devices):
+        sc = prepare(asset, settings, device=d)
+        dev = torch.device("cuda", d)
+        prm = make_render_params(W, H, settings.passes, settings.multisample, mode, settings.cutoff_s ** 2, True,
+                                 settings.seed, settings.background, 0, i, G, rng=rng)
+        tiles = max(shard_tiles(W, H, i, G), 1)
+        hits = torch.empty(tiles * 256 * settings.multisample, dtype=torch.int32, device=dev)
+        acc = torch.empty((tiles * 256, 4), dtype=torch.float32, device=dev)
+        out = torch.zeros((max_tiles * 256, 4), dtype=torch.float32, device=dev)
+        sc.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(),
+                         torch.cuda.current_stream(dev).cuda_stream)
+        outs.append(out)
+    d0 = torch.device("cuda", devices[0])
+    for d in set(devices):
+        torch.cuda.current_stream(torch.device("cuda", d)).synchronize()
+    packed = torch.cat([o.to(d0).reshape(-1) for o in outs])
+    frame = torch.zeros(H * W * 4, dtype=torch.float32, device=d0)
+    unpack_tiles_device(packed.data_ptr(), W, H, G, max_tiles, frame.data_ptr(),
+                        torch.cuda.current_stream(d0).cuda_stream)
+    f = frame.reshape(H, W, 4).double().cpu().numpy()
+    return AccumBuffer(f[..., :3], f[..., 3], settings.samples_per_pixel)

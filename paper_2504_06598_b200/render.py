@@ -145,7 +145,7 @@ def prepare(asset, settings: RenderSettings, bvh=None, device: int = 0) -> Devic
 
 
 def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, threads: int | None = None,
-           device: int = 0, rng: str = "counter") -> AccumBuffer:
+           device: int = 0, rng: str = "counter", devices=None) -> AccumBuffer:
     """Render a frame on the GPU (render.py:125-174).
 
     ``threads`` is accepted for signature compatibility (the reference's CPU
@@ -153,8 +153,14 @@ def render(asset, camera: CameraConfig, settings: RenderSettings, bvh=None, thre
     reference's own trig-hash stream in fp64 (parity mode, slower).
     ``settings.reference_mode`` renders exact sorted compositing instead
     (render_exact, kernels.py:677-723), with ``spp = passes``.
+    ``devices=[d0, d1, ...]`` shards 16x16 tiles over several GPUs from this
+    one process (``multi_gpu.render_devices``); same frame, bit for bit.
     """
     del threads
+    if devices is not None and len(devices) > 1 and not settings.reference_mode and bvh is None:
+        from .multi_gpu import render_devices
+
+        return render_devices(asset, camera, settings, devices, rng=rng)
     sc = prepare(asset, settings, bvh, device)
     cam = camera_tuple(camera, settings.width, settings.height)
     mode = 0 if settings.depth_mode == "mean" else 1

@@ -200,6 +200,19 @@ class DeviceScene:
                                          _ptr(out_t), _ptr(out_id)))
         return out_t, out_id
 
+    def trace_rays_device(self, d_rays: int, num_rays: int, nslots: int, d_t: int, d_id: int, stream: int,
+                          t_min=0.0, t_max=TMAX, mode=0, s2=8.0, clip=True, seed=0, ray_id0=0, sample0=0) -> None:
+        """srt_trace_rays_device: counter-RNG walks of device-resident rays
+        (d_rays: (R, 6) f64 origin+direction) into device outputs d_t (R, N)
+        f32 and d_id (R, N) i32, asynchronously on `stream`."""
+        p = SrtTraceParams()
+        p.t_min, p.t_max, p.mode, p.clip, p.s2 = float(t_min), float(t_max), int(mode), int(bool(clip)), float(s2)
+        p.rng = RNG["counter"]
+        p.seed, p.ray_id0, p.sample0 = seed & 0xFFFFFFFF, ray_id0 & 0xFFFFFFFF, sample0 & 0xFFFFFFFF
+        check(_lib.load().srt_trace_rays_device(self.handle, ctypes.byref(p), ctypes.c_void_p(d_rays), int(num_rays),
+                                                int(nslots), ctypes.c_void_p(d_t), ctypes.c_void_p(d_id),
+                                                ctypes.c_void_p(stream)))
+
     def transmittance(self, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0) -> np.ndarray:
         o = _c64(origins).reshape(-1, 3)
         d = _c64(dirs).reshape(-1, 3)

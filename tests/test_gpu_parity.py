@@ -362,3 +362,51 @@ def test_mapped_host_output_equals_copy_path(passes, nslots):
     np.testing.assert_array_equal(rgb_m, rgb_c)
     np.testing.assert_array_equal(op_m, op_c)
     assert op_c.max() > 0
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_render_devices_equals_single_gpu(devices):
+    """render(..., devices=[...]) shards interleaved tiles over the listed GPUs
+    from one process (the same device may repeat: shards then run back to
+    back); the unpacked frame equals the single-GPU render bit for bit."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(4_000, seed=21, sh_degree=1)
+    st = RenderSettings(width=100, height=52, spp=4, multisample=2, seed=9, background=[0.2, 0.1, 0.0])
+    one = render(a, front_camera(), st)
+    many = render(a, front_camera(), st, devices=devices)
+    np.testing.assert_array_equal(many.rgb, one.rgb)
+    np.testing.assert_array_equal(many.opacity, one.opacity)
+    assert many.spp == one.spp == 4
+
+
+def test_concurrent_renders_on_one_scene():
+    """Host entry points on one scene handle serialise (SURVEY.md 8(b)
+    threading row): four threads rendering the same cached scene get the
+    frame a single call produces."""
+    import threading
+
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(3_000, seed=4, sh_degree=2)
+    st = RenderSettings(width=64, height=48, spp=2, seed=5)
+    want = render(a, front_camera(), st)
+    got, errs = [None] * 4, []
+
+    def run(i):
+        try:
+            got[i] = render(a, front_camera(), st)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    for g in got:
+        np.testing.assert_array_equal(g.rgb, want.rgb)
+        np.testing.assert_array_equal(g.opacity, want.opacity)
