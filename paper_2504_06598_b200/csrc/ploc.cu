@@ -46,6 +46,7 @@ __global__ void k_ploc_nn(int nc, int radius, const float4 *__restrict__ lo, con
         float4 ul = make_float4(fminf(l.x, l2.x), fminf(l.y, l2.y), fminf(l.z, l2.z), 0.f);
         float4 uh = make_float4(fmaxf(h.x, h2.x), fmaxf(h.y, h2.y), fmaxf(h.z, h2.z), 0.f);
         float a = half_area(ul, uh);
+        if (!(a <= 3.0e38f)) a = INFINITY;  // degenerate (unbounded) boxes: inf*0 must not give NaN orderings
         // ties go to the partner i ^ 1 (then the lower index): runs of equal
         // boxes pair up all at once and build a balanced subtree
         if (a < best || (a == best && j == (i ^ 1))) {

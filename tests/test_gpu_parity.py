@@ -410,3 +410,33 @@ def test_concurrent_renders_on_one_scene():
     for g in got:
         np.testing.assert_array_equal(g.rgb, want.rgb)
         np.testing.assert_array_equal(g.opacity, want.opacity)
+
+
+@pytest.mark.parametrize("method", ["ploc", "lbvh"])
+def test_degenerate_primitives_are_skipped(oracle, method):
+    """Degenerate primitives -- zero, indefinite and non-finite inverse
+    covariances -- are skipped by the candidate test exactly as in the
+    reference (kernels.py:167-168); their unbounded boxes must not break the
+    GPU builders or the walk."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(3_000, seed=6)
+    pk = a.packed
+    cov = pk.cov_inv6.copy()
+    bad = np.arange(0, 3_000, 37)
+    cov[bad[0::3]] = 0.0                                   # dAd = 0
+    cov[bad[1::3]] = [-1.0, 0.0, 0.0, -1.0, 0.0, -1.0]     # negative definite
+    cov[bad[2::3], 0] = np.nan                             # non-finite
+    o, d = random_rays(np.random.default_rng(3), 2_000)
+    sc = DeviceScene(pk.means, cov, pk.opacities, pk.sh, pk.sh_degree)
+    sc.build_bvh(CUTOFF, method=method)
+    table = np.zeros((3_000, 1))
+    t, ids = sc.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 1, rng="table", table=table)
+    sc.close()
+    assert not np.isin(ids, bad).any()
+    lo, hi = a.aabb_arrays(CUTOFF)
+    ob = oracle.sah_build(lo, hi)
+    ot, oid = oracle.trace_batch(ob, pk.means, cov, pk.opacities, o, d, 0.0, TMAX, 0, S2, True, 1, rng="table",
+                                 table=table)
+    assert np.mean(ids == oid) >= 0.999
