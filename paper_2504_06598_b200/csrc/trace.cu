@@ -497,6 +497,12 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
         }
 }
 
+// The fields of a ray the exact candidate reads (a light RayState).
+struct ExactRay {
+    double ox, oy, oz, dx, dy, dz, inv_dd;
+    float fdx, fdy, fdz, t_min, t_max0;
+};
+
 // Leaf job of the packet kernel: screen on the owner's fp32 direction and
 // the shared camera origin; the exact fp64 stage rebuilds the owner's ray
 // from its fp64 direction only when the screen cannot decide.
@@ -512,22 +518,32 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
     if (!sc.maybe) return;
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
+    // single-slot walks draw once and reuse the draw in the exact stage
+    const float u0 = NS == 1 ? counter_u(keys[0], (uint32_t)pid) : 0.0f;
     bool need = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k)
-        if (sc.t_lo <= unpack_t(best[k])) need |= counter_u(keys[k], (uint32_t)pid) <= sc.alpha_hi;
+        if (sc.t_lo <= unpack_t(best[k]))
+            need |= (NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid)) <= sc.alpha_hi;
     if (!need) return;
     ct.add(3, 1);
-    RayState r;
-    init_ray(r, cam.e[0], cam.e[1], cam.e[2], dd[0], dd[1], dd[2], 0.0, DBL_MAX);
+    // the camera ray's fields the exact candidate reads; camera directions are
+    // unit in fp64 to an ulp, and 1/|d|^2 only sets the re-centring point,
+    // so inv_dd = 1 (as in the screen) changes the fp32 result by < 1e-15
+    ExactRay r;
+    r.ox = cam.e[0], r.oy = cam.e[1], r.oz = cam.e[2];
+    r.dx = dd[0], r.dy = dd[1], r.dz = dd[2];
+    r.inv_dd = 1.0;
+    r.fdx = (float)r.dx, r.fdy = (float)r.dy, r.fdz = (float)r.dz;
+    r.t_min = 0.0f, r.t_max0 = INFINITY;
     // one re-centring: the second (peak) re-centring only matters for extreme
     // anisotropy and would raise this loop's register count by ~10
-    Cand c = candidate<MODE, RayState, false>(r, m, a, b, w.s2);
+    Cand c = candidate<MODE, ExactRay, false>(r, m, a, b, w.s2);
     if (!c.valid) return;
     unsigned long long key = pack_hit(c.t, pid);
 #pragma unroll
     for (int k = 0; k < NS; ++k)
-        if (key < best[k] && counter_u(keys[k], (uint32_t)pid) < c.alpha) {
+        if (key < best[k] && (NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid)) < c.alpha) {
             atomicMin(best + k, key);
             ct.add(4, 1);
         }
