@@ -17,7 +17,12 @@ KEYS = [
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-    "smsp__sass_average_branch_targets_threads_uniform.pct",
+    "smsp__sass_average_branch_targets_threads_uniform.pct", "lts__t_sectors.sum",
+    "lts__t_sectors_srcunit_tex_op_read.sum", "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "smsp__thread_inst_executed_per_inst_executed.pct",
 ]
 
 
@@ -53,6 +58,18 @@ def main():
     rep, lcsv, outdir = sys.argv[1], sys.argv[2], Path(sys.argv[3])
     outdir.mkdir(parents=True, exist_ok=True)
     summary = {"full": raw(rep)}
+    # achieved bandwidths of each profiled launch (DRAM, L2 = 32-B sectors)
+    for k in summary["full"]:
+        try:
+            ms = float(k["gpu__time_duration.sum"][0]) * (1e-3 if k["gpu__time_duration.sum"][1] == "us" else 1.0)
+            unit = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+            dr = sum(float(k[m][0]) * unit[k[m][1]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            l2 = float(k["lts__t_sectors.sum"][0]) * 32 / 1e6
+            k["derived.dram_GBps"] = (f"{dr / ms:.1f}", "GB/s")
+            k["derived.l2_GBps"] = (f"{l2 / ms:.1f}", "GB/s")
+            k["derived.l2_bytes_per_launch"] = (f"{l2:.1f}", "Mbyte")
+        except (KeyError, ValueError):
+            pass
     if lcsv != "-":
         summary["launch_list"] = launches(lcsv)
     (outdir / "ncu_summary.json").write_text(json.dumps(summary, indent=1))
