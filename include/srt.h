@@ -223,6 +223,23 @@ srt_status srt_render_pass_device(const SrtScene *scene, const SrtCamera *camera
                                   const SrtRenderParams *params, int32_t pass, float *d_accum,
                                   int32_t first, int32_t last, float *d_out, void *stream);
 /* Whole frame on device: all passes, d_out (H*W) float4 rgba means. */
+/* All params->passes passes of a frame in ONE launch over every (packet,
+ * pass): samples are summed in 2^-32 fixed point with integer atomics (order
+ * independent, bitwise deterministic) into d_acc ((local tiles*256) * 4
+ * uint64, zeroed by the call), then resolved to float4 means in d_out
+ * (row-major H*W, or tile-compact when sharded).  Counter stream only.
+ * Balances small frames and many-pass convergence runs far better than one
+ * launch per pass.  d_out may be NULL: only the sums are produced (see
+ * srt_resolve_frame_device). */
+srt_status srt_render_frame_device(const SrtScene *scene, const SrtCamera *camera,
+                                   const SrtRenderParams *params, uint64_t *d_acc, float *d_out,
+                                   void *stream);
+/* Fixed-point sums of the shard params->shard_index / shard_count (as left by
+ * srt_render_frame_device) -> f64 means written row-major into the full-frame
+ * device (or mapped host) buffers d_rgb (H,W,3) and d_op (H,W); each shard
+ * writes only its own pixels.  Runs on the current device. */
+srt_status srt_resolve_frame_device(const SrtRenderParams *params, const uint64_t *d_acc, double *d_rgb,
+                                    double *d_op, void *stream);
 srt_status srt_render_device(const SrtScene *scene, const SrtCamera *camera,
                              const SrtRenderParams *params, int32_t *d_hits, float *d_accum,
                              float *d_out, void *stream);

@@ -94,6 +94,9 @@ SYMBOLS = [
                                      _vp, _i32, _i32, _vp, _vp]),
     ("srt_render_pass_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _i32, _vp,
                                       _i32, _i32, _vp, _vp]),
+    ("srt_render_frame_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp,
+                                       _vp]),
+    ("srt_resolve_frame_device", _i32, [ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp, _vp]),
     ("srt_render_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp,
                                  _vp]),
     ("srt_trace_stats", _i32, [_vp, _vp, _i32]),

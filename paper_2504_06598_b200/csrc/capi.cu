@@ -872,6 +872,42 @@ srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const S
     return rc;
 }
 
+srt_status srt_render_frame_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p,
+                                   uint64_t *d_acc, float *d_out, void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_acc) {
+        set_error("null camera or buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (p->rng == SRT_RNG_TRIG64) {
+        set_error("the one-launch frame draws the counter stream; use srt_render_device for trig64");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    RenderArgs a = make_render_args(p);
+    cudaStream_t st = (cudaStream_t)stream;
+    rc = cuda_status(cudaMemsetAsync(d_acc, 0, sizeof(uint64_t) * 4 * a.local_tiles * 256, st), "accumulator reset");
+    if (!rc)
+        rc = launch_render_frame_multipass(s, make_cam(camera), a, p->pass0, p->passes,
+                                           (unsigned long long *)d_acc, st);
+    if (!rc && d_out)
+        rc = launch_resolve_fixed(a, (unsigned long long *)d_acc, p->passes, (float4 *)d_out, nullptr, nullptr, st);
+    return rc;
+}
+
+srt_status srt_resolve_frame_device(const SrtRenderParams *p, const uint64_t *d_acc, double *d_rgb, double *d_op,
+                                    void *stream) {
+    if (!p || !d_acc || !d_rgb || !d_op || p->width < 1 || p->height < 1 || p->passes < 1 || p->nslots < 1 ||
+        p->shard_count < 0 || (p->shard_count > 0 && (p->shard_index < 0 || p->shard_index >= p->shard_count))) {
+        set_error("invalid resolve parameters");
+        return SRT_ERR_INVALID_ARG;
+    }
+    RenderArgs a = make_render_args(p);
+    return launch_resolve_fixed(a, (const unsigned long long *)d_acc, p->passes, nullptr, d_rgb, d_op,
+                                (cudaStream_t)stream);
+}
+
 srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRenderParams *p, double *out_rgb,
                       double *out_op, int64_t *out_ids) {
     SRT_LOCK(sc);
@@ -905,6 +941,32 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     float4 *d_out = (float4 *)(base + al(hits_bytes) + al(acc_bytes));
     double *d_rgb = (double *)(base + al(hits_bytes) + al(acc_bytes) + al(out_bytes));
     double *d_op = d_rgb + npix * 3;
+    // Several counter-stream passes: one balanced launch over every (packet,
+    // pass), fixed-point sums, one resolve straight into the f64 outputs.
+    if (p->passes > 1 && a.rng != SRT_RNG_TRIG64 && !out_ids) {
+        size_t acc_bytes64 = sizeof(unsigned long long) * 4 * cpix;
+        rc = scratch_reserve(s, al(acc_bytes64) + al(f64_bytes));
+        if (rc) return rc;
+        unsigned long long *d_acc64 = (unsigned long long *)s->d_scratch;
+        double *f_rgb = (double *)((char *)s->d_scratch + al(acc_bytes64));
+        double *f_op = f_rgb + npix * 3;
+        double *m_rgb = mapped_host(out_rgb), *m_op = mapped_host(out_op);
+        bool direct = m_rgb && m_op;
+        rc = cuda_status(cudaMemsetAsync(d_acc64, 0, acc_bytes64, st), "accumulator reset");
+        if (!rc) rc = launch_render_frame_multipass(s, cam, a, p->pass0, p->passes, d_acc64, st);
+        if (!rc)
+            rc = launch_resolve_fixed(a, d_acc64, p->passes, nullptr, direct ? m_rgb : f_rgb, direct ? m_op : f_op,
+                                      st);
+        if (!rc && !direct) {
+            rc = cuda_status(cudaMemcpyAsync(out_rgb, f_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st),
+                             "rgb download");
+            if (!rc)
+                rc = cuda_status(cudaMemcpyAsync(out_op, f_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st),
+                                 "opacity download");
+        }
+        if (!rc) rc = check_flag(s, st);
+        return rc;
+    }
     // Outputs in mapped page-locked memory (srt_host_alloc): the last fused
     // pass stores the f64 frame straight into them, so the device->host
     // transfer overlaps the walk and no resolve kernel or copy follows.

@@ -94,6 +94,41 @@ srt_status launch_resolve_f64(const RenderArgs &a, const float4 *d_out, double *
     return cuda_status(cudaGetLastError(), "k_resolve_f64 launch");
 }
 
+// Fixed-point frame sums (unit * 4 u64, 2^-32 units; opacity in 2^32 units)
+// -> per-pixel means: float4 d_out (row-major unsharded, tile-compact when
+// sharded) or, when d_rgb is set, the f64 frame (H,W,3)+(H,W) straight into
+// its final (possibly mapped host) buffers.
+__global__ void k_resolve_fixed(RenderArgs a, int64_t unit, const unsigned long long *__restrict__ acc, double inv,
+                                float4 *out, double *rgb, double *op) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= unit) return;
+    int px, py;
+    tile_pixel_s(a, i >> 8, (int)(i & 255), px, py);
+    if (px >= a.width || py >= a.height) return;
+    const unsigned long long *q = acc + i * 4;
+    const double k = inv * 2.3283064365386963e-10;  // 2^-32
+    double r = (double)q[0] * k, g = (double)q[1] * k, b = (double)q[2] * k, o = (double)(q[3] >> 32) * inv;
+    if (rgb) {
+        int64_t pix = (int64_t)py * a.width + px;
+        rgb[pix * 3 + 0] = r;
+        rgb[pix * 3 + 1] = g;
+        rgb[pix * 3 + 2] = b;
+        op[pix] = o;
+    } else {
+        int64_t oidx = a.shard_count > 1 ? i : (int64_t)py * a.width + px;
+        out[oidx] = make_float4((float)r, (float)g, (float)b, (float)o);
+    }
+}
+
+srt_status launch_resolve_fixed(const RenderArgs &a, const unsigned long long *d_acc, int npass, float4 *d_out,
+                                double *d_rgb, double *d_op, cudaStream_t st) {
+    int64_t unit = a.local_tiles * 256;
+    if (unit == 0) return SRT_OK;
+    double inv = 1.0 / ((double)npass * (double)a.nslots);
+    k_resolve_fixed<<<(unsigned)((unit + 255) / 256), 256, 0, st>>>(a, unit, d_acc, inv, d_out, d_rgb, d_op);
+    return cuda_status(cudaGetLastError(), "k_resolve_fixed launch");
+}
+
 // gathered: [shard][max_tiles*256] float4, tile-compact per shard.
 __global__ void k_unpack_tiles(const float4 *__restrict__ gathered, int width, int height, int shard_count,
                                int64_t max_tiles, int tiles_x, int64_t total_tiles, float4 *frame) {

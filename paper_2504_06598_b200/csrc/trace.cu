@@ -272,19 +272,33 @@ struct CameraSource {
     int pass;
     uint32_t fkey;
     int32_t *hits;
-    __host__ __device__ __forceinline__ uint32_t total() const { return (uint32_t)(a.local_tiles * 256); }
+    // Multi-pass launches (npass > 1): work item idx covers pass
+    // pass + idx / unit of tile-compact pixel idx % unit; a packet never
+    // straddles two passes (unit is a multiple of 256).  Results are summed
+    // into acc64 in 2^-32 fixed point with integer atomics, so the sum does
+    // not depend on which warp ran which (packet, pass) -- bitwise
+    // deterministic -- and the whole frame is one balanced launch.
+    unsigned long long *acc64;
+    uint32_t npass, unit;
+    __host__ __device__ __forceinline__ uint32_t total() const { return unit * npass; }
     template <int NS>
     __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
+        uint32_t ps = (uint32_t)pass;
+        if (npass > 1) {
+            uint32_t f = idx / unit;
+            idx -= f * unit;
+            ps += f;
+        }
         int px, py;
         tile_pixel(a, idx >> 8, idx & 255, px, py);
         if (px >= a.width || py >= a.height) return false;
         double dx, dy, dz;
-        camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)pass, a.seed, a.width, a.height, dx, dy, dz);
+        camera_ray(cam, (uint32_t)px, (uint32_t)py, ps, a.seed, a.width, a.height, dx, dy, dz);
         init_ray(r, cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX);
         init_slots<NS>(sl, a.nslots);
         uint32_t ray_id = (uint32_t)py * (uint32_t)a.width + (uint32_t)px;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, (uint32_t)pass * (uint32_t)a.nslots + k);
+        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, ps * (uint32_t)a.nslots + k);
         return true;
     }
     // fused shading (hits == nullptr): accumulate straight from the walk
@@ -324,6 +338,14 @@ struct CameraSource {
                 g += a.bg[1];
                 b += a.bg[2];
             }
+        }
+        if (acc64) {
+            unsigned long long *q = acc64 + (int64_t)(idx % unit) * 4;
+            atomicAdd(q + 0, __float2ull_rn(r * 4294967296.0f));
+            atomicAdd(q + 1, __float2ull_rn(g * 4294967296.0f));
+            atomicAdd(q + 2, __float2ull_rn(b * 4294967296.0f));
+            atomicAdd(q + 3, (unsigned long long)(unsigned)o << 32);  // hit count in the high word
+            return;
         }
         float4 acc = first ? make_float4(0.f, 0.f, 0.f, 0.f) : accum[idx];
         acc.x += r;
@@ -1116,6 +1138,9 @@ srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const Re
     src.out = d_out;
     src.rgb64 = d_rgb64;
     src.op64 = d_op64;
+    src.acc64 = nullptr;
+    src.npass = 1;
+    src.unit = (uint32_t)(a.local_tiles * 256);
     src.first = first ? 1 : 0;
     src.last = last ? 1 : 0;
     src.cam = cam;
@@ -1133,6 +1158,39 @@ srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const Re
         x ^= x >> 16;
         src.fkey = x;
     }
+    WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
+    return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
+}
+
+// All `npass` passes (pass0 ...) of a frame in ONE packet launch, summed into
+// the zeroed fixed-point accumulator d_acc64 (unit * 4 u64); see CameraSource.
+srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass0,
+                                         int npass, unsigned long long *d_acc64, cudaStream_t st) {
+    CameraSource src;
+    src.accum = nullptr;
+    src.out = nullptr;
+    src.rgb64 = nullptr;
+    src.op64 = nullptr;
+    src.first = 0;
+    src.last = 0;
+    src.cam = cam;
+    src.a = a;
+    src.pass = pass0;
+    src.hits = nullptr;
+    src.acc64 = d_acc64;
+    src.unit = (uint32_t)(a.local_tiles * 256);
+    src.npass = (uint32_t)npass;
+    if ((uint64_t)src.unit * (uint64_t)npass > 0xFFFFFFFFull) {
+        set_error("too many (pixel, pass) work items in one launch");
+        return SRT_ERR_INVALID_ARG;
+    }
+    uint32_t x = a.seed ^ 0x9E3779B9u;
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    src.fkey = x;
     WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
     return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
 }

@@ -198,10 +198,9 @@ def gpu_shard_renderer(scene, camera_tuple, settings, device):
             return out
         # trace scratch in the tile-compact layout of the traced tiles
         tiles = shard_tiles(p.width, p.height, p.rank, p.world) if p.mode == "tiles" else shard_tiles(p.width, p.height)
-        hits = torch.empty(max(tiles, 1) * 256 * settings.multisample, dtype=torch.int32, device=dev)
-        acc = torch.empty((max(tiles, 1) * 256, 4), dtype=torch.float32, device=dev)
-        scene.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(),
-                            torch.cuda.current_stream(dev).cuda_stream)
+        # every pass in one launch, fixed-point sums (bitwise the render() frame)
+        acc = torch.empty((max(tiles, 1) * 256, 4), dtype=torch.int64, device=dev)
+        scene.render_frame_device(cam, prm, acc.data_ptr(), out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream)
         return out
 
     return run
@@ -233,16 +232,18 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
 def render_devices(asset, camera, settings, devices, rng: str = "counter"):
     """Single-process multi-GPU render (SURVEY.md 8(b) "plus optional devices";
     8(e) tile sharding): one host thread drives every device -- shard i of G
-    traces the interleaved tiles t % G == i on ``devices[i]`` into a
-    tile-compact buffer (async launches on per-device streams), the buffers
-    are copied to ``devices[0]`` (peer copies over NVLink) and unpacked there
-    by ``srt_unpack_tiles_device``.  The counter stream is keyed per pixel, so
-    the frame equals the single-GPU render bit for bit.  A device may appear
-    more than once (its shards then run back to back on one stream)."""
+    traces the interleaved tiles t % G == i on ``devices[i]`` in one launch
+    (every pass, fixed-point sums, async on per-device streams); the sums are
+    copied to ``devices[0]`` (peer copies over NVLink) and resolved there into
+    one f64 frame, each shard writing its own pixels.  The counter stream is
+    keyed per pixel and the sums are exact, so the frame equals the
+    single-GPU render bit for bit.  A device may appear more than once (its
+    shards then run back to back on one stream).  Single-pass frames and
+    rng="trig64" take the per-pass path with float means, as render() does."""
     import torch
 
     from .render import AccumBuffer, prepare
-    from .scene import camera_tuple, make_camera, make_render_params, shard_tiles, unpack_tiles_device
+    from .scene import camera_tuple, make_camera, make_render_params, resolve_frame_device, shard_tiles
 
     devices = [int(d) for d in devices]
     G = len(devices)
@@ -251,26 +252,43 @@ def render_devices(asset, camera, settings, devices, rng: str = "counter"):
     W, H = settings.width, settings.height
     cam = make_camera(camera_tuple(camera, W, H))
     mode = 0 if settings.depth_mode == "mean" else 1
-    max_tiles = max_shard_tiles(W, H, G)
-    outs = []
+    d0 = torch.device("cuda", devices[0])
+    fixed = rng == "counter" and settings.passes > 1  # srt_render's multi-pass path
+    prms, bufs = [], []
     for i, d in enumerate(devices):
         sc = prepare(asset, settings, device=d)
         dev = torch.device("cuda", d)
         prm = make_render_params(W, H, settings.passes, settings.multisample, mode, settings.cutoff_s ** 2, True,
                                  settings.seed, settings.background, 0, i, G, rng=rng)
         tiles = max(shard_tiles(W, H, i, G), 1)
-        hits = torch.empty(tiles * 256 * settings.multisample, dtype=torch.int32, device=dev)
-        acc = torch.empty((tiles * 256, 4), dtype=torch.float32, device=dev)
-        out = torch.zeros((max_tiles * 256, 4), dtype=torch.float32, device=dev)
-        sc.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(),
-                         torch.cuda.current_stream(dev).cuda_stream)
-        outs.append(out)
-    d0 = torch.device("cuda", devices[0])
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        if fixed:
+            acc = torch.empty((tiles * 256, 4), dtype=torch.int64, device=dev)
+            sc.render_frame_device(cam, prm, acc.data_ptr(), 0, stream)
+            bufs.append(acc)
+        else:
+            hits = torch.empty(tiles * 256 * settings.multisample, dtype=torch.int32, device=dev)
+            acc = torch.empty((tiles * 256, 4), dtype=torch.float32, device=dev)
+            out = torch.zeros((max_shard_tiles(W, H, G) * 256, 4), dtype=torch.float32, device=dev)
+            sc.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), out.data_ptr(), stream)
+            bufs.append(out)
+        prms.append(prm)
     for d in set(devices):
         torch.cuda.current_stream(torch.device("cuda", d)).synchronize()
-    packed = torch.cat([o.to(d0).reshape(-1) for o in outs])
+    s0 = torch.cuda.current_stream(d0).cuda_stream
+    if fixed:
+        rgb = torch.zeros((H, W, 3), dtype=torch.float64, device=d0)
+        op = torch.zeros((H, W), dtype=torch.float64, device=d0)
+        with torch.cuda.device(d0):
+            for prm, acc in zip(prms, bufs):
+                a0 = acc.to(d0)
+                resolve_frame_device(prm, a0.data_ptr(), rgb.data_ptr(), op.data_ptr(), s0)
+            torch.cuda.current_stream(d0).synchronize()
+        return AccumBuffer(rgb.cpu().numpy(), op.cpu().numpy(), settings.samples_per_pixel)
+    from .scene import unpack_tiles_device
+
+    packed = torch.cat([o.to(d0).reshape(-1) for o in bufs])
     frame = torch.zeros(H * W * 4, dtype=torch.float32, device=d0)
-    unpack_tiles_device(packed.data_ptr(), W, H, G, max_tiles, frame.data_ptr(),
-                        torch.cuda.current_stream(d0).cuda_stream)
+    unpack_tiles_device(packed.data_ptr(), W, H, G, max_shard_tiles(W, H, G), frame.data_ptr(), s0)
     f = frame.reshape(H, W, 4).double().cpu().numpy()
     return AccumBuffer(f[..., :3], f[..., 3], settings.samples_per_pixel)

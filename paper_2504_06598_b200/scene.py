@@ -321,10 +321,24 @@ class DeviceScene:
                                                  int(pass_index), ctypes.c_void_p(d_accum), int(bool(first)),
                                                  int(bool(last)), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)))
 
+    def render_frame_device(self, camera, prm, d_acc, d_out, stream) -> None:
+        """srt_render_frame_device: every pass of the frame in one launch;
+        d_acc: (local tiles * 256, 4) uint64 scratch, d_out: float4 means."""
+        check(_lib.load().srt_render_frame_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),
+                                                  ctypes.c_void_p(d_acc), ctypes.c_void_p(d_out),
+                                                  ctypes.c_void_p(stream)))
+
     def render_device(self, camera, prm, d_hits, d_accum, d_out, stream) -> None:
         check(_lib.load().srt_render_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),
                                             ctypes.c_void_p(d_hits), ctypes.c_void_p(d_accum),
                                             ctypes.c_void_p(d_out), ctypes.c_void_p(stream)))
+
+
+def resolve_frame_device(prm, d_acc: int, d_rgb: int, d_op: int, stream: int) -> None:
+    """srt_resolve_frame_device: a shard's fixed-point sums -> f64 means in the
+    row-major full-frame buffers (current device)."""
+    check(_lib.load().srt_resolve_frame_device(ctypes.byref(prm), ctypes.c_void_p(d_acc), ctypes.c_void_p(d_rgb),
+                                               ctypes.c_void_p(d_op), ctypes.c_void_p(stream)))
 
 
 def shard_tiles(width: int, height: int, shard_index: int = 0, shard_count: int = 1) -> int:

@@ -364,8 +364,8 @@ def test_mapped_host_output_equals_copy_path(passes, nslots):
     assert op_c.max() > 0
 
 
-@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
-def test_render_devices_equals_single_gpu(devices):
+@pytest.mark.parametrize("devices,spp", [([0, 0], 4), ([0, 0, 0], 4), ([0, 0], 1)])
+def test_render_devices_equals_single_gpu(devices, spp):
     """render(..., devices=[...]) shards interleaved tiles over the listed GPUs
     from one process (the same device may repeat: shards then run back to
     back); the unpacked frame equals the single-GPU render bit for bit."""
@@ -373,12 +373,12 @@ def test_render_devices_equals_single_gpu(devices):
     from paper_2504_06598_b200.synthetic import random_cloud
 
     a = random_cloud(4_000, seed=21, sh_degree=1)
-    st = RenderSettings(width=100, height=52, spp=4, multisample=2, seed=9, background=[0.2, 0.1, 0.0])
+    st = RenderSettings(width=100, height=52, spp=spp, multisample=min(2, spp), seed=9, background=[0.2, 0.1, 0.0])
     one = render(a, front_camera(), st)
     many = render(a, front_camera(), st, devices=devices)
     np.testing.assert_array_equal(many.rgb, one.rgb)
     np.testing.assert_array_equal(many.opacity, one.opacity)
-    assert many.spp == one.spp == 4
+    assert many.spp == one.spp == spp
 
 
 def test_concurrent_renders_on_one_scene():
@@ -440,3 +440,42 @@ def test_degenerate_primitives_are_skipped(oracle, method):
     ot, oid = oracle.trace_batch(ob, pk.means, cov, pk.opacities, o, d, 0.0, TMAX, 0, S2, True, 1, rng="table",
                                  table=table)
     assert np.mean(ids == oid) >= 0.999
+
+
+@pytest.mark.parametrize("passes,nslots,mode", [(16, 1, 0), (3, 4, 1)])
+def test_one_launch_frame_matches_per_pass_and_is_deterministic(passes, nslots, mode):
+    """srt_render_frame_device runs every (packet, pass) of a frame in one
+    launch with 2^-32 fixed-point integer sums: the same samples as one
+    launch per pass (float running sums) up to fp32 summation rounding, and
+    bitwise reproducible across runs whatever the warp schedule."""
+    import torch
+
+    from paper_2504_06598_b200 import front_camera
+    from paper_2504_06598_b200.scene import (DeviceScene, camera_tuple, make_camera, make_render_params,
+                                             shard_tiles)
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(8_000, seed=17, sh_degree=3)
+    sc = DeviceScene.from_packed(a.packed)
+    sc.build_bvh(np.sqrt(S2))
+    W, H = 96, 80
+    cam = make_camera(camera_tuple(front_camera(), W, H))
+    prm = make_render_params(W, H, passes, nslots, mode, S2, True, 5, (0.1, 0.2, 0.3))
+    t = shard_tiles(W, H)
+    s = torch.cuda.current_stream().cuda_stream
+    acc64 = torch.empty((t * 256, 4), dtype=torch.int64, device="cuda")
+    outs = []
+    for _ in range(2):
+        out = torch.zeros((W * H, 4), device="cuda")
+        sc.render_frame_device(cam, prm, acc64.data_ptr(), out.data_ptr(), s)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    hits = torch.empty(t * 256 * nslots, dtype=torch.int32, device="cuda")
+    acc = torch.empty((t * 256, 4), device="cuda")
+    ref = torch.zeros((W * H, 4), device="cuda")
+    sc.render_device(cam, prm, hits.data_ptr(), acc.data_ptr(), ref.data_ptr(), s)
+    torch.cuda.synchronize()
+    sc.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_allclose(outs[0], ref.cpu().numpy(), rtol=2e-6, atol=2e-6)
+    assert outs[0][:, 3].max() > 0

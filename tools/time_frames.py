@@ -45,10 +45,15 @@ for _ in range(3):
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 tt, ts = [], []
 fused = os.environ.get("SRT_SPLIT") != "1"
+onelaunch = os.environ.get("SRT_ONE_LAUNCH") == "1"
+acc64 = torch.empty(t * 256 * 4, dtype=torch.int64, device="cuda") if onelaunch else None
 for _ in range(reps):
     flush.fill_(1)
     ev[0].record()
-    if fused:
+    if onelaunch:
+        sc.render_frame_device(cam, prm, acc64.data_ptr(), out.data_ptr(), s)
+        ev[1].record()
+    elif fused:
         for f in range(st.passes):
             sc.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), s)
         ev[1].record()
