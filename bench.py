@@ -61,6 +61,28 @@ def _traffic_per_launch():
     return None
 
 
+def _issue_roofline(kernel_ms: float, clocks):
+    """Issue-slot roofline of the dominant kernel: the walk is bound by SM
+    instruction issue, not bytes.  achieved = warp instructions
+    per launch (ncu, profiles/ncu_summary.json) / the live kernel time; peak =
+    1 warp instruction per cycle per SM sub-partition (148 SMs x 4) at the SM
+    clock sampled during the timed region."""
+    try:
+        d = json.loads(PROFILE_SUMMARY.read_text())
+        inst = float(d["warp_inst_per_launch"])
+    except Exception:
+        return None
+    import torch
+
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+    peak = sms * 4 * mhz * 1e6 / 1e9  # G warp-instructions / s
+    achieved = inst / (kernel_ms * 1e-3) / 1e9
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "G warp-inst/s", "frac": achieved / peak,
+            "warp_inst_per_launch": inst, "ncu_issue_active_pct": d.get("issue_active_pct"),
+            "source": "warp instructions from profiles/ncu_summary.json, kernel time live"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
@@ -309,6 +331,7 @@ def run_ours(args) -> None:
                          "kernel": "k_trace_packet (fused walk + SH shade + accumulate)", "kernel_ms": trace_avg_ms,
                          "algorithmic_bytes_per_walk": BYTES_PER_WALK, "walks_per_launch": walks_per_launch,
                          "peak_source": peak_src},
+            "roofline_issue": _issue_roofline(trace_avg_ms, clocks),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * st.passes + (args.steps if world > 1 else 0),

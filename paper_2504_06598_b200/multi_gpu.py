@@ -172,6 +172,94 @@ def render_frame(p: ShardPlan, shard_render: Callable, group=None, device=None):
         p.height, p.width, 4)
 
 
+FIXED_ONE = float(1 << 32)  # 2^32: fixed-point unit of the frame sums (csrc/trace.cu CameraSource)
+
+
+def resolve_sums(sums: np.ndarray, width: int, height: int, rank: int, world: int, passes: int, nslots: int,
+                 frame: np.ndarray) -> None:
+    """CPU statement of srt_resolve_frame_device: a shard's tile-compact
+    fixed-point sums (n, 4) int64 -> f64 means written into its pixels of
+    the (H, W, 4) frame."""
+    px, py, ok = compact_pixels(width, height, rank, world)
+    s = np.asarray(sums, np.int64).reshape(-1, 4)[: px.shape[0]][ok]
+    inv = 1.0 / (float(passes) * float(nslots))
+    frame[py[ok], px[ok], :3] = s[:, :3].astype(np.uint64).astype(np.float64) * (inv / FIXED_ONE)
+    frame[py[ok], px[ok], 3] = (s[:, 3].astype(np.uint64) >> np.uint64(32)).astype(np.float64) * inv
+
+
+def render_frame_sums(p: ShardPlan, shard_sums: Callable, nslots: int, group=None):
+    """Run one sharded frame on exact fixed-point sums (every pass of the
+    rank's share in one launch, srt_render_frame_device).
+
+    ``shard_sums(plan) -> int64 tensor (n, 4)``: tile-compact 2^-32 sums of
+    the rank's tiles ("tiles", n = max shard tiles * 256) or of the whole
+    frame over its pass range ("samples", the one-shard layout).  "tiles"
+    gathers the sums to rank 0, which resolves each shard into its own pixels;
+    "samples" adds them with one integer ``reduce`` -- exact, so the order
+    NCCL sums in does not matter.  Either way the f64 frame on rank 0 is bit
+    for bit the single-GPU frame, for any world size.  Returns (H, W, 4) f64
+    on rank 0, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    local = shard_sums(p)
+    if p.world > 1:
+        if p.mode == "tiles":
+            gathered = [torch.empty_like(local) for _ in range(p.world)] if p.rank == 0 else None
+            dist.gather(local, gathered, dst=0, group=group)
+        else:
+            dist.reduce(local, dst=0, op=dist.ReduceOp.SUM, group=group)
+            gathered = [local]
+        if p.rank != 0:
+            return None
+    else:
+        gathered = [local]
+    shards = [(r, p.world, g) for r, g in enumerate(gathered)] if p.mode == "tiles" else [(0, 1, gathered[0])]
+    if local.is_cuda:
+        from .scene import make_render_params, resolve_frame_device
+
+        rgb = torch.zeros((p.height, p.width, 3), dtype=torch.float64, device=local.device)
+        op = torch.zeros((p.height, p.width), dtype=torch.float64, device=local.device)
+        for r, g_world, buf in shards:
+            prm = make_render_params(p.width, p.height, p.passes, nslots, 0, 1.0, True, 0, (0.0, 0.0, 0.0), 0, r,
+                                     g_world)
+            resolve_frame_device(prm, buf.data_ptr(), rgb.data_ptr(), op.data_ptr(),
+                                 torch.cuda.current_stream(local.device).cuda_stream)
+        return torch.cat([rgb, op[..., None]], dim=2)
+    frame = np.zeros((p.height, p.width, 4))
+    for r, g_world, buf in shards:
+        resolve_sums(buf.numpy(), p.width, p.height, r, g_world, p.passes, nslots, frame)
+    return torch.from_numpy(frame)
+
+
+def gpu_shard_sums(scene, camera_tuple, settings, device):
+    """shard_sums callback: the rank's share of every pass in one libsrt launch."""
+    import torch
+
+    from .scene import make_camera, make_render_params, shard_tiles
+
+    cam = make_camera(camera_tuple)
+    mode = 0 if settings.depth_mode == "mean" else 1
+
+    def run(p: ShardPlan):
+        dev = torch.device("cuda", device)
+        if p.mode == "tiles":
+            prm = make_render_params(p.width, p.height, p.passes, settings.multisample, mode, settings.cutoff_s ** 2,
+                                     True, settings.seed, settings.background, 0, p.rank, p.world)
+            n = max_shard_tiles(p.width, p.height, p.world) * 256
+        else:
+            prm = make_render_params(p.width, p.height, max(p.local_passes, 1), settings.multisample, mode,
+                                     settings.cutoff_s ** 2, True, settings.seed, settings.background, p.pass0)
+            n = shard_tiles(p.width, p.height) * 256
+        acc = torch.zeros((n, 4), dtype=torch.int64, device=dev)
+        if p.mode == "samples" and p.local_passes == 0:
+            return acc
+        scene.render_frame_device(cam, prm, acc.data_ptr(), 0, torch.cuda.current_stream(dev).cuda_stream)
+        return acc
+
+    return run
+
+
 def gpu_shard_renderer(scene, camera_tuple, settings, device):
     """shard_render callback tracing the rank's share with libsrt on `device`."""
     import torch
@@ -222,7 +310,11 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
     sc = prepare(asset, settings, device=device)
     ct = camera_tuple(camera, settings.width, settings.height)
     p = plan(mode, rank, world, settings.width, settings.height, settings.passes)
-    frame = render_frame(p, gpu_shard_renderer(sc, ct, settings, device), group)
+    if settings.passes > 1 or mode == "samples":
+        # exact fixed-point sums: bitwise the single-GPU render() frame
+        frame = render_frame_sums(p, gpu_shard_sums(sc, ct, settings, device), settings.multisample, group)
+    else:
+        frame = render_frame(p, gpu_shard_renderer(sc, ct, settings, device), group)
     if frame is None:
         return None
     f = frame.double().cpu().numpy()

@@ -120,3 +120,78 @@ def test_gloo_world2_gather_matches_single_render(mode):
         assert pr.exitcode == 0
     err = q.get(timeout=5)
     assert err <= 1e-6, err
+
+
+def _sums_worker(rank, world, port, mode, q):
+    """Fixed-point-sum frames over gloo: per-sample colours from the oracle,
+    2^-32 integer sums per rank, gathered ("tiles") or reduced ("samples")."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as O
+        from paper_2504_06598_b200.synthetic import front_camera, random_cloud
+
+        asset = random_cloud(800, seed=4, sh_degree=1)
+        pk = asset.packed
+        lo, hi = asset.aabb_arrays(np.sqrt(S2))
+        b = O.sah_build(lo, hi)
+        w, h, passes = 40, 24, 5
+        cam = front_camera()
+        ct = O.camera_tuple(cam.position, cam.look_at, cam.up, cam.fov_deg, w, h)
+        per_pass = []
+        for f in range(passes):
+            r = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=1, pass0=f, s2=S2,
+                         seed=3, rng="counter")
+            fx = np.rint(np.dstack([r["rgb"], np.zeros((h, w))]) * mg.FIXED_ONE).astype(np.int64)
+            fx[..., 3] = np.rint(r["opacity"]).astype(np.int64) << 32
+            per_pass.append(fx)
+
+        def compact(frame_sums, r, g):
+            px, py, ok = mg.compact_pixels(w, h, r, g)
+            buf = np.zeros((mg.max_shard_tiles(w, h, g) * 256, 4), np.int64)
+            buf[: px.shape[0]][ok] = frame_sums[py[ok], px[ok]]
+            return buf
+
+        def shard_sums(p):
+            if p.mode == "tiles":
+                return torch.from_numpy(compact(sum(per_pass), p.rank, p.world))
+            a, e = mg.pass_range(p.passes, p.rank, p.world)
+            part = sum(per_pass[a:e]) if e > a else np.zeros((h, w, 4), np.int64)
+            return torch.from_numpy(compact(part, 0, 1))
+
+        p = mg.plan(mode, rank, world, w, h, passes)
+        frame = mg.render_frame_sums(p, shard_sums, 1)
+        if rank == 0:
+            single = np.zeros((h, w, 4))
+            mg.resolve_sums(compact(sum(per_pass), 0, 1), w, h, 0, 1, passes, 1, single)
+            ref = O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 1, ct, w, h, passes=passes, s2=S2, seed=3,
+                           rng="counter")
+            want = np.dstack([ref["rgb"], ref["opacity"]])
+            q.put((bool(np.array_equal(frame.numpy(), single)), float(np.abs(frame.numpy() - want).max())))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["tiles", "samples"])
+def test_gloo_world2_fixed_point_sums_are_bitwise_single_frame(mode):
+    """render_frame_sums (the GPU driver's multi-pass path): integer sums make
+    the world-2 frame bit for bit the one-rank frame, in both shardings."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sums_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+        assert pr.exitcode == 0
+    same, err = q.get(timeout=5)
+    assert same
+    assert err <= 1e-9, err
