@@ -352,8 +352,23 @@ def unpack_tiles_device(d_gathered: int, width: int, height: int, shard_count: i
                                               ctypes.c_void_p(stream)))
 
 
+_CAMERA_CACHE: dict = {}
+
+
 def camera_tuple(camera, width: int, height: int) -> tuple:
-    """The 14 camera scalars of render.py:140-150 from a CameraConfig."""
+    """The 14 camera scalars of render.py:140-150 from a CameraConfig
+    (memoised on the camera's values: the numpy basis costs ~90 us a frame)."""
+    key = (*map(float, camera.position), *map(float, camera.look_at), *map(float, camera.up), float(camera.fov_deg),
+           int(width), int(height))
+    hit = _CAMERA_CACHE.get(key)
+    if hit is None:
+        if len(_CAMERA_CACHE) > 1024:
+            _CAMERA_CACHE.clear()
+        hit = _CAMERA_CACHE[key] = _camera_tuple(camera, width, height)
+    return hit
+
+
+def _camera_tuple(camera, width: int, height: int) -> tuple:
     fwd = camera.look_at - camera.position
     fwd = fwd / np.linalg.norm(fwd)
     right = np.cross(fwd, camera.up)
