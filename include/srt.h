@@ -184,8 +184,8 @@ srt_status srt_render_exact(const SrtScene *scene, const SrtCamera *camera,
  * SRT_RNG_TRIG64); the kk nearest accepted candidates, sorted by (t, prim id),
  * are composited front to back with their own alphas over `background`
  * (kernels.py:479-518, 561-580).  kk >= 1; params->nslots/clip are ignored.
- * out_rgb (R,3) f64.  More than 256 accepted with kk > 256 ->
- * SRT_ERR_STACK_OVERFLOW. */
+ * out_rgb (R,3) f64.  Any kk and any number of accepted candidates (peeled
+ * 128 at a time). */
 srt_status srt_biased_rays(const SrtScene *scene, const SrtTraceParams *params, const double *origins,
                            const double *dirs, int64_t num_rays, int32_t kk, const double *background,
                            double *out_rgb);

@@ -94,7 +94,7 @@ srt_status check_flag(const SrtScene *s, cudaStream_t st) {
     if (rc) return rc;
     if (flag) {
         cudaMemsetAsync(s->d_flag, 0, sizeof(int), st);
-        set_error("traversal stack overflow (BVH deeper than the 128-entry stack, or more than 512 exact candidates)");
+        set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
         return SRT_ERR_STACK_OVERFLOW;
     }
     return SRT_OK;

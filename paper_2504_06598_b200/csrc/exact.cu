@@ -7,14 +7,16 @@
 // inside its conservative box), sorts them by (t, prim id) -- the stable
 // order of np.argsort(kind="mergesort") over ids appended in increasing order
 // -- and composites front to back in fp64: L = sum T_i a_i c_i + T bg.
+// Candidates are taken kExactChunk at a time in (t, id) order (NearestK), one
+// unclipped walk per chunk, so rays through thousands of candidates need no
+// per-ray buffer beyond the chunk.
 #include <cfloat>
+#include <climits>
 
 #include "srt_internal.h"
 #include "srt_trig64.cuh"
 
 namespace srt {
-
-constexpr int kExactCap = 512;  // candidates per ray (overflow -> SRT_ERR_STACK_OVERFLOW)
 
 // Every leaf primitive whose conservative box the ray crosses inside
 // [t_min, t_max0], in no particular order: visit(slot, gm, ga, gb).
@@ -58,48 +60,98 @@ __device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState
     }
 }
 
+// The K nearest (t, prim id) keys offered during one walk, as a bounded
+// max-heap (root = farthest kept); sort() leaves them ascending.  Exact and
+// biased compositing peel a ray's candidates K at a time with it: each walk
+// keeps the K nearest above the last one composited, so any number of
+// candidates is handled exactly in ceil(m / K) walks with O(K) state.
+template <class T, class A, int K>
+struct NearestK {
+    T t[K];
+    A a[K];
+    int id[K];
+    int n;
+    __device__ static bool less(T t1, int i1, T t2, int i2) { return t1 < t2 || (t1 == t2 && i1 < i2); }
+    __device__ void sift_down(int j, T tt, int ii, A aa, int size) {
+        while (true) {
+            int c = 2 * j + 1;
+            if (c >= size) break;
+            if (c + 1 < size && less(t[c], id[c], t[c + 1], id[c + 1])) ++c;
+            if (!less(tt, ii, t[c], id[c])) break;
+            t[j] = t[c];
+            id[j] = id[c];
+            a[j] = a[c];
+            j = c;
+        }
+        t[j] = tt;
+        id[j] = ii;
+        a[j] = aa;
+    }
+    __device__ void offer(T tt, int ii, A aa) {
+        if (n < K) {
+            int j = n++;
+            while (j > 0) {
+                int p = (j - 1) >> 1;
+                if (!less(t[p], id[p], tt, ii)) break;
+                t[j] = t[p];
+                id[j] = id[p];
+                a[j] = a[p];
+                j = p;
+            }
+            t[j] = tt;
+            id[j] = ii;
+            a[j] = aa;
+        } else if (less(tt, ii, t[0], id[0])) {
+            sift_down(0, tt, ii, aa, n);
+        }
+    }
+    __device__ void sort() {
+        for (int end = n - 1; end > 0; --end) {
+            T tt = t[end];
+            int ii = id[end];
+            A aa = a[end];
+            t[end] = t[0];
+            id[end] = id[0];
+            a[end] = a[0];
+            sift_down(0, tt, ii, aa, end);
+        }
+    }
+};
+
+constexpr int kExactChunk = 256;  // candidates composited per walk (exact mode)
+
 template <int MODE>
 __device__ void exact_ray(const SceneView &s, const RayState &r, float s2, const float *bg, double out[4],
                           int *overflow) {
-    float ct[kExactCap];
-    float ca[kExactCap];
-    int cid[kExactCap];
-    int m = 0;
-    for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
-        Cand c = candidate<MODE>(r, gm, ga, gb, s2);
-        if (!c.valid) return;
-        if (m >= kExactCap) {
-            atomicExch(overflow, 1);
-            return;
-        }
-        ct[m] = c.t;
-        ca[m] = c.alpha;
-        cid[m] = __float_as_int(gb.z);
-        ++m;
-    });
-    // insertion sort by (t, prim id)
-    for (int i = 1; i < m; ++i) {
-        float t = ct[i], a = ca[i];
-        int id = cid[i];
-        int j = i - 1;
-        while (j >= 0 && (ct[j] > t || (ct[j] == t && cid[j] > id))) {
-            ct[j + 1] = ct[j];
-            ca[j + 1] = ca[j];
-            cid[j + 1] = cid[j];
-            --j;
-        }
-        ct[j + 1] = t;
-        ca[j + 1] = a;
-        cid[j + 1] = id;
-    }
+    NearestK<float, float, kExactChunk> h;
+    float lo_t = -INFINITY;  // exclusive lower bound (lo_t, lo_id) of the next chunk
+    int lo_id = INT_MIN;
     double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
-    for (int i = 0; i < m; ++i) {
-        float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, cid[i], r.fdx, r.fdy, r.fdz);
-        double w = trans * (double)ca[i];
-        rr += w * col.x;
-        gg += w * col.y;
-        bb += w * col.z;
-        trans *= 1.0 - (double)ca[i];
+    while (true) {
+        h.n = 0;
+        for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+            Cand c = candidate<MODE>(r, gm, ga, gb, s2);
+            if (!c.valid) return;
+            const int id = __float_as_int(gb.z);
+            if (!decltype(h)::less(lo_t, lo_id, c.t, id)) return;  // composited by an earlier chunk
+            h.offer(c.t, id, c.alpha);
+        });
+        const int m = h.n;
+        h.sort();
+        // front to back in (t, prim id) order -- the stable mergesort order of
+        // kernels.py:463 over ids appended in increasing order
+        for (int i = 0; i < m; ++i) {
+            SRT_DCHECK(h.id[i] >= 0 && h.id[i] < s.n);
+            float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, h.id[i], r.fdx, r.fdy, r.fdz);
+            double w = trans * (double)h.a[i];
+            rr += w * col.x;
+            gg += w * col.y;
+            bb += w * col.z;
+            trans *= 1.0 - (double)h.a[i];
+        }
+        if (m < kExactChunk || trans == 0.0) break;  // all consumed, or nothing further can contribute
+        lo_t = h.t[m - 1];
+        lo_id = h.id[m - 1];
     }
     out[0] = rr + trans * bg[0];
     out[1] = gg + trans * bg[1];
@@ -154,13 +206,14 @@ __global__ void __launch_bounds__(128) k_exact_frame(SceneView s, CamD cam, Rend
 // Biased k-nearest composite (kernels.py:479-518, 561-580; tracer.py:305-343):
 // every valid candidate in (t_min, t_max) is accepted with ONE draw (slot 0 of
 // the ray's stream), and only the kk nearest accepted are composited with
-// their original alphas, background behind.  The kk nearest are kept as a
-// sorted list while walking, so memory is O(min(kk, cap)), not O(accepted).
+// their original alphas, background behind.  Accepted candidates are peeled
+// kBiasedChunk at a time (NearestK), so any kk and any number of accepted
+// candidates are handled with O(kBiasedChunk) state.
 //   RNG counter: u = counter_u(walk_key(frame_key(seed), ray_id0+i, sample0), pid)
 //   RNG table:   u = table[pid * table_slots + 0]
 //   RNG trig64:  u = the reference's trig hash of the fp64 hit (kernels.py:55-60)
 // ---------------------------------------------------------------------------
-constexpr int kBiasedCap = 256;
+constexpr int kBiasedChunk = 128;  // accepted candidates composited per walk (biased mode)
 
 struct BiasedArgs {
     double t_min, t_max, s2;
@@ -177,70 +230,56 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
     RayState r;
     init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], a.t_min, a.t_max);
     const t64::Ray64 r64{q[0], q[1], q[2], q[3], q[4], q[5], a.t_min, a.t_max};
-    const int keep = a.kk < 1 ? 1 : (a.kk < kBiasedCap ? a.kk : kBiasedCap);
-    double bt[kBiasedCap], ba[kBiasedCap];
-    int bid[kBiasedCap];
-    bt[0] = INFINITY;  // (keep >= 1; silences a maybe-uninitialised diagnostic)
-    ba[0] = 0.0;
-    bid[0] = 0;
-    int m = 0;            // kept (<= keep), sorted by (t, pid)
-    bool dropped = false; // an accepted candidate fell off the kept list
+    const int kk = a.kk < 1 ? 1 : a.kk;
     const float s2f = (float)a.s2;
-    for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
-        const int pid = __float_as_int(gb.z);
-        double t, alpha;
-        bool acc;
-        if (RNG == SRT_RNG_TRIG64) {
-            double resid, hx, hy, hz;
-            if (!t64::candidate<MODE>(r64, s.means64 + (int64_t)pid * 3, s.cov64 + (int64_t)pid * 6, a.s2, t, resid,
-                                      hx, hy, hz))
-                return;
-            if (t <= a.t_min || t >= a.t_max) return;
-            alpha = t64::mul(s.opac64[pid], exp(t64::mul(-0.5, resid)));
-            acc = t64::hash_position(hx, hy, hz, 0) < alpha;
-        } else {
-            Cand c = candidate<MODE>(r, gm, ga, gb, s2f);
-            if (!c.valid) return;
-            t = c.t;
-            alpha = c.alpha;
-            if (RNG == SRT_RNG_TABLE)
-                acc = __ldg(a.table + (int64_t)pid * a.tstride) < alpha;
-            else
-                acc = counter_u(key, (uint32_t)pid) < c.alpha;
-        }
-        if (!acc) return;
-        // insert into the sorted kept list, dropping the farthest when full
-        int j = m;
-        if (m == keep) {
-            if (!(t < bt[m - 1] || (t == bt[m - 1] && pid < bid[m - 1]))) {
-                dropped = true;
-                return;
-            }
-            dropped = true;
-            --j;
-        } else {
-            ++m;
-        }
-        while (j > 0 && (bt[j - 1] > t || (bt[j - 1] == t && bid[j - 1] > pid))) {
-            bt[j] = bt[j - 1];
-            ba[j] = ba[j - 1];
-            bid[j] = bid[j - 1];
-            --j;
-        }
-        bt[j] = t;
-        ba[j] = alpha;
-        bid[j] = pid;
-    });
-    if (dropped && keep < a.kk) atomicExch(overflow, 1);  // kk > cap and more accepted than the cap
+    NearestK<double, double, kBiasedChunk> h;
+    double lo_t = -INFINITY;  // exclusive lower bound (lo_t, lo_id) of the next chunk
+    int lo_id = INT_MIN;
+    int done = 0;
     double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
-    for (int k = 0; k < m; ++k) {
-        SRT_DCHECK(bid[k] >= 0 && bid[k] < s.n);
-        float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, bid[k], r.fdx, r.fdy, r.fdz);
-        double w = trans * ba[k];
-        rr += w * col.x;
-        gg += w * col.y;
-        bb += w * col.z;
-        trans *= 1.0 - ba[k];
+    while (done < kk) {
+        h.n = 0;
+        for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+            const int pid = __float_as_int(gb.z);
+            double t, alpha;
+            bool acc;
+            if (RNG == SRT_RNG_TRIG64) {
+                double resid, hx, hy, hz;
+                if (!t64::candidate<MODE>(r64, s.means64 + (int64_t)pid * 3, s.cov64 + (int64_t)pid * 6, a.s2, t,
+                                          resid, hx, hy, hz))
+                    return;
+                if (t <= a.t_min || t >= a.t_max) return;
+                alpha = t64::mul(s.opac64[pid], exp(t64::mul(-0.5, resid)));
+                acc = t64::hash_position(hx, hy, hz, 0) < alpha;
+            } else {
+                Cand c = candidate<MODE>(r, gm, ga, gb, s2f);
+                if (!c.valid) return;
+                t = c.t;
+                alpha = c.alpha;
+                if (RNG == SRT_RNG_TABLE)
+                    acc = __ldg(a.table + (int64_t)pid * a.tstride) < alpha;
+                else
+                    acc = counter_u(key, (uint32_t)pid) < c.alpha;
+            }
+            if (!acc || !decltype(h)::less(lo_t, lo_id, t, pid)) return;
+            h.offer(t, pid, alpha);
+        });
+        const int m = h.n;
+        h.sort();
+        const int take = m < kk - done ? m : kk - done;
+        for (int k = 0; k < take; ++k) {
+            SRT_DCHECK(h.id[k] >= 0 && h.id[k] < s.n);
+            float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, h.id[k], r.fdx, r.fdy, r.fdz);
+            double w = trans * h.a[k];
+            rr += w * col.x;
+            gg += w * col.y;
+            bb += w * col.z;
+            trans *= 1.0 - h.a[k];
+        }
+        done += take;
+        if (m < kBiasedChunk || trans == 0.0) break;
+        lo_t = h.t[m - 1];
+        lo_id = h.id[m - 1];
     }
     out[0] = rr + trans * a.bg.x;
     out[1] = gg + trans * a.bg.y;

@@ -150,3 +150,36 @@ def test_biased_frame_counter_matches_explicit_rays():
     per_ray = sc.biased_rays(o, d, 2, s2=st.cutoff_s ** 2, seed=3, ray_id0=0, sample0=0)
     ok = np.all(np.abs(frame.reshape(-1, 3) - per_ray) <= 1e-6, axis=1)
     assert ok.mean() >= 0.99
+
+
+def test_exact_and_biased_peel_many_candidates(oracle):
+    """A ray through 700 layers (more than any chunk): exact compositing peels
+    the candidates 256 at a time and matches the closed form and the oracle;
+    the biased composite with every candidate accepted and k = 600 (several
+    128-chunks) equals the exact composite truncated after 600 layers."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import pancake_stack
+
+    n = 700
+    rs = np.random.default_rng(3)
+    alphas = rs.uniform(0.001, 0.01, n)
+    colors = rs.uniform(0.0, 1.0, (n, 3))
+    a = pancake_stack(alphas, colors, z0=1.0, spacing=0.05, thickness=0.004)
+    pk = a.packed
+    o = np.array([[0.01, -0.02, 0.0], [0.3, 0.1, 0.0]])
+    d = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 1.0]])
+    sc = DeviceScene.from_packed(pk)
+    sc.build_bvh(np.sqrt(S2))
+    rgb, op = sc.exact_rays(o, d, s2=S2, background=(0.2, 0.3, 0.4))
+    want_rgb, want_op = oracle.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, o, d, s2=S2,
+                                           background=(0.2, 0.3, 0.4))
+    np.testing.assert_allclose(rgb, want_rgb, rtol=2e-5, atol=2e-6)
+    np.testing.assert_allclose(op, want_op, rtol=2e-5, atol=2e-6)
+    trans = np.cumprod(np.concatenate([[1.0], 1.0 - alphas]))
+    closed = (trans[:n, None] * alphas[:, None] * colors).sum(axis=0) + trans[n] * np.array([0.2, 0.3, 0.4])
+    np.testing.assert_allclose(rgb[0], closed, rtol=1e-4)
+    got = sc.biased_rays(o, d, 600, s2=S2, background=(0.2, 0.3, 0.4), rng="table", table=np.zeros(n))
+    sc.close()
+    k = 600
+    trunc = (trans[:k, None] * alphas[:k, None] * colors[:k]).sum(axis=0) + trans[k] * np.array([0.2, 0.3, 0.4])
+    np.testing.assert_allclose(got[0], trunc, rtol=1e-4)
