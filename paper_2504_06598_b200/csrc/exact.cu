@@ -21,7 +21,8 @@ namespace srt {
 // Every leaf primitive whose conservative box the ray crosses inside
 // [t_min, t_max0], in no particular order: visit(slot, gm, ga, gb).
 template <class Visit>
-__device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState &r, int *overflow, Visit &&visit) {
+__device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState &r, int *overflow, Visit &&visit,
+                                              const float *far = nullptr, float lo = -INFINITY) {
     if (s.num_nodes4 == 0) return;
     int stk[kStackSize];
     int sp = 0, node = 0;
@@ -42,8 +43,11 @@ __device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState
             float ya = fmaf(ly[k], r.idy, -r.oidy), yb = fmaf(hy[k], r.idy, -r.oidy);
             float za = fmaf(lz[k], r.idz, -r.oidz), zb = fmaf(hz[k], r.idz, -r.oidz);
             float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
-            float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), r.t_max0));
-            if (!(tn <= tf)) continue;
+            // optional window [lo, *far] (chunked peeling): a candidate's depth
+            // lies in its box's slab interval, so boxes entirely before lo or
+            // after *far hold nothing the caller still wants
+            float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far ? *far : r.t_max0));
+            if (!(tn <= tf) || tf < lo) continue;
             if (kid[k] >= 0) {
                 if (sp >= kStackSize) {
                     atomicExch(overflow, 1);
@@ -71,6 +75,7 @@ struct NearestK {
     A a[K];
     int id[K];
     int n;
+    int cap = K;  // kept entries (<= K)
     __device__ static bool less(T t1, int i1, T t2, int i2) { return t1 < t2 || (t1 == t2 && i1 < i2); }
     __device__ void sift_down(int j, T tt, int ii, A aa, int size) {
         while (true) {
@@ -88,7 +93,7 @@ struct NearestK {
         a[j] = aa;
     }
     __device__ void offer(T tt, int ii, A aa) {
-        if (n < K) {
+        if (n < cap) {
             int j = n++;
             while (j > 0) {
                 int p = (j - 1) >> 1;
@@ -118,6 +123,15 @@ struct NearestK {
     }
 };
 
+// Window bounds for for_each_leaf, widened so fp32 rounding of a candidate's
+// depth against its box's slab interval can never prune it.
+__device__ __forceinline__ float window_hi(double t) {
+    return t >= 3.0e38 ? INFINITY : __double2float_ru(t + 1e-5 * (fabs(t) + 1.0));
+}
+__device__ __forceinline__ float window_lo(double t) {
+    return t <= -3.0e38 ? -INFINITY : __double2float_rd(t - 1e-5 * (fabs(t) + 1.0));
+}
+
 constexpr int kExactChunk = 256;  // candidates composited per walk (exact mode)
 
 template <int MODE>
@@ -129,13 +143,18 @@ __device__ void exact_ray(const SceneView &s, const RayState &r, float s2, const
     double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
     while (true) {
         h.n = 0;
-        for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
-            Cand c = candidate<MODE>(r, gm, ga, gb, s2);
-            if (!c.valid) return;
-            const int id = __float_as_int(gb.z);
-            if (!decltype(h)::less(lo_t, lo_id, c.t, id)) return;  // composited by an earlier chunk
-            h.offer(c.t, id, c.alpha);
-        });
+        float far = INFINITY;  // the chunk's farthest kept depth once it is full
+        for_each_leaf(
+            s, r, overflow,
+            [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+                Cand c = candidate<MODE>(r, gm, ga, gb, s2);
+                if (!c.valid) return;
+                const int id = __float_as_int(gb.z);
+                if (!decltype(h)::less(lo_t, lo_id, c.t, id)) return;  // composited by an earlier chunk
+                h.offer(c.t, id, c.alpha);
+                if (h.n == h.cap) far = window_hi(h.t[0]);
+            },
+            &far, window_lo(lo_t));
         const int m = h.n;
         h.sort();
         // front to back in (t, prim id) order -- the stable mergesort order of
@@ -239,6 +258,8 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
     double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
     while (done < kk) {
         h.n = 0;
+        h.cap = kk - done < kBiasedChunk ? kk - done : kBiasedChunk;
+        float far = INFINITY;
         for_each_leaf(s, r, overflow, [&](const float4 &gm, const float4 &ga, const float4 &gb) {
             const int pid = __float_as_int(gb.z);
             double t, alpha;
@@ -263,10 +284,11 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
             }
             if (!acc || !decltype(h)::less(lo_t, lo_id, t, pid)) return;
             h.offer(t, pid, alpha);
-        });
+            if (h.n == h.cap) far = window_hi(h.t[0]);
+        }, &far, window_lo(lo_t));
         const int m = h.n;
         h.sort();
-        const int take = m < kk - done ? m : kk - done;
+        const int take = m;  // cap <= kk - done
         for (int k = 0; k < take; ++k) {
             SRT_DCHECK(h.id[k] >= 0 && h.id[k] < s.n);
             float3 col = sh_color(s.sh, s.sh_k, s.sh_deg, h.id[k], r.fdx, r.fdy, r.fdz);
@@ -277,7 +299,7 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
             trans *= 1.0 - h.a[k];
         }
         done += take;
-        if (m < kBiasedChunk || trans == 0.0) break;
+        if (m < h.cap || trans == 0.0) break;
         lo_t = h.t[m - 1];
         lo_id = h.id[m - 1];
     }
