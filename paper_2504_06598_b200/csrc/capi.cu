@@ -185,6 +185,15 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
         return SRT_ERR_CUDA;
     }
     DeviceGuard g(device);
+    {
+        // stream-ordered scratch (ray sorting) stays pooled between calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     SrtScene *s = new SrtScene();
     s->device = device;
     s->n = desc->n;

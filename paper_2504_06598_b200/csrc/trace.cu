@@ -14,9 +14,14 @@
 // switches to candidate evaluation once every lane holds a postponed leaf.
 // That keeps the expensive candidate code (kernels.py:139-189 + the
 // acceptance draw) executing with most lanes converged.
+#include <algorithm>
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "srt_internal.h"
 
@@ -378,6 +383,7 @@ struct CameraSource {
 struct ArraySource {
     static constexpr bool kCoherent = false;
     const double *rays;  // (R, 6)
+    const uint32_t *perm;  // optional processing order (sorted rays); results keyed by the original index
     uint32_t R;
     double t_min, t_max;
     int nslots;
@@ -387,6 +393,7 @@ struct ArraySource {
     __host__ __device__ __forceinline__ uint32_t total() const { return R; }
     template <int NS>
     __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
+        if (perm) idx = __ldg(perm + idx);
         const double *q = rays + (int64_t)idx * 6;
         init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
         init_slots<NS>(sl, nslots);
@@ -396,6 +403,7 @@ struct ArraySource {
     }
     template <int NS>
     __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
+        if (perm) idx = __ldg(perm + idx);
 #pragma unroll
         for (int k = 0; k < NS; ++k)
             if (k < nslots) {
@@ -1172,7 +1180,29 @@ srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const Re
 
 // All `npass` passes (pass0 ...) of a frame in ONE packet launch, summed into
 // the zeroed fixed-point accumulator d_acc64 (unit * 4 u64); see CameraSource.
+// Frames with more than 2^32 (pixel, pass) work items are split into pass
+// chunks; integer sums do not care which launch added what.
+static srt_status launch_multipass_chunk(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass0,
+                                         int npass, unsigned long long *d_acc64, cudaStream_t st);
+
 srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass0,
+                                         int npass, unsigned long long *d_acc64, cudaStream_t st) {
+    const uint64_t unit = (uint64_t)(a.local_tiles * 256);
+    if (unit == 0 || npass <= 0) return SRT_OK;
+    uint64_t limit = 0xFFFFFFFFull;  // work items per launch (32-bit work counter)
+    if (const char *e = getenv("SRT_MULTIPASS_MAX_ITEMS")) limit = std::min<uint64_t>(limit, strtoull(e, nullptr, 10));
+    const int per = (int)std::min<uint64_t>((uint64_t)npass, limit / unit);
+    if (per < 1) {
+        set_error("frame too large for one work counter");
+        return SRT_ERR_INVALID_ARG;
+    }
+    srt_status rc = SRT_OK;
+    for (int f = 0; f < npass && !rc; f += per)
+        rc = launch_multipass_chunk(s, cam, a, pass0 + f, std::min(per, npass - f), d_acc64, st);
+    return rc;
+}
+
+static srt_status launch_multipass_chunk(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass0,
                                          int npass, unsigned long long *d_acc64, cudaStream_t st) {
     CameraSource src;
     src.accum = nullptr;
@@ -1188,10 +1218,6 @@ srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, con
     src.acc64 = d_acc64;
     src.unit = (uint32_t)(a.local_tiles * 256);
     src.npass = (uint32_t)npass;
-    if ((uint64_t)src.unit * (uint64_t)npass > 0xFFFFFFFFull) {
-        set_error("too many (pixel, pass) work items in one launch");
-        return SRT_ERR_INVALID_ARG;
-    }
     uint32_t x = a.seed ^ 0x9E3779B9u;
     x ^= x >> 16;
     x *= 0x7feb352du;
@@ -1201,6 +1227,114 @@ srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, con
     src.fkey = x;
     WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
     return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
+}
+
+// ---------------------------------------------------------------------------
+// Ray reordering for large batches of explicit (possibly incoherent) rays:
+// 30-bit keys = 8-bit-per-axis Morton code of the origin inside the batch's
+// origin bounds, then 2 bits per direction component; a stable radix sort of
+// (key, index) gives the processing order.  Neighbouring lanes then walk
+// neighbouring, similarly directed rays.  Results and random draws stay keyed
+// by the original index, so the output does not depend on the order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread8(uint32_t v) {  // 8 bits -> every third bit
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ int ordered(float f) {
+    int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float unordered(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+__global__ void k_ray_bounds(const double *__restrict__ rays, uint32_t R, int *bounds) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {INT_MIN, INT_MIN, INT_MIN};
+    if (i < R)
+        for (int a = 0; a < 3; ++a) lo[a] = hi[a] = ordered((float)rays[(int64_t)i * 6 + a]);
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+        if ((threadIdx.x & 31) == 0 && lo[a] <= hi[a]) {
+            atomicMin(bounds + a, lo[a]);
+            atomicMax(bounds + 3 + a, hi[a]);
+        }
+    }
+}
+
+__global__ void k_ray_keys(const double *__restrict__ rays, uint32_t R, const int *__restrict__ bounds,
+                           uint32_t *keys, uint32_t *idx) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R) return;
+    const double *q = rays + (int64_t)i * 6;
+    uint32_t m = 0, dkey = 0;
+    for (int a = 0; a < 3; ++a) {
+        float lo = unordered(bounds[a]), hi = unordered(bounds[3 + a]);
+        float u = hi > lo ? ((float)q[a] - lo) / (hi - lo) : 0.0f;
+        uint32_t c = (uint32_t)fminf(fmaxf(u * 256.0f, 0.0f), 255.0f);
+        m |= spread8(c) << a;
+        float d = (float)q[3 + a];
+        uint32_t db = d < -0.5f ? 0u : (d < 0.0f ? 1u : (d < 0.5f ? 2u : 3u));
+        dkey = (dkey << 2) | db;
+    }
+    keys[i] = (m << 6) | dkey;
+    idx[i] = i;
+}
+
+static srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out,
+                            cudaStream_t st) {
+    *d_perm_out = nullptr;
+    *d_mem_out = nullptr;
+    {
+        // 64 evenly spaced rays: one shared origin means a camera-like batch,
+        // already coherent in its given order -- walk it as it is
+        double probe[64][6];
+        const size_t step = (size_t)(R / 64) * 6 * sizeof(double);
+        srt_status rc0 = cuda_status(cudaMemcpy2DAsync(probe, sizeof(probe[0]), d_rays, step, sizeof(probe[0]), 64,
+                                                       cudaMemcpyDeviceToHost, st), "ray probe");
+        if (!rc0) rc0 = cuda_status(cudaStreamSynchronize(st), "ray probe");
+        if (rc0) return rc0;
+        bool one_origin = true;
+        for (int j = 1; j < 64 && one_origin; ++j)
+            one_origin = probe[j][0] == probe[0][0] && probe[j][1] == probe[0][1] && probe[j][2] == probe[0][2];
+        if (one_origin) return SRT_OK;
+    }
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)R, 0, 30, st);
+    size_t arr = ((sizeof(uint32_t) * (size_t)R + 255) / 256) * 256;
+    size_t total = 4 * arr + 256 + temp;
+    char *mem = nullptr;
+    srt_status rc = cuda_status(cudaMallocAsync((void **)&mem, total, st), "ray sort scratch");
+    if (rc) return rc;
+    uint32_t *k0 = (uint32_t *)mem, *k1 = (uint32_t *)(mem + arr), *v0 = (uint32_t *)(mem + 2 * arr),
+             *v1 = (uint32_t *)(mem + 3 * arr);
+    int *bounds = (int *)(mem + 4 * arr);
+    void *tmp = mem + 4 * arr + 256;
+    const int init[6] = {INT_MAX, INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MIN};
+    rc = cuda_status(cudaMemcpyAsync(bounds, init, sizeof(init), cudaMemcpyHostToDevice, st), "ray bounds init");
+    unsigned blocks = (R + 255) / 256;
+    if (!rc) {
+        k_ray_bounds<<<blocks, 256, 0, st>>>(d_rays, R, bounds);
+        rc = cuda_status(cudaGetLastError(), "ray bounds");
+    }
+    if (!rc) {
+        k_ray_keys<<<blocks, 256, 0, st>>>(d_rays, R, bounds, k0, v0);
+        rc = cuda_status(cudaGetLastError(), "ray keys");
+    }
+    if (!rc)
+        rc = cuda_status(cub::DeviceRadixSort::SortPairs(tmp, temp, k0, k1, v0, v1, (int)R, 0, 30, st), "ray sort");
+    if (rc) {
+        cudaFreeAsync(mem, st);
+        return rc;
+    }
+    *d_perm_out = v1;
+    *d_mem_out = mem;
+    return SRT_OK;
 }
 
 srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int nslots,
@@ -1226,9 +1360,22 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     src.sample0 = p->sample0;
     src.out_t = d_t;
     src.out_id = d_id;
+    src.perm = nullptr;
+    // large batches are walked in sorted order (SRT_RAY_SORT=0 disables)
+    // (single-slot walks: the cooperative multi-slot kernel measured no gain)
+    static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
+    void *sort_mem = nullptr;
+    if (R >= sort_min && nslots == 1) {
+        uint32_t *perm = nullptr;
+        srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
+        if (rc) return rc;
+        src.perm = perm;
+    }
     WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
-    if (p->rng == SRT_RNG_TABLE) return dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st);
-    return dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
+    srt_status rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st)
+                                            : dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
+    if (sort_mem) cudaFreeAsync(sort_mem, st);
+    return rc;
 }
 
 // ---------------------------------------------------------------------------

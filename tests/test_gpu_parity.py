@@ -480,3 +480,47 @@ def test_one_launch_frame_matches_per_pass_and_is_deterministic(passes, nslots, 
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_allclose(outs[0], ref.cpu().numpy(), rtol=2e-6, atol=2e-6)
     assert outs[0][:, 3].max() > 0
+
+
+def test_one_launch_frame_splits_into_pass_chunks(monkeypatch):
+    """Frames with more (pixel, pass) work items than one 32-bit work counter
+    covers run as several launches into the same integer sums: forcing a
+    tiny per-launch limit gives the identical frame."""
+    from paper_2504_06598_b200 import front_camera
+    from paper_2504_06598_b200.scene import DeviceScene, camera_tuple
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(3_000, seed=2, sh_degree=1)
+    sc = DeviceScene.from_packed(a.packed)
+    sc.build_bvh(np.sqrt(S2))
+    W, H = 48, 32
+    cam = camera_tuple(front_camera(), W, H)
+    want = sc.render(cam, W, H, 7, 2, 0, S2, True, 1, (0.0, 0.1, 0.2))
+    monkeypatch.setenv("SRT_MULTIPASS_MAX_ITEMS", str(W * H * 3))  # -> 3 passes per launch
+    got = sc.render(cam, W, H, 7, 2, 0, S2, True, 1, (0.0, 0.1, 0.2))
+    sc.close()
+    np.testing.assert_array_equal(got[0], want[0])
+    np.testing.assert_array_equal(got[1], want[1])
+
+
+def test_large_incoherent_batch_walked_in_sorted_order(oracle):
+    """Batches of >= 65536 single-slot rays with distinct origins are walked
+    in Morton/direction-sorted order; draws and outputs stay keyed by the
+    original ray index, so ids equal the oracle's for the same stream."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(5_000, seed=13, sh_degree=0)
+    pk = a.packed
+    o, d = random_rays(np.random.default_rng(8), 70_000)
+    sc = DeviceScene.from_packed(pk)
+    sc.build_bvh(CUTOFF)
+    t, ids = sc.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 1, seed=21, ray_id0=5)
+    sc.close()
+    lo, hi = a.aabb_arrays(CUTOFF)
+    ob = oracle.sah_build(lo, hi)
+    ot, oid = oracle.trace_batch(ob, pk.means, pk.cov_inv6, pk.opacities, o, d, 0.0, TMAX, 0, S2, True, 1,
+                                 rng="counter", seed=21, ray_id0=5)
+    assert np.mean(ids == oid) >= 0.999
+    same = (ids == oid) & (oid >= 0)
+    np.testing.assert_allclose(t[same], ot[same], rtol=2e-5, atol=1e-5)
