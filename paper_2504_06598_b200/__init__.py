@@ -2,10 +2,12 @@
 
 Drop-in for the hot path of the reference package ``splatray``
 (arXiv 2504.06598): ``render(asset, camera, settings)`` and the kernel-level
-``kernels.render_stochastic`` / ``kernels.trace_batch`` run on hand-written
-sm_100a CUDA (``csrc/``, C ABI in ``include/srt.h``) with a GPU LBVH, a
-stochastic N-slot traversal driven by a counter RNG, and a fused SH-shade +
-accumulate pass.  There is no CPU fallback.
+entry points of ``kernels`` run on hand-written sm_100a CUDA (``csrc/``, C
+ABI in ``include/srt.h``): a GPU PLOC/LBVH build, a warp-packet stochastic
+N-slot traversal driven by a counter RNG with SH shading fused into the
+walk, exact and biased compositing, the reference's trig-hash stream in
+fp64 (``rng="trig64"``), PLY ingest and multi-GPU frame drivers.  There is
+no CPU fallback.
 """
 
 from .assets import EmptyAssetError, PackedScene, SplatAsset

@@ -1,9 +1,10 @@
 """Operator-boundary shim: the reference's compiled-kernel entry points, on the GPU.
 
-``render_stochastic``, ``trace_batch`` and ``transmittance_batch`` take the
-SAME positional arguments as /root/reference/pkg/src/splatray/kernels.py
-(lines 622-628, 527-532 and 544-549): flat float64/int64 numpy arrays in,
-outputs written in place, None returned.  Pointing the reference's callers
+``render_stochastic``, ``trace_batch``, ``transmittance_batch``,
+``exact_batch``, ``render_exact`` and ``biased_batch`` take the SAME
+positional arguments as /root/reference/pkg/src/splatray/kernels.py (lines
+622-628, 527-532, 544-549, 584-588, 677-681, 561-565): flat float64/int64
+numpy arrays in, outputs written in place, None returned.  Pointing the reference's callers
 (``render.py:166-173``, ``validate.py:106,177``, its acceptance tests) at
 this module swaps its numba CPU loops for libsrt.  Keyword-only extras
 select the counter stream (seed / ray_id0 / sample0), a scripted ``table``
@@ -11,8 +12,9 @@ of uniforms, ``rng="trig64"`` (the reference's own trig-hash draw in fp64,
 for direct comparison with the unmodified reference), and the device.
 
 Differences from the reference, by construction:
-* the acceptance draw is the counter RNG (or a table), not the trig hash of
-  the fp64 hit position (SURVEY.md F2);
+* the default acceptance draw is the counter RNG (or a table), not the trig
+  hash of the fp64 hit position; ``rng="trig64"`` restores
+  the reference's own draw;
 * depths are traced in fp32 (``out_t`` agrees to ~1e-6 relative);
 * multi-primitive reference leaves keep their per-primitive box tests.
 """
