@@ -17,6 +17,12 @@
 //   6. k_geom         primitive records permuted into leaf ("slot") order.
 // With method SRT_BVH_PLOC, steps 4-5 are replaced by agglomerative PLOC
 // clustering over the same Morton order (ploc.cu).
+#include <functional>
+#include <vector>
+#include <cstring>
+#include <cstdio>
+#include <algorithm>
+#include <cmath>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "srt_internal.h"
@@ -384,7 +390,7 @@ struct Entry4 {
     float lo[3], hi[3];
 };
 
-__device__ __forceinline__ void node2_child(const Node2 &nd, int c, Entry4 &e) {
+__host__ __device__ __forceinline__ void node2_child(const Node2 &nd, int c, Entry4 &e) {
     if (c == 0) {
         e.code = nd.kids.x;
         e.lo[0] = nd.xy0.x; e.hi[0] = nd.xy0.y; e.lo[1] = nd.xy0.z; e.hi[1] = nd.xy0.w;
@@ -396,9 +402,53 @@ __device__ __forceinline__ void node2_child(const Node2 &nd, int c, Entry4 &e) {
     }
 }
 
-__device__ __forceinline__ float area(const Entry4 &e) {
+__host__ __device__ __forceinline__ float area(const Entry4 &e) {
     float dx = e.hi[0] - e.lo[0], dy = e.hi[1] - e.lo[1], dz = e.hi[2] - e.lo[2];
     return dx * dy + dy * dz + dz * dx;
+}
+
+// Node4 record from up to 4 child entries (boxes) and their final codes (inner
+// node4 index, leaf ~slot, kLeafEmpty), with the traversal hints: valid / leaf
+// child masks and, for each of the 8 ray direction octants, the children
+// ordered near-to-far along that octant's diagonal (2 bits per child).
+__host__ __device__ inline void make_node4(Node4 &o, const Entry4 *e, int cnt, const int *kids) {
+    float lo[3][4], hi[3][4];
+    for (int k = 0; k < 4; ++k)
+        for (int a = 0; a < 3; ++a) {
+            lo[a][k] = k < cnt ? e[k].lo[a] : 3.0e38f;
+            hi[a][k] = k < cnt ? e[k].hi[a] : -3.0e38f;
+        }
+    o.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    o.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    o.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    o.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    o.kids = make_int4(kids[0], kids[1], kids[2], kids[3]);
+    unsigned validm = 0, leafm = 0;
+    float ctr[4][3];
+    for (int k = 0; k < 4; ++k) {
+        if (kids[k] != kLeafEmpty) validm |= 1u << k;
+        if (kids[k] < 0 && kids[k] != kLeafEmpty) leafm |= 1u << k;
+        for (int a = 0; a < 3; ++a) ctr[k][a] = 0.5f * (lo[a][k] + hi[a][k]);
+    }
+    unsigned ord[2] = {0, 0};
+    for (int oc = 0; oc < 8; ++oc) {
+        float dir[3] = {(oc & 1) ? -1.f : 1.f, (oc & 2) ? -1.f : 1.f, (oc & 4) ? -1.f : 1.f};
+        float key[4];
+        int idx[4] = {0, 1, 2, 3};
+        for (int k = 0; k < 4; ++k)
+            key[k] = (validm >> k) & 1u ? ctr[k][0] * dir[0] + ctr[k][1] * dir[1] + ctr[k][2] * dir[2] : 3.0e38f;
+        for (int i = 1; i < 4; ++i)  // insertion sort of 4
+            for (int j = i; j > 0 && key[idx[j]] < key[idx[j - 1]]; --j) {
+                int t = idx[j];
+                idx[j] = idx[j - 1];
+                idx[j - 1] = t;
+            }
+        unsigned byte = idx[0] | (idx[1] << 2) | (idx[2] << 4) | (idx[3] << 6);
+        ord[oc >> 2] |= byte << ((oc & 3) * 8);
+    }
+    o.pad = make_int4((int)(validm | (leafm << 4)), (int)ord[0], (int)ord[1], cnt);
 }
 
 // work item: (binary node id, 4-wide node index)
@@ -440,69 +490,171 @@ __global__ void k_collapse4(const Node2 *__restrict__ n2, const int2 *__restrict
     for (int k = 0; k < cnt; ++k) ninner += e[k].code >= 0;
     int base4 = ninner ? atomicAdd(n4_count, ninner) : 0;
     int basew = ninner ? atomicAdd(n_out, ninner) : 0;
-    float lo[3][4], hi[3][4];
     int kids[4];
     int j = 0;
     for (int k = 0; k < 4; ++k) {
-        if (k < cnt) {
-            for (int a = 0; a < 3; ++a) {
-                lo[a][k] = e[k].lo[a];
-                hi[a][k] = e[k].hi[a];
-            }
-            if (e[k].code >= 0) {
-                kids[k] = base4 + j;
-                work_out[basew + j] = make_int2(e[k].code, base4 + j);
-                ++j;
-            } else {
-                kids[k] = e[k].code;
-            }
+        if (k < cnt && e[k].code >= 0) {
+            kids[k] = base4 + j;
+            work_out[basew + j] = make_int2(e[k].code, base4 + j);
+            ++j;
         } else {
-            for (int a = 0; a < 3; ++a) {
-                lo[a][k] = 3.0e38f;
-                hi[a][k] = -3.0e38f;
-            }
-            kids[k] = kLeafEmpty;
+            kids[k] = k < cnt ? e[k].code : kLeafEmpty;
         }
     }
     Node4 o;
-    o.lox = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-    o.hix = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-    o.loy = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-    o.hiy = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-    o.loz = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-    o.hiz = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-    o.kids = make_int4(kids[0], kids[1], kids[2], kids[3]);
-    // traversal hints: valid / leaf child masks and, for each of the 8 ray
-    // direction octants, the children ordered near-to-far along that octant's
-    // diagonal (2 bits per child, 8 bits per octant)
-    unsigned validm = 0, leafm = 0;
-    float ctr[4][3];
-    for (int k = 0; k < 4; ++k) {
-        if (kids[k] != kLeafEmpty) validm |= 1u << k;
-        if (kids[k] < 0 && kids[k] != kLeafEmpty) leafm |= 1u << k;
-        for (int a = 0; a < 3; ++a) ctr[k][a] = 0.5f * (lo[a][k] + hi[a][k]);
-    }
-    unsigned ord[2] = {0, 0};
-    for (int oc = 0; oc < 8; ++oc) {
-        float dir[3] = {(oc & 1) ? -1.f : 1.f, (oc & 2) ? -1.f : 1.f, (oc & 4) ? -1.f : 1.f};
-        float key[4];
-        int idx[4] = {0, 1, 2, 3};
-        for (int k = 0; k < 4; ++k)
-            key[k] = (validm >> k) & 1u ? ctr[k][0] * dir[0] + ctr[k][1] * dir[1] + ctr[k][2] * dir[2] : 3.0e38f;
-        for (int i = 1; i < 4; ++i)  // insertion sort of 4
-            for (int j = i; j > 0 && key[idx[j]] < key[idx[j - 1]]; --j) {
-                int t = idx[j];
-                idx[j] = idx[j - 1];
-                idx[j - 1] = t;
-            }
-        unsigned byte = idx[0] | (idx[1] << 2) | (idx[2] << 4) | (idx[3] << 6);
-        ord[oc >> 2] |= byte << ((oc & 3) * 8);
-    }
-    o.pad = make_int4((int)(validm | (leafm << 4)), (int)ord[0], (int)ord[1], cnt);
+    make_node4(o, e, cnt, kids);
     n4[w.y] = o;
 }
 
+// ---------------------------------------------------------------------------
+// Cost-optimal collapse (host dynamic programme over the binary tree, after
+// Ylitie et al. 2017's wide-BVH collapse).  For binary node x with children
+// a, b and slot counts j = 1..4:
+//   F(x, 1) = T(x)  (x becomes a 4-wide node)      F(leaf, 1) = A(leaf) * cj
+//   F(x, j) = G(x, j) = min_{j1 + j2 = j} F(a, j1) + F(b, j2)   (x opened)
+//   T(x)    = A(x) * cv + min_{j = 2..4} [A(x) * ct * j + G(x, j)]
+// with A the box surface area (visit probability), cv the cost of visiting a
+// node, ct of testing one child box, cj of one leaf job.  The 4-wide tree is
+// then emitted top-down (breadth first) following the argmins.
+// ---------------------------------------------------------------------------
+static srt_status collapse4_dp(SrtScene *s, float cv, float ct, float cj) {
+    const int m2 = s->num_nodes;
+    std::vector<Node2> n2(m2);
+    srt_status rc = cuda_status(cudaMemcpy(n2.data(), s->d_nodes, sizeof(Node2) * m2, cudaMemcpyDeviceToHost),
+                                "node download");
+    if (rc) return rc;
+    const float INF = INFINITY;
+    std::vector<float> F((size_t)m2 * 4, INF);
+    std::vector<signed char> split((size_t)m2 * 4, 1), bestj(m2, 2);
+    auto childF = [&](const Entry4 &e, int j) -> float {  // j = 1..4
+        if (e.code == kLeafEmpty) return INF;
+        if (e.code < 0) return j == 1 ? area(e) * cj : INF;
+        return F[(size_t)e.code * 4 + (j - 1)];
+    };
+    // post-order over the binary tree from the root (node 0)
+    std::vector<int> order;
+    order.reserve(m2);
+    {
+        std::vector<int> stk{0};
+        while (!stk.empty()) {
+            int x = stk.back();
+            stk.pop_back();
+            order.push_back(x);
+            for (int c = 0; c < 2; ++c) {
+                int code = c == 0 ? n2[x].kids.x : n2[x].kids.y;
+                if (code >= 0) stk.push_back(code);
+            }
+        }
+    }
+    for (int oi = (int)order.size() - 1; oi >= 0; --oi) {
+        const int x = order[oi];
+        Entry4 a, b;
+        node2_child(n2[x], 0, a);
+        node2_child(n2[x], 1, b);
+        Entry4 u = a;
+        if (b.code != kLeafEmpty)
+            for (int k = 0; k < 3; ++k) {
+                u.lo[k] = a.code == kLeafEmpty ? b.lo[k] : std::min(a.lo[k], b.lo[k]);
+                u.hi[k] = a.code == kLeafEmpty ? b.hi[k] : std::max(a.hi[k], b.hi[k]);
+            }
+        const float A = area(u);
+        float G[5] = {INF, INF, INF, INF, INF};
+        for (int j = 1; j <= 4; ++j) {
+            if (a.code == kLeafEmpty || b.code == kLeafEmpty) {  // single child (one-primitive trees)
+                G[j] = childF(a.code == kLeafEmpty ? b : a, j);
+                split[(size_t)x * 4 + j - 1] = (signed char)(a.code == kLeafEmpty ? 0 : j);
+                continue;
+            }
+            for (int j1 = 1; j1 < j; ++j1) {
+                float c = childF(a, j1) + childF(b, j - j1);
+                if (c < G[j]) {
+                    G[j] = c;
+                    split[(size_t)x * 4 + j - 1] = (signed char)j1;
+                }
+            }
+        }
+        float best = INF;
+        int bj = 2;
+        for (int j = 1; j <= 4; ++j) {
+            float c = A * ct * (float)j + G[j];
+            if (c < best) {
+                best = c;
+                bj = j;
+            }
+        }
+        if (!(best < INF)) bj = (a.code == kLeafEmpty || b.code == kLeafEmpty) ? 1 : 2;  // unbounded boxes
+        bestj[x] = (signed char)bj;
+        F[(size_t)x * 4 + 0] = A * cv + best;
+        for (int j = 2; j <= 4; ++j) F[(size_t)x * 4 + j - 1] = G[j];
+    }
+    // top-down emission, breadth first: node4 index 0 is the root
+    std::vector<Node4> out;
+    out.reserve(m2);
+    std::vector<int> queue{0};
+    std::vector<Entry4> slots;
+    // expand entry e (a child box + code) into j slots
+    std::function<void(const Entry4 &, int)> expand = [&](const Entry4 &e, int j) {
+        if (j == 1 || e.code < 0) {
+            slots.push_back(e);
+            return;
+        }
+        Entry4 a, b;
+        node2_child(n2[e.code], 0, a);
+        node2_child(n2[e.code], 1, b);
+        int j1 = split[(size_t)e.code * 4 + j - 1];
+        if (a.code == kLeafEmpty) return expand(b, j);
+        if (b.code == kLeafEmpty) return expand(a, j);
+        expand(a, j1);
+        expand(b, j - j1);
+    };
+    out.emplace_back();
+    for (size_t qi = 0; qi < queue.size(); ++qi) {
+        const int x = queue[qi];
+        slots.clear();
+        Entry4 a, b;
+        node2_child(n2[x], 0, a);
+        node2_child(n2[x], 1, b);
+        const int j = bestj[x];
+        if (a.code == kLeafEmpty || b.code == kLeafEmpty) {
+            expand(a.code == kLeafEmpty ? b : a, j);
+        } else {
+            int j1 = split[(size_t)x * 4 + j - 1];
+            expand(a, j1);
+            expand(b, j - j1);
+        }
+        int kids[4];
+        const int cnt = (int)slots.size();
+        for (int k = 0; k < 4; ++k) {
+            if (k < cnt && slots[k].code >= 0) {
+                kids[k] = (int)out.size();
+                out.emplace_back();
+                queue.push_back(slots[k].code);
+            } else {
+                kids[k] = k < cnt ? slots[k].code : kLeafEmpty;
+            }
+        }
+        make_node4(out[qi], slots.data(), cnt, kids);
+    }
+    if (s->d_nodes4) cudaFree(s->d_nodes4);
+    s->d_nodes4 = nullptr;
+    rc = cuda_status(cudaMalloc(&s->d_nodes4, sizeof(Node4) * out.size()), "node4 alloc");
+    if (!rc)
+        rc = cuda_status(cudaMemcpy(s->d_nodes4, out.data(), sizeof(Node4) * out.size(), cudaMemcpyHostToDevice),
+                         "node4 upload");
+    if (!rc) s->num_nodes4 = (int32_t)out.size();
+    return rc;
+}
+
 srt_status collapse4(SrtScene *s) {
+    if (s->num_nodes > 0) {
+        static const char *mode = getenv("SRT_COLLAPSE");
+        if (mode && !strcmp(mode, "dp")) {
+            float cv = 1.0f, ct = 0.25f, cj = 1.0f;
+            if (const char *c = getenv("SRT_COLLAPSE_COSTS")) sscanf(c, "%f,%f,%f", &cv, &ct, &cj);
+            cudaStreamSynchronize(s->stream);
+            return collapse4_dp(s, cv, ct, cj);
+        }
+    }
     cudaStream_t st = s->stream;
     if (s->d_nodes4) cudaFree(s->d_nodes4);
     s->d_nodes4 = nullptr;
