@@ -184,5 +184,42 @@ def biased() -> None:
     np.savez_compressed(OUT / "biased_500.npz", **res)
 
 
+def c3target() -> None:
+    """10. The headline workload at full scale, from the unmodified reference:
+    density-preserving random_cloud(1M, SH3, f = (1e4/n)^(1/3)), its own SAH
+    BVH, trace_batch ids/depths of the pass-0 camera rays of a 16-pixel grid
+    of the 1920x1080 frame, and render()'s rgb/opacity on the same grid."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+    sys.path.insert(0, REF)
+    from splatray import kernels, synthetic
+    from splatray.config import RenderSettings
+
+    R = importlib.import_module("splatray.render")
+    n = 1_000_000
+    f = (1e4 / n) ** (1.0 / 3.0)
+    a = synthetic.random_cloud(n, seed=0, scale_range=(0.02 * f, 0.25 * f), sh_degree=3)
+    cam = synthetic.front_camera()
+    st = RenderSettings(width=1920, height=1080, spp=1)
+    bvh = R.scene_bvh(a, st.cutoff_s)
+    xs, ys = np.meshgrid(np.arange(8, 1920, 16), np.arange(8, 1080, 16))
+    rays = [R.generate_camera_ray(cam, st, (int(x), int(y)), 0) for x, y in zip(xs.ravel(), ys.ravel())]
+    origins = np.array([r.origin for r in rays])
+    dirs = np.array([r.direction for r in rays])
+    pk = a.packed
+    tmax = float(np.finfo(np.float64).max)
+    out_t = np.empty((len(rays), 1))
+    out_id = np.empty((len(rays), 1), np.int64)
+    kernels.trace_batch(*R._bvh_args(bvh), pk.means, pk.cov_inv6, pk.opacities, origins, dirs, 0.0, tmax, 0,
+                        st.cutoff_s ** 2, True, out_t, out_id)
+    buf = R.render(a, cam, st, bvh=bvh)
+    np.savez_compressed(OUT / "c3target_grid.npz", px=xs.ravel(), py=ys.ravel(), origins=origins, dirs=dirs,
+                        t=out_t, id=out_id, rgb=buf.rgb[ys, xs].reshape(-1, 3), opacity=buf.opacity[ys, xs].ravel())
+
+
 if __name__ == "__main__":
-    biased() if sys.argv[1:] == ["biased"] else main()
+    if sys.argv[1:] == ["biased"]:
+        biased()
+    elif sys.argv[1:] == ["c3target"]:
+        c3target()
+    else:
+        main()

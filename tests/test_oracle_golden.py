@@ -202,3 +202,20 @@ def test_biased_batch_bitwise(oracle, golden):
             rgb = oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 2, t["origins"], t["dirs"], kk,
                                       mode=mode, s2=S2, background=[0.15, 0.25, 0.35], rng="trig")
             np.testing.assert_array_equal(rgb, g[f"rgb_m{mode}_k{kk}"])
+
+
+def test_c3target_scale_trace_bitwise(oracle, golden):
+    """The oracle at the headline scale (density-preserving 1M SH-3 cloud, its
+    SAH tree, pass-0 camera rays of a 16-pixel grid of the 1080p frame):
+    trace_batch ids and depths bit-identical to the unmodified reference's."""
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    g = golden("c3target_grid")
+    a = density_cloud(1_000_000)
+    pk = a.packed
+    lo, hi = a.aabb_arrays(np.sqrt(S2))
+    b = oracle.sah_build(lo, hi)
+    t, ids = oracle.trace_batch(b, pk.means, pk.cov_inv6, pk.opacities, g["origins"], g["dirs"], 0.0, TMAX, 0, S2,
+                                True, 1, rng="trig")
+    np.testing.assert_array_equal(ids, g["id"])
+    np.testing.assert_array_equal(t, g["t"])
