@@ -64,7 +64,9 @@ def main() -> None:
     one = SplatAsset(means=np.zeros((1, 3)), rotations=np.array([[1.0, 0, 0, 0]]), scales=np.full((1, 3), 0.3),
                      opacities=np.array([0.5]), sh=np.zeros((1, 3, 1)))
     render(one, front_camera(), RenderSettings(width=8, height=8, spp=1))
-    print("sanitize workload ok")
+    from paper_2504_06598_b200 import _lib
+
+    print("sanitize workload ok,", getattr(_lib.load(), "_name", "?"))
 
 
 if __name__ == "__main__":
