@@ -1386,9 +1386,10 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
 template <int MODE>
 __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double *__restrict__ rays, int64_t R,
                                                        double t_min, double t_max, float s2, double *out,
-                                                       int *overflow) {
+                                                       int *overflow, const uint32_t *__restrict__ perm) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R) return;
+    if (perm) i = __ldg(perm + i);  // walked in sorted order, written in the caller's
     const double *q = rays + i * 6;
     RayState r;
     init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
@@ -1429,11 +1430,22 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
                                 int mode, double s2, double *d_out, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
     if (blocks == 0) return SRT_OK;
+    uint32_t *perm = nullptr;
+    void *sort_mem = nullptr;
+    static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
+    if (R >= sort_min && R <= (int64_t)UINT32_MAX) {
+        srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
+        if (rc) return rc;
+    }
     if (mode == 0)
-        k_transmittance<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag);
+        k_transmittance<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
+                                                   perm);
     else
-        k_transmittance<1><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag);
-    return cuda_status(cudaGetLastError(), "k_transmittance launch");
+        k_transmittance<1><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
+                                                   perm);
+    srt_status rc = cuda_status(cudaGetLastError(), "k_transmittance launch");
+    if (sort_mem) cudaFreeAsync(sort_mem, st);
+    return rc;
 }
 
 }  // namespace srt
