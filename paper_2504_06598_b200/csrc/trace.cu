@@ -286,12 +286,19 @@ struct CameraSource {
     unsigned long long *acc64;
     uint32_t npass, unit;
     __host__ __device__ __forceinline__ uint32_t total() const { return unit * npass; }
+    // Work items are packet-major: the npass consecutive 32-item packets of
+    // a group walk the same 32 pixels, one pass each, so the group's nodes
+    // and primitives are fetched once into L1/L2 for all of its passes.
+    __device__ __forceinline__ uint32_t item_pass(uint32_t idx) const { return (idx >> 5) % npass; }
+    __device__ __forceinline__ uint32_t item_pixel(uint32_t idx) const {
+        return ((idx >> 5) / npass) * 32u + (idx & 31u);
+    }
     template <int NS>
     __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
         uint32_t ps = (uint32_t)pass;
         if (npass > 1) {
-            uint32_t f = idx / unit;
-            idx -= f * unit;
+            const uint32_t f = item_pass(idx);
+            idx = item_pixel(idx);
             ps += f;
         }
         int px, py;
@@ -345,7 +352,7 @@ struct CameraSource {
             }
         }
         if (acc64) {
-            unsigned long long *q = acc64 + (int64_t)(idx % unit) * 4;
+            unsigned long long *q = acc64 + (int64_t)item_pixel(idx) * 4;
             atomicAdd(q + 0, __float2ull_rn(r * 4294967296.0f));
             atomicAdd(q + 1, __float2ull_rn(g * 4294967296.0f));
             atomicAdd(q + 2, __float2ull_rn(b * 4294967296.0f));
