@@ -286,9 +286,33 @@ def run_ours(args) -> None:
     achieved = alg_bytes / (trace_avg_ms * 1e-3) / 1e9
     peak, peak_src = _peaks()
 
-    # e2e: the public API with host buffers (rank 0 only, single device)
+    # e2e: the public API with host buffers.  N > 1: render_distributed on
+    # every rank (tile shards, one NCCL gather, f64 frame on rank 0's host),
+    # wall clock on rank 0 between barriers
     e2e = None
-    if rank == 0:
+    if world > 1:
+        from paper_2504_06598_b200.multi_gpu import render_distributed
+
+        render_distributed(asset, front_camera(), st, mode="tiles", device=local)  # warm
+        e2e_t = []
+        buf = None
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.fill_(1)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            t0 = time.perf_counter()
+            out_buf = render_distributed(asset, front_camera(), st, mode="tiles", device=local)
+            dist.barrier()
+            e2e_t.append(time.perf_counter() - t0)
+            buf = out_buf if rank == 0 else buf
+        if rank == 0:
+            e2e = {"value": rays_per_frame / statistics.median(e2e_t) / 1e6, "unit": "Mrays/s",
+                   "h2d_bytes_per_step": 192 * world, "d2h_bytes_per_step": int(buf.rgb.nbytes + buf.opacity.nbytes),
+                   "ms_per_frame": statistics.median(e2e_t) * 1e3,
+                   "path": "paper_2504_06598_b200.multi_gpu.render_distributed() on every rank: tile shards traced "
+                           "and shaded per GPU, one NCCL gather to rank 0, unpacked on its GPU, f64 AccumBuffer "
+                           "copied to rank 0's host; wall clock on rank 0 between barriers"}
+    elif rank == 0:
         render(asset, front_camera(), st, device=local)  # warm (allocates scratch)
         e2e_t = []
         for _ in range(max(3, min(args.steps, 10))):
