@@ -317,7 +317,15 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
         frame = render_frame(p, gpu_shard_renderer(sc, ct, settings, device), group)
     if frame is None:
         return None
-    f = frame.double().cpu().numpy()
+    if frame.is_cuda:
+        # f64 on the device, then one device->host copy into page-locked memory
+        f64 = frame.double()
+        host = torch.empty(f64.shape, dtype=torch.float64, pin_memory=True)
+        host.copy_(f64, non_blocking=True)
+        torch.cuda.current_stream(f64.device).synchronize()
+        f = host.numpy()
+    else:
+        f = frame.double().numpy()
     return AccumBuffer(f[..., :3], f[..., 3], settings.samples_per_pixel)
 
 
