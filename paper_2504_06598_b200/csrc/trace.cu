@@ -921,7 +921,11 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             // ---- inner children: warp-uniform order by the warp-min entry ----
             int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
                       (wkey[3] != 0x7FFFFFFF);
-            if (nin > 0) {
+            if (nin == 1) {
+                // one inner child hit: descend, nothing to order or push
+                int k = wkey[0] != 0x7FFFFFFF ? 0 : (wkey[1] != 0x7FFFFFFF ? 1 : (wkey[2] != 0x7FFFFFFF ? 2 : 3));
+                node = pick(kids, k);
+            } else if (nin > 1) {
 #define SRT_CX(a, b)                      \
     {                                     \
         int lo_ = min(wkey[a], wkey[b]);  \
