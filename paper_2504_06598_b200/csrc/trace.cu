@@ -837,7 +837,27 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 far = fminf(far, worst);
             }
         };
-        while (node != kDone) {
+        while (true) {
+            // the one job-flush site (a single inlined copy of the job code): a
+            // full batch, or the end of the walk
+            if (njobs >= BATCH || (node == kDone && sp == 0 && njobs)) run_jobs();
+            if (node == kDone) {
+                if (sp == 0) break;
+                // pop, culling entries beyond every lane's far bound
+                int maxfar = __reduce_max_sync(FULL, __float_as_int(far));  // far >= 0, or -inf when idle
+                __syncwarp();
+                while (sp > 0) {
+                    --sp;
+                    if (lane == 0) ct.add(5, 1);
+                    if (sstk_key[wid][sp] <= maxfar) {
+                        node = sstk_node[wid][sp];
+                        SRT_DCHECK(node >= 0 && node < s.num_nodes4);
+                        break;
+                    }
+                    if (lane == 0) ct.add(6, 1);
+                }
+                if (node == kDone) continue;  // all culled: flush what is queued, then finish
+            }
             if (lane == 0) ct.add(0, 1);
             int4 kids;
             int key[4];
@@ -867,7 +887,6 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     }
                     njobs += __popc(bm);
                 }
-                if (njobs >= BATCH) run_jobs();
                 unsigned ihit = anyhit & ~leafm;
                 if (ihit) {
                     unsigned ordb = ((unsigned)(oct < 4 ? hint.y : hint.z) >> ((oct & 3) * 8)) & 0xFFu;
@@ -915,9 +934,8 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     wkey[k] = __reduce_min_sync(FULL, h ? key[k] : 0x7FFFFFFF);
                 }
             }
-            // leaf jobs run in batches: deferring them a node or two only delays
-            // the far-bound clip, never changes a result (order-free acceptance)
-            if (njobs >= BATCH) run_jobs();
+            // leaf jobs run in batches (loop top): deferring them a node or two
+            // only delays the far-bound clip, never changes a result
             // ---- inner children: warp-uniform order by the warp-min entry ----
             int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
                       (wkey[3] != 0x7FFFFFFF);
@@ -951,25 +969,6 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 sp += nin - 1;
                 node = pick(kids, wkey[0] & 3);
             }
-            }
-            if (node == kDone) {
-                if (sp == 0 && njobs) run_jobs();
-                if (sp > 0) {
-                    // pop, culling entries beyond every lane's far bound
-                    int maxfar = __reduce_max_sync(FULL, __float_as_int(far));  // far >= 0, or -inf when idle
-                    __syncwarp();
-                    while (sp > 0) {
-                        --sp;
-                        if (lane == 0) ct.add(5, 1);
-                        if (sstk_key[wid][sp] <= maxfar) {
-                            node = sstk_node[wid][sp];
-                            SRT_DCHECK(node >= 0 && node < s.num_nodes4);
-                            break;
-                        }
-                        if (lane == 0) ct.add(6, 1);
-                    }
-                    if (node == kDone && njobs) run_jobs();
-                }
             }
             __syncwarp();
         }
