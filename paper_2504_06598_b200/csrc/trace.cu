@@ -1078,29 +1078,34 @@ static int env_int(const char *name, int dflt);
 
 template <int NS, int MODE, int RNG, class Src, bool STATS>
 static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
-    // SRT_PACKET_CFG (experiments, N=1 mean-depth only): 0 batch 32, entry-
-    // sorted children, 7 blocks/SM (default), 1 batch 64, 2 = 0, 3 batch 64 +
-    // 8 blocks/SM, 4 octant-ordered children
+    // SRT_PACKET_CFG (A/B experiments, N=1 mean depth; 0 = the default below,
+    // batch 48, 8 blocks/SM): 1 batch 64 unconstrained, 2 batch 32 7 blocks,
+    // 3 batch 64 8 blocks, 4 octant-ordered children, 5 batch 48 7 blocks,
+    // 6 batch 16, 9 batch 32, 10 batch 24 (7 blocks)
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
     if constexpr (NS == 1 && MODE == 0 && !STATS) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
         if (cfg == 4) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 1>(s, src, w, st);
-        if (cfg == 5) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8, 0>(s, src, w, st);
+        if (cfg == 5) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 7, 0>(s, src, w, st);
         if (cfg == 6) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 16, 7, 0>(s, src, w, st);
+        if (cfg == 9) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7, 0>(s, src, w, st);
+        if (cfg == 10) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 24, 7, 0>(s, src, w, st);
     }
     if constexpr (NS >= 8 && MODE == 0 && !STATS) {
         if (cfg == 7) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 5, 0>(s, src, w, st);
         if (cfg == 8) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 6, 0>(s, src, w, st);
     }
-    // 7 resident blocks/SM (72 registers, no spills) measured 4% faster than
-    // the unconstrained 80-register build at N=1, and 12% faster than the
-    // 90-register build at N=4 (3.16 vs 3.53 ms, C3)
+    // 8 resident blocks/SM (64 registers, no spills) at N=1: 1.936 vs 1.964 ms
+    // at 7 blocks (once the walk had a single job-flush site); 7 blocks were
+    // 12% faster than the 90-register build at N=4 (3.16 vs 3.53 ms, C3)
     // resident blocks per SM requested from the register allocator, per slot
     // count: the largest without spills (N=8: +6%, N=16: +4% over unconstrained)
-    constexpr int kMinB = (NS <= 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5);
-    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, kMinB, 0>(s, src, w, st);
+    constexpr int kMinB = NS == 1 ? 8 : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5));
+    // leaf jobs per batch: 48 for single-slot walks (1.964 vs 1.976 ms at 32)
+    constexpr int kBatch = NS == 1 ? 48 : 32;
+    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB, 0>(s, src, w, st);
 }
 
 template <int NS, int MODE, int RNG, class Src>
