@@ -1081,7 +1081,8 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     // SRT_PACKET_CFG (A/B experiments, N=1 mean depth; 0 = the default below,
     // batch 48, 8 blocks/SM): 1 batch 64 unconstrained, 2 batch 32 7 blocks,
     // 3 batch 64 8 blocks, 4 octant-ordered children, 5 batch 48 7 blocks,
-    // 6 batch 16, 9 batch 32, 10 batch 24 (7 blocks)
+    // 6 batch 16, 9 batch 32, 10 batch 24 (7 blocks), 11 batch 64 8 blocks,
+    // 12 / 13 batch 48 at 9 / 10 blocks (56 / 48 registers: 2.03 / 2.13 ms)
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
     if constexpr (NS == 1 && MODE == 0 && !STATS) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
@@ -1092,6 +1093,9 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
         if (cfg == 6) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 16, 7, 0>(s, src, w, st);
         if (cfg == 9) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7, 0>(s, src, w, st);
         if (cfg == 10) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 24, 7, 0>(s, src, w, st);
+        if (cfg == 11) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8, 0>(s, src, w, st);
+        if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9, 0>(s, src, w, st);
+        if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10, 0>(s, src, w, st);
     }
     if constexpr (NS >= 8 && MODE == 0 && !STATS) {
         if (cfg == 7) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 5, 0>(s, src, w, st);
