@@ -1097,6 +1097,10 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
         if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9, 0>(s, src, w, st);
         if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10, 0>(s, src, w, st);
     }
+    if constexpr ((NS == 2 || NS == 4) && MODE == 0 && !STATS) {
+        if (cfg == 14) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8, 0>(s, src, w, st);
+        if (cfg == 15) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 7, 0>(s, src, w, st);
+    }
     if constexpr (NS >= 8 && MODE == 0 && !STATS) {
         if (cfg == 7) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 5, 0>(s, src, w, st);
         if (cfg == 8) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 6, 0>(s, src, w, st);
@@ -1106,9 +1110,11 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     // 12% faster than the 90-register build at N=4 (3.16 vs 3.53 ms, C3)
     // resident blocks per SM requested from the register allocator, per slot
     // count: the largest without spills (N=8: +6%, N=16: +4% over unconstrained)
-    constexpr int kMinB = NS == 1 ? 8 : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5));
-    // leaf jobs per batch: 48 for single-slot walks (1.964 vs 1.976 ms at 32)
-    constexpr int kBatch = NS == 1 ? 48 : 32;
+    constexpr int kMinB = (NS == 1 || (NS == 2 && MODE == 0)) ? 8
+                          : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5));
+    // leaf jobs per batch: 48 for N=1 (1.964 vs 1.976 ms at 32) and N=4
+    // (2.957 vs 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
+    constexpr int kBatch = (NS == 1 || (NS == 4 && MODE == 0)) ? 48 : 32;
     return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB, 0>(s, src, w, st);
 }
 
