@@ -524,3 +524,26 @@ def test_large_incoherent_batch_walked_in_sorted_order(oracle):
     assert np.mean(ids == oid) >= 0.999
     same = (ids == oid) & (oid >= 0)
     np.testing.assert_allclose(t[same], ot[same], rtol=2e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("w,h,spp,nslots", [(96, 64, 8, 2), (17, 5, 32, 16), (1, 1, 3, 1)])
+def test_one_launch_frame_vs_oracle(oracle, w, h, spp, nslots):
+    """render() of multi-pass frames (one launch, fixed-point sums) against
+    the counter-mode oracle's means: same samples, so pixel means agree to
+    fp32 colour rounding wherever every sample's id agrees (>= 99% of pixels);
+    odd frame sizes and 16 slots included."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.scene import camera_tuple
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(5_000, seed=31, sh_degree=2)
+    st = RenderSettings(width=w, height=h, spp=spp, multisample=nslots, seed=6, background=[0.3, 0.2, 0.1])
+    got = render(a, front_camera(), st)
+    pk = a.packed
+    ct = camera_tuple(front_camera(), w, h)
+    ref = oracle.render(_oracle_bvh(oracle, a), pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree,
+                        np.array(ct), w, h, passes=st.passes, nslots=nslots, s2=S2, seed=6, rng="counter",
+                        background=st.background)
+    ok = np.all(np.abs(got.rgb - ref["rgb"]) <= 1e-5 * np.abs(ref["rgb"]) + 1e-6, axis=2)
+    ok &= np.abs(got.opacity - ref["opacity"]) <= 1e-12
+    assert ok.mean() >= 0.99, ok.mean()
