@@ -272,6 +272,7 @@ __device__ __forceinline__ void tile_pixel(const RenderArgs &a, int64_t lt, int 
 
 struct CameraSource {
     static constexpr bool kCoherent = true;  // neighbouring indices = neighbouring pixels
+    static constexpr bool kRayOrigin = false;  // every ray starts at cam.e
     CamD cam;
     RenderArgs a;
     int pass;
@@ -389,6 +390,7 @@ struct CameraSource {
 
 struct ArraySource {
     static constexpr bool kCoherent = false;
+    static constexpr bool kRayOrigin = true;
     const double *rays;  // (R, 6)
     const uint32_t *perm;  // optional processing order (sorted rays); results keyed by the original index
     uint32_t R;
@@ -423,6 +425,16 @@ struct ArraySource {
                                                   float) const {
         finish<NS>(idx, sl);
     }
+};
+
+// Explicit rays that point into one hemisphere (camera batches, the
+// reference's parallel jittered rays, validate.py:36-43), walked as warp
+// packets: neighbouring indices (after the optional sort) share nodes.  The
+// per-lane origin and 1/|d|^2 travel through shared memory to the leaf jobs.
+struct PacketArraySource : ArraySource {
+    static constexpr bool kCoherent = true;
+    CamD cam;              // unused (the packet kernel reads per-lane origins)
+    float f_tmin, f_tmax;  // the candidate interval as init_ray rounds it
 };
 
 // ---------------------------------------------------------------------------
@@ -543,10 +555,13 @@ struct ExactRay {
 // Leaf job of the packet kernel: screen on the owner's fp32 direction and
 // the shared camera origin; the exact fp64 stage rebuilds the owner's ray
 // from its fp64 direction only when the screen cannot decide.
-template <int NS, int MODE, bool STATS>
+// RO (explicit-ray packets): the owner's fp64 origin and 1/|d|^2 come from
+// ro[0..3] and the candidate interval from sr, instead of the camera's.
+template <int NS, int MODE, bool STATS, bool RO = false>
 __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, const ScreenRay &sr, const double *dd,
                                            const WalkCfg &w, int slot, unsigned long long *best,
-                                           const uint32_t *keys, float far, Counters<STATS> &ct) {
+                                           const uint32_t *keys, float far, Counters<STATS> &ct,
+                                           const double *ro = nullptr) {
     ct.add(1, 1);
     SRT_DCHECK(slot >= 0 && slot < s.n);
     const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
@@ -568,11 +583,17 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
     // unit in fp64 to an ulp, and 1/|d|^2 only sets the re-centring point,
     // so inv_dd = 1 (as in the screen) changes the fp32 result by < 1e-15
     ExactRay r;
-    r.ox = cam.e[0], r.oy = cam.e[1], r.oz = cam.e[2];
     r.dx = dd[0], r.dy = dd[1], r.dz = dd[2];
-    r.inv_dd = 1.0;
     r.fdx = (float)r.dx, r.fdy = (float)r.dy, r.fdz = (float)r.dz;
-    r.t_min = 0.0f, r.t_max0 = INFINITY;
+    if constexpr (RO) {
+        r.ox = ro[0], r.oy = ro[1], r.oz = ro[2];
+        r.inv_dd = ro[3];
+        r.t_min = sr.t_min, r.t_max0 = sr.t_max0;
+    } else {
+        r.ox = cam.e[0], r.oy = cam.e[1], r.oz = cam.e[2];
+        r.inv_dd = 1.0;
+        r.t_min = 0.0f, r.t_max0 = INFINITY;
+    }
     // one re-centring: the second (peak) re-centring only matters for extreme
     // anisotropy and would raise this loop's register count by ~10
     Cand c = candidate<MODE, ExactRay, false>(r, m, a, b, w.s2);
@@ -767,6 +788,10 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     __shared__ unsigned char sown[W][BATCH + 128];
     __shared__ int sstk_node[W][PSTACK];
     __shared__ int sstk_key[W][PSTACK];
+    // explicit-ray packets (Src::kRayOrigin): each lane's own origin
+    constexpr bool RO = Src::kRayOrigin;
+    __shared__ float4 sorg[RO ? W : 1][32];    // fp32 origin + max |o_i|
+    __shared__ double sdo[RO ? W : 1][32][4];  // fp64 origin + 1/|d|^2 (exact stage)
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t total = src.total();
@@ -788,6 +813,13 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             sdd[wid][lane][0] = r.dx;
             sdd[wid][lane][1] = r.dy;
             sdd[wid][lane][2] = r.dz;
+            if constexpr (RO) {
+                sorg[wid][lane] = make_float4(r.fox, r.foy, r.foz, r.omag);
+                sdo[wid][lane][0] = r.ox;
+                sdo[wid][lane][1] = r.oy;
+                sdo[wid][lane][2] = r.oz;
+                sdo[wid][lane][3] = r.inv_dd;
+            }
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
                 sbest[wid][lane][k] = pack_hit(sl.t[k], -1);
@@ -818,13 +850,23 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     int o = sown[wid][j];
                     float4 dv = sdir[wid][o];
                     ScreenRay sr;
-                    sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
                     sr.fdx = dv.x; sr.fdy = dv.y; sr.fdz = dv.z;
-                    sr.inv_dd = 1.0;  // camera directions are unit in fp64
-                    sr.t_min = 0.0f;
-                    sr.t_max0 = INFINITY;
-                    packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
-                                                skey[wid][o], dv.w, ct);
+                    if constexpr (RO) {
+                        float4 og = sorg[wid][o];
+                        sr.fox = og.x; sr.foy = og.y; sr.foz = og.z; sr.omag = og.w;
+                        sr.inv_dd = sdo[wid][o][3];
+                        sr.t_min = src.f_tmin;
+                        sr.t_max0 = src.f_tmax;
+                        packet_job<NS, MODE, STATS, true>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
+                                                          skey[wid][o], dv.w, ct, sdo[wid][o]);
+                    } else {
+                        sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
+                        sr.inv_dd = 1.0;  // camera directions are unit in fp64
+                        sr.t_min = 0.0f;
+                        sr.t_max0 = INFINITY;
+                        packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
+                                                    skey[wid][o], dv.w, ct);
+                    }
                 }
             }
             __syncwarp();
@@ -1084,7 +1126,7 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     // 6 batch 16, 9 batch 32, 10 batch 24 (7 blocks), 11 batch 64 8 blocks,
     // 12 / 13 batch 48 at 9 / 10 blocks (56 / 48 registers: 2.03 / 2.13 ms)
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
-    if constexpr (NS == 1 && MODE == 0 && !STATS) {
+    if constexpr (NS == 1 && MODE == 0 && !STATS && !Src::kRayOrigin) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
@@ -1097,11 +1139,11 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
         if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9, 0>(s, src, w, st);
         if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10, 0>(s, src, w, st);
     }
-    if constexpr ((NS == 2 || NS == 4) && MODE == 0 && !STATS) {
+    if constexpr ((NS == 2 || NS == 4) && MODE == 0 && !STATS && !Src::kRayOrigin) {
         if (cfg == 14) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8, 0>(s, src, w, st);
         if (cfg == 15) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 7, 0>(s, src, w, st);
     }
-    if constexpr (NS >= 8 && MODE == 0 && !STATS) {
+    if constexpr (NS >= 8 && MODE == 0 && !STATS && !Src::kRayOrigin) {
         if (cfg == 7) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 5, 0>(s, src, w, st);
         if (cfg == 8) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 6, 0>(s, src, w, st);
     }
@@ -1123,6 +1165,11 @@ static srt_status launch_trace_t(const SrtScene *s, const Src &src, const WalkCf
     if (src.total() == 0) return SRT_OK;
     static const int variant = env_int("SRT_TRACE_VARIANT", 3);
     static const bool stats = env_int("SRT_TRACE_STATS", 0) != 0 && s->d_stats;
+    if constexpr (Src::kCoherent && Src::kRayOrigin) {
+        // explicit-ray packets (launch_trace_rays decides when)
+        if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
+        return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
+    } else {
     if constexpr (Src::kCoherent) {
         if (variant == 3) {
             if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
@@ -1146,6 +1193,7 @@ static srt_status launch_trace_t(const SrtScene *s, const Src &src, const WalkCf
     }
     if (NS == 1 && variant == 1) return launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st);
     return launch_trace_v<NS, MODE, RNG, Src, 32, false>(s, src, w, st);
+    }
 }
 
 template <class Src, int RNG>
@@ -1310,24 +1358,31 @@ __global__ void k_ray_keys(const double *__restrict__ rays, uint32_t R, const in
     idx[i] = i;
 }
 
+// 64 evenly spaced rays of a batch (R >= 64): one shared origin (a camera
+// batch, already coherent in its given order) and whether every probed
+// direction lies in the hemisphere of the first (a coherent batch: camera
+// rays, the reference's parallel jittered rays, validate.py:36-43).  Only the
+// kernel choice depends on it, never a result.
+static srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin, bool &one_hemisphere,
+                             cudaStream_t st) {
+    double probe[64][6];
+    const size_t step = (size_t)(R / 64) * 6 * sizeof(double);
+    srt_status rc = cuda_status(cudaMemcpy2DAsync(probe, sizeof(probe[0]), d_rays, step, sizeof(probe[0]), 64,
+                                                  cudaMemcpyDeviceToHost, st), "ray probe");
+    if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "ray probe");
+    if (rc) return rc;
+    one_origin = one_hemisphere = true;
+    for (int j = 1; j < 64; ++j) {
+        one_origin &= probe[j][0] == probe[0][0] && probe[j][1] == probe[0][1] && probe[j][2] == probe[0][2];
+        one_hemisphere &= probe[j][3] * probe[0][3] + probe[j][4] * probe[0][4] + probe[j][5] * probe[0][5] > 0.0;
+    }
+    return SRT_OK;
+}
+
 static srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out,
                             cudaStream_t st) {
     *d_perm_out = nullptr;
     *d_mem_out = nullptr;
-    {
-        // 64 evenly spaced rays: one shared origin means a camera-like batch,
-        // already coherent in its given order -- walk it as it is
-        double probe[64][6];
-        const size_t step = (size_t)(R / 64) * 6 * sizeof(double);
-        srt_status rc0 = cuda_status(cudaMemcpy2DAsync(probe, sizeof(probe[0]), d_rays, step, sizeof(probe[0]), 64,
-                                                       cudaMemcpyDeviceToHost, st), "ray probe");
-        if (!rc0) rc0 = cuda_status(cudaStreamSynchronize(st), "ray probe");
-        if (rc0) return rc0;
-        bool one_origin = true;
-        for (int j = 1; j < 64 && one_origin; ++j)
-            one_origin = probe[j][0] == probe[0][0] && probe[j][1] == probe[0][1] && probe[j][2] == probe[0][2];
-        if (one_origin) return SRT_OK;
-    }
     size_t temp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)R, 0, 30, st);
@@ -1386,19 +1441,39 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     src.out_t = d_t;
     src.out_id = d_id;
     src.perm = nullptr;
-    // large batches are walked in sorted order (SRT_RAY_SORT=0 disables)
-    // (single-slot walks: the cooperative multi-slot kernel measured no gain)
+    // Batches of >= 4096 rays in one hemisphere are walked as warp packets
+    // (counter RNG; SRT_PACKET_RAYS: -1 auto, 0 never, 1 always); large
+    // batches from distinct origins are walked in sorted order (SRT_RAY_SORT=0
+    // disables; per-lane single-slot walks, or any packet walk)
+    const int packet_env = env_int("SRT_PACKET_RAYS", -1);  // read per call (tests switch it)
     static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
+    bool one_origin = false, one_hemisphere = false;
+    if (R >= 4096 && (R >= sort_min || packet_env < 0)) {
+        srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
+        if (rc) return rc;
+    }
+    const bool packets = p->rng == SRT_RNG_COUNTER &&
+                         (packet_env > 0 || (packet_env < 0 && R >= 4096 && one_hemisphere));
     void *sort_mem = nullptr;
-    if (R >= sort_min && nslots == 1) {
+    if (R >= sort_min && !one_origin && (nslots == 1 || packets)) {
         uint32_t *perm = nullptr;
         srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
         if (rc) return rc;
         src.perm = perm;
     }
     WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
-    srt_status rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st)
-                                            : dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
+    srt_status rc;
+    if (packets) {
+        PacketArraySource ps;
+        static_cast<ArraySource &>(ps) = src;
+        memset(&ps.cam, 0, sizeof(ps.cam));
+        ps.f_tmin = (float)p->t_min;  // the interval exactly as init_ray rounds it
+        ps.f_tmax = p->t_max >= 3.0e38 ? INFINITY : (float)p->t_max;
+        rc = dispatch<PacketArraySource, SRT_RNG_COUNTER>(s, ps, w, nslots, p->mode, st);
+    } else {
+        rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st)
+                                     : dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
+    }
     if (sort_mem) cudaFreeAsync(sort_mem, st);
     return rc;
 }

@@ -1,0 +1,111 @@
+"""Explicit rays (trace_batch, kernels.py:527-540) walked as warp packets.
+
+Batches of >= 4096 rays whose probed directions share a hemisphere (camera
+batches, the reference's parallel jittered rays, validate.py:36-43) go to the
+packet kernel with per-lane origins; SRT_PACKET_RAYS=1 forces it for any
+batch, 0 disables it.  Every route must give the oracle's ids on the same
+counter stream (>= 99.9%, ties only) and its depths within fp32 tolerance.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import CUTOFF, S2, TMAX, axis_rays, random_rays
+
+pytestmark = pytest.mark.gpu
+
+
+def camera_rays(w, h, origin=(0.0, 0.0, -6.0), half=0.45):
+    """Row-major pinhole rays from one origin towards the cloud (unit dirs)."""
+    xs = (np.arange(w) + 0.5) / w * 2.0 - 1.0
+    ys = 1.0 - (np.arange(h) + 0.5) / h * 2.0
+    gx, gy = np.meshgrid(xs * half * w / h, ys * half)
+    d = np.stack([gx.ravel(), gy.ravel(), np.ones(w * h)], axis=1)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = np.tile(np.asarray(origin, dtype=np.float64), (w * h, 1))
+    return o, d
+
+
+def _scene(n, seed, deg=0):
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    a = random_cloud(n, seed=seed, sh_degree=deg)
+    sc = DeviceScene.from_packed(a.packed)
+    sc.build_bvh(CUTOFF)
+    return a, sc
+
+
+def _check(oracle, a, sc, o, d, t_min, t_max, mode, nslots, seed=3, ray_id0=11, sample0=2):
+    t, ids = sc.trace_rays(o, d, t_min, t_max, mode, S2, True, nslots, "counter", seed=seed, ray_id0=ray_id0,
+                           sample0=sample0)
+    pk = a.packed
+    lo, hi = a.aabb_arrays(CUTOFF)
+    tr, ir = oracle.trace_batch(oracle.sah_build(lo, hi), pk.means, pk.cov_inv6, pk.opacities, o, d, t_min, t_max,
+                                mode, S2, True, nslots, rng="counter", seed=seed, ray_id0=ray_id0, sample0=sample0)
+    agree = np.mean(ids == ir)
+    assert agree >= 0.999, agree
+    hit = (ids == ir) & (ir >= 0)
+    assert hit.sum() > 0.05 * ids.size  # the batch actually hits the cloud
+    np.testing.assert_allclose(t[hit], tr[hit], rtol=2e-5, atol=1e-5)
+    assert np.all(np.isinf(t[ids < 0]))
+    return t, ids
+
+
+@pytest.mark.parametrize("nslots", [1, 4])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_forced_packets_on_incoherent_rays(oracle, monkeypatch, nslots, mode):
+    """Correctness never depends on coherence: random origins and directions."""
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
+    a, sc = _scene(20_000, 9)
+    o, d = random_rays(np.random.default_rng(2), 20_000)
+    _check(oracle, a, sc, o, d, 0.0, TMAX, mode, nslots)
+    sc.close()
+
+
+@pytest.mark.parametrize("nslots", [1, 2, 16])
+def test_camera_batch_auto_route(oracle, nslots):
+    a, sc = _scene(30_000, 4, deg=1)
+    o, d = camera_rays(128, 96)
+    _check(oracle, a, sc, o, d, 0.0, TMAX, 0, nslots)
+    sc.close()
+
+
+@pytest.mark.parametrize("nslots", [1, 4])
+def test_jittered_parallel_rays_sorted_packets(oracle, nslots):
+    """The reference's validate.py ray batch (distinct origins, one direction)
+    above the sort threshold: sorted packets, outputs keyed by input index."""
+    a, sc = _scene(10_000, 6)
+    o, d = axis_rays(np.random.default_rng(5), 70_000, lateral=1.5)
+    o[:, 2] = -5.0
+    _check(oracle, a, sc, o, d, 0.0, TMAX, 0, nslots)
+    sc.close()
+
+
+def test_packets_non_unit_directions_and_finite_interval(oracle, monkeypatch):
+    """1/|d|^2 and the (t_min, t_max) interval travel per batch / per lane."""
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
+    a, sc = _scene(20_000, 12)
+    o, d = camera_rays(80, 60)
+    # center mode's depth is (mu - o).d (kernels.py:171-173): a scaled d moves
+    # the evaluation point off the peak, so the reference hits almost nothing
+    _check(oracle, a, sc, o, d, 5.0, 7.0, 1, 4)
+    d *= np.linspace(0.5, 3.0, d.shape[0])[:, None]
+    _check(oracle, a, sc, o, d, 0.3, 4.0, 0, 1)
+    _check(oracle, a, sc, o, d, 0.3, 4.0, 0, 4)
+    sc.close()
+
+
+def test_routes_agree(monkeypatch):
+    """Packet and per-lane walks of the same camera batch: same ids and depths
+    up to threshold ties."""
+    a, sc = _scene(30_000, 7)
+    o, d = camera_rays(160, 120)
+    monkeypatch.setenv("SRT_PACKET_RAYS", "0")
+    t0, i0 = sc.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 2, "counter", seed=1)
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
+    t1, i1 = sc.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 2, "counter", seed=1)
+    sc.close()
+    assert np.mean(i0 == i1) >= 0.9999
+    same = (i0 == i1) & (i0 >= 0)
+    np.testing.assert_allclose(t0[same], t1[same], rtol=1e-6, atol=1e-7)

@@ -1,7 +1,9 @@
 """Throughput of explicit-ray walks (trace_batch semantics, srt_trace_rays_device)
 on device-resident rays: python tools/time_rays.py [n_prims] [n_rays] [kind] [N]
 kind: "random" (origins in the cloud, isotropic directions: incoherent
-secondary rays) or "camera" (the C3-target primary rays, row-major)."""
+secondary rays), "camera" (the C3-target primary rays, row-major) or
+"parallel" (validate.py:36-43-style jittered origins on z = -6, all along +z).
+SRT_PACKET_RAYS=0/1 pins the route (default: packets for one-hemisphere batches)."""
 import sys
 
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
@@ -25,6 +27,9 @@ if kind == "random":
     o = rng.uniform(-2, 2, (R, 3))
     d = rng.normal(size=(R, 3))
     d /= np.linalg.norm(d, axis=1, keepdims=True)
+elif kind == "parallel":
+    o = np.stack([rng.uniform(-2, 2, R), rng.uniform(-2, 2, R), np.full(R, -6.0)], axis=1)
+    d = np.tile([0.0, 0.0, 1.0], (R, 1))
 else:
     W, H = 1920, 1080
     cam = front_camera()
