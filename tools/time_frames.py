@@ -14,7 +14,8 @@ H = int(a[2]) if len(a) > 2 else 1080
 spp = int(a[3]) if len(a) > 3 else 1
 N = int(a[4]) if len(a) > 4 else 1
 reps = int(a[5]) if len(a) > 5 else 10
-asset = density_cloud(n) if n > 10_000 else random_cloud(n, sh_degree=0)
+_seed = int(__import__("os").environ.get("SRT_SEED", "0"))  # scene seed (sweeps over scenes)
+asset = density_cloud(n, seed=_seed) if n > 10_000 else random_cloud(n, seed=_seed, sh_degree=0)
 st = RenderSettings(width=W, height=H, spp=spp, multisample=N)
 sc = prepare(asset, st)
 import os
