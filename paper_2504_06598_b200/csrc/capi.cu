@@ -45,6 +45,49 @@ srt_status scratch_reserve(SrtScene *s, size_t bytes) {
     return SRT_OK;
 }
 
+__global__ void k_pack_rays(const double *__restrict__ o, const double *__restrict__ d, int64_t R, double *rays) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= R) return;
+    double *q = rays + i * 6;
+    q[0] = o[i * 3], q[1] = o[i * 3 + 1], q[2] = o[i * 3 + 2];
+    q[3] = d[i * 3], q[4] = d[i * 3 + 1], q[5] = d[i * 3 + 2];
+}
+
+static srt_status launch_pack_rays(const double *d_o, const double *d_d, int64_t R, double *d_rays, cudaStream_t st) {
+    k_pack_rays<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(d_o, d_d, R, d_rays);
+    return cuda_status(cudaGetLastError(), "k_pack_rays");
+}
+
+// The caller's (R,3) origin and direction arrays -> (R,6) ray records on the
+// device: two contiguous uploads into `stage` (48 R bytes), interleaved there
+// (no host packing pass).
+static srt_status upload_rays(const double *o, const double *d, int64_t R, double *stage, double *d_rays,
+                              cudaStream_t st) {
+    srt_status rc = cuda_status(cudaMemcpyAsync(stage, o, sizeof(double) * 3 * R, cudaMemcpyHostToDevice, st),
+                                "origins upload");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(stage + 3 * R, d, sizeof(double) * 3 * R, cudaMemcpyHostToDevice, st),
+                              "dirs upload");
+    if (!rc) rc = launch_pack_rays(stage, stage + 3 * R, R, d_rays, st);
+    return rc;
+}
+
+// t32 (f32 walk depths) or t64 (trig64 depths); misses (id < 0) -> +inf
+__global__ void k_widen_hits(const float *__restrict__ t32, const double *__restrict__ t64,
+                             const int32_t *__restrict__ id, int64_t m, double *t, int64_t *id64) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int32_t h = id[i];
+    double v = t32 ? (double)t32[i] : t64[i];
+    t[i] = t32 && h < 0 ? INFINITY : v;
+    id64[i] = h;
+}
+
+static srt_status launch_widen_hits(const float *t32, const double *t64, const int32_t *id, int64_t m, double *t,
+                             int64_t *id64, cudaStream_t st) {
+    k_widen_hits<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(t32, t64, id, m, t, id64);
+    return cuda_status(cudaGetLastError(), "k_widen_hits");
+}
+
 int64_t shard_tiles(int width, int height, int shard_index, int shard_count) {
     int64_t total = (int64_t)((width + 15) / 16) * ((height + 15) / 16);
     if (shard_count <= 1) return total;
@@ -607,21 +650,21 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     size_t ray_bytes = sizeof(double) * R * 6;
     size_t out_bytes = (sizeof(double) + sizeof(int32_t)) * R * nslots;
     size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
-    rc = scratch_reserve(s, ray_bytes + out_bytes + table_bytes + 256);
+    // staging: the caller's (R,3) origin and direction arrays on the way in,
+    // the widened (f64 t, i64 id) outputs on the way out
+    size_t stage_bytes = std::max(ray_bytes, sizeof(double) * 2 * R * nslots);
+    size_t stage_off = (ray_bytes + out_bytes + table_bytes + 255) & ~(size_t)255;
+    rc = scratch_reserve(s, stage_off + stage_bytes);
     if (rc) return rc;
     char *base = (char *)s->d_scratch;
     double *d_rays = (double *)base;
     float *d_t = (float *)(base + ray_bytes);
     int32_t *d_id = (int32_t *)(base + ray_bytes + sizeof(float) * R * nslots);
     double *d_table = table_bytes ? (double *)(base + ((ray_bytes + out_bytes + 15) & ~(size_t)15)) : nullptr;
-    std::vector<double> packed((size_t)R * 6);
-    for (int64_t i = 0; i < R; ++i) {
-        for (int k = 0; k < 3; ++k) {
-            packed[i * 6 + k] = origins[i * 3 + k];
-            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
-        }
-    }
-    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    double *d_stage = (double *)(base + stage_off);
+    // contiguous uploads straight from the caller's arrays, interleaved into
+    // the (R,6) ray records on the device (no host packing pass)
+    rc = upload_rays(origins, dirs, R, d_stage, d_rays, st);
     if (!rc && d_table)
         rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
     double *d_t64 = (double *)(base + ray_bytes);
@@ -632,26 +675,17 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
         else
             rc = launch_trace_rays(s, p, d_rays, R, nslots, d_table, d_t, d_id, st);
     }
-    if (!rc && p->rng == SRT_RNG_TRIG64) {
-        std::vector<int32_t> hid((size_t)R * nslots);
-        rc = cuda_status(cudaMemcpyAsync(out_t, d_t64, sizeof(double) * hid.size(), cudaMemcpyDeviceToHost, st), "t");
-        if (!rc) rc = cuda_status(cudaMemcpyAsync(hid.data(), d_id, sizeof(int32_t) * hid.size(), cudaMemcpyDeviceToHost, st), "id");
-        if (!rc) rc = check_flag(s, st);
-        if (rc) return rc;
-        for (size_t i = 0; i < hid.size(); ++i) out_id[i] = hid[i];
-        return SRT_OK;
-    }
-    std::vector<float> ht((size_t)R * nslots);
-    std::vector<int32_t> hid((size_t)R * nslots);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(ht.data(), d_t, sizeof(float) * ht.size(), cudaMemcpyDeviceToHost, st), "t download");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(hid.data(), d_id, sizeof(int32_t) * hid.size(), cudaMemcpyDeviceToHost, st), "id download");
+    // widen on the device (f32 t -> f64, +inf on miss; i32 id -> i64) and
+    // download straight into the caller's arrays
+    const int64_t m = R * (int64_t)nslots;
+    double *w_t = d_stage;
+    int64_t *w_id = (int64_t *)(d_stage + m);
+    if (!rc) rc = launch_widen_hits(p->rng == SRT_RNG_TRIG64 ? nullptr : d_t, p->rng == SRT_RNG_TRIG64 ? d_t64 : nullptr,
+                                    d_id, m, w_t, w_id, st);
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_t, w_t, sizeof(double) * m, cudaMemcpyDeviceToHost, st), "t download");
+    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_id, w_id, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, st), "id download");
     if (!rc) rc = check_flag(s, st);
-    if (rc) return rc;
-    for (size_t i = 0; i < ht.size(); ++i) {
-        out_t[i] = hid[i] >= 0 ? (double)ht[i] : INFINITY;
-        out_id[i] = hid[i];
-    }
-    return SRT_OK;
+    return rc;
 }
 
 srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, const double *dirs, int64_t R,
@@ -670,17 +704,11 @@ srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, con
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
     size_t ray_bytes = sizeof(double) * R * 6;
-    srt_status rc = scratch_reserve(s, ray_bytes + sizeof(double) * R);
+    srt_status rc = scratch_reserve(s, 2 * ray_bytes + sizeof(double) * R);
     if (rc) return rc;
     double *d_rays = (double *)s->d_scratch;
     double *d_out = d_rays + R * 6;
-    std::vector<double> packed((size_t)R * 6);
-    for (int64_t i = 0; i < R; ++i)
-        for (int k = 0; k < 3; ++k) {
-            packed[i * 6 + k] = origins[i * 3 + k];
-            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
-        }
-    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    rc = upload_rays(origins, dirs, R, d_out + R, d_rays, st);
     if (!rc) rc = launch_transmittance(s, d_rays, R, t_min, t_max, mode, s2, d_out, st);
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out, d_out, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "download");
     if (!rc) rc = check_flag(s, st);
@@ -704,18 +732,12 @@ srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const doubl
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
     size_t ray_bytes = sizeof(double) * R * 6;
-    srt_status rc = scratch_reserve(s, ray_bytes + sizeof(double) * R * 4);
+    srt_status rc = scratch_reserve(s, 2 * ray_bytes + sizeof(double) * R * 4);
     if (rc) return rc;
     double *d_rays = (double *)s->d_scratch;
     double *d_rgb = d_rays + R * 6;
     double *d_op = d_rgb + R * 3;
-    std::vector<double> packed((size_t)R * 6);
-    for (int64_t i = 0; i < R; ++i)
-        for (int k = 0; k < 3; ++k) {
-            packed[i * 6 + k] = origins[i * 3 + k];
-            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
-        }
-    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    rc = upload_rays(origins, dirs, R, d_op + R, d_rays, st);
     if (!rc) rc = launch_exact_rays(s, d_rays, R, t_min, t_max, mode, s2, background, d_rgb, d_op, st);
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * R * 3, cudaMemcpyDeviceToHost, st), "rgb");
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "op");
@@ -739,18 +761,12 @@ srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const do
     size_t ray_bytes = sizeof(double) * R * 6;
     size_t rgb_bytes = sizeof(double) * R * 3;
     size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
-    rc = scratch_reserve(s, ray_bytes + rgb_bytes + table_bytes);
+    rc = scratch_reserve(s, 2 * ray_bytes + rgb_bytes + table_bytes);
     if (rc) return rc;
     double *d_rays = (double *)s->d_scratch;
     double *d_rgb = d_rays + R * 6;
     double *d_table = table_bytes ? d_rgb + R * 3 : nullptr;
-    std::vector<double> packed((size_t)R * 6);
-    for (int64_t i = 0; i < R; ++i)
-        for (int k = 0; k < 3; ++k) {
-            packed[i * 6 + k] = origins[i * 3 + k];
-            packed[i * 6 + 3 + k] = dirs[i * 3 + k];
-        }
-    rc = cuda_status(cudaMemcpyAsync(d_rays, packed.data(), ray_bytes, cudaMemcpyHostToDevice, st), "rays upload");
+    rc = upload_rays(origins, dirs, R, (double *)((char *)(d_rgb + R * 3) + table_bytes), d_rays, st);
     if (!rc && d_table)
         rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
     if (!rc) rc = launch_biased_rays(s, p, d_rays, R, kk, background, d_table, d_rgb, st);
