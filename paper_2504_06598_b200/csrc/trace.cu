@@ -1526,16 +1526,172 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
     out[i] = result;
 }
 
+// Coherent transmittance batches (one hemisphere, e.g. shadow rays towards a
+// light): the warp walks its 32 rays as a packet -- one node fetch and slab
+// test per lane, leaf hits compacted by ballot into a job queue -- and every
+// job evaluates the owner's fp64 candidate exactly as k_transmittance does,
+// multiplying (1 - alpha) into the owner's product in shared memory.  The
+// walk is unclipped (kernels.py:392-432), so nothing is culled; only the
+// product order differs from the per-lane walk (roundoff).
+template <int MODE>
+__global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneView s, const double *__restrict__ rays,
+                                                                        const uint32_t *__restrict__ perm, uint32_t R,
+                                                                        double t_min, double t_max, float s2,
+                                                                        double *out, uint32_t *work, int *overflow) {
+    constexpr int W = kTraceThreads / 32;
+    constexpr int PSTACK = 128, BATCH = 32;
+    __shared__ double sray[W][32][6];
+    __shared__ unsigned long long sprod[W][32];
+    __shared__ int sjob[W][BATCH + 128];
+    __shared__ unsigned char sown[W][BATCH + 128];
+    __shared__ int sstk[W][PSTACK];
+    const unsigned FULL = 0xffffffffu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    while (true) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(work, 32u);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= R) break;
+        const uint32_t idx = base + (uint32_t)lane;
+        const bool valid = idx < R;
+        const uint32_t ri = valid ? (perm ? __ldg(perm + idx) : idx) : 0u;
+        RayState r;
+        float far;
+        if (valid) {
+            const double *q = rays + (int64_t)ri * 6;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) sray[wid][lane][c] = q[c];
+            init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+            sprod[wid][lane] = __double_as_longlong(1.0);
+            far = r.t_max0;
+        } else {
+            init_ray(r, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
+            far = -INFINITY;  // hits nothing
+        }
+        int sp = 0, njobs = 0;
+        int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
+        bool ovf = false;
+        while (true) {
+            if (njobs >= BATCH || (node == kDone && sp == 0 && njobs)) {
+                __syncwarp();
+                for (int jb = 0; jb < njobs; jb += 32) {
+                    const int j = jb + lane;
+                    if (j < njobs) {
+                        const int o = sown[wid][j];
+                        const int slot = sjob[wid][j];
+                        SRT_DCHECK(slot >= 0 && slot < s.n);
+                        const double *q = sray[wid][o];
+                        RayState ro;
+                        init_ray(ro, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+                        const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+                        float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+                        Cand cd = candidate<MODE>(ro, m, a, b, s2);
+                        if (cd.valid) {
+                            const double f = 1.0 - (double)cd.alpha;
+                            unsigned long long *p = &sprod[wid][o];
+                            unsigned long long old = *p, assumed;
+                            do {
+                                assumed = old;
+                                old = atomicCAS(p, assumed, __double_as_longlong(__longlong_as_double(assumed) * f));
+                            } while (assumed != old);
+                        }
+                    }
+                }
+                __syncwarp();
+                njobs = 0;
+            }
+            if (node == kDone) {
+                if (sp == 0 || ovf) break;
+                node = sstk[wid][--sp];
+            }
+            int4 kids;
+            int key[4];
+            SRT_DCHECK(node >= 0 && node < s.num_nodes4);
+            const unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
+            const unsigned anyhit = __reduce_or_sync(FULL, hitm);
+            node = kDone;
+            for (unsigned m = anyhit; m; m &= m - 1) {
+                const int k = __ffs(m) - 1;
+                const int code = pick(kids, k);  // warp-uniform
+                if (code < 0) {
+                    const bool h = (hitm >> k) & 1u;
+                    const unsigned bm = __ballot_sync(FULL, h);
+                    if (h) {
+                        const int o = njobs + __popc(bm & lt);
+                        SRT_DCHECK(o < BATCH + 128);
+                        sjob[wid][o] = ~code;
+                        sown[wid][o] = (unsigned char)lane;
+                    }
+                    njobs += __popc(bm);
+                } else if (node == kDone) {
+                    node = code;
+                } else if (sp < PSTACK) {
+                    if (lane == 0) sstk[wid][sp] = code;
+                    ++sp;
+                } else {
+                    if (lane == 0) atomicExch(overflow, 1);
+                    ovf = true;
+                }
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        if (valid) out[ri] = __longlong_as_double(sprod[wid][lane]);
+        __syncwarp();
+    }
+}
+
 srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max,
                                 int mode, double s2, double *d_out, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
     if (blocks == 0) return SRT_OK;
     uint32_t *perm = nullptr;
     void *sort_mem = nullptr;
+    // one-hemisphere batches of >= 4096 rays walk as packets (SRT_PACKET_RAYS
+    // as for srt_trace_rays); one-origin batches are already coherent: no sort
     static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
-    if (R >= sort_min && R <= (int64_t)UINT32_MAX) {
+    const int packet_env = env_int("SRT_PACKET_RAYS", -1);
+    const bool fits = R <= (int64_t)UINT32_MAX;
+    bool one_origin = false, one_hemisphere = false;
+    if (fits && R >= 4096 && (R >= sort_min || packet_env < 0)) {
+        srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
+        if (rc) return rc;
+    }
+    const bool packets = fits && (packet_env > 0 || (packet_env < 0 && R >= 4096 && one_hemisphere));
+    if (fits && R >= sort_min && !one_origin) {
         srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
         if (rc) return rc;
+    }
+    if (packets) {
+        static int blocks_per_sm = 0;
+        if (!blocks_per_sm) {
+            if (mode == 0)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_transmittance_packet<0>, kTraceThreads, 0);
+            else
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_transmittance_packet<1>, kTraceThreads, 0);
+            if (blocks_per_sm < 1) blocks_per_sm = 1;
+        }
+        if (!g_num_sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        uint32_t *work = s->next_work();
+        srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
+        int64_t need = (R + kTraceThreads - 1) / kTraceThreads;
+        int64_t grid = std::min<int64_t>((int64_t)g_num_sms * blocks_per_sm, need);
+        if (!rc) {
+            if (mode == 0)
+                k_transmittance_packet<0><<<(unsigned)grid, kTraceThreads, 0, st>>>(
+                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work, s->d_flag);
+            else
+                k_transmittance_packet<1><<<(unsigned)grid, kTraceThreads, 0, st>>>(
+                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work, s->d_flag);
+            rc = cuda_status(cudaGetLastError(), "k_transmittance_packet launch");
+        }
+        if (sort_mem) cudaFreeAsync(sort_mem, st);
+        return rc;
     }
     if (mode == 0)
         k_transmittance<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,

@@ -1,4 +1,5 @@
-"""Explicit rays (trace_batch, kernels.py:527-540) walked as warp packets.
+"""Explicit rays (trace_batch, kernels.py:527-540; transmittance_batch,
+kernels.py:544-557) walked as warp packets.
 
 Batches of >= 4096 rays whose probed directions share a hemisphere (camera
 batches, the reference's parallel jittered rays, validate.py:36-43) go to the
@@ -109,3 +110,49 @@ def test_routes_agree(monkeypatch):
     assert np.mean(i0 == i1) >= 0.9999
     same = (i0 == i1) & (i0 >= 0)
     np.testing.assert_allclose(t0[same], t1[same], rtol=1e-6, atol=1e-7)
+
+
+# ---- transmittance_batch (kernels.py:544-557) as packets --------------------
+
+def _check_trans(oracle, a, sc, o, d, t_min, t_max, mode):
+    got = sc.transmittance(o, d, t_min, t_max, mode, S2)
+    pk = a.packed
+    lo, hi = a.aabb_arrays(CUTOFF)
+    want = oracle.transmittance(oracle.sah_build(lo, hi), pk.means, pk.cov_inv6, pk.opacities, o, d, t_min, t_max,
+                                mode, S2)
+    assert np.mean(want < 0.999) > 0.05  # the batch actually crosses the cloud
+    np.testing.assert_allclose(got, want, rtol=2e-4, atol=2e-6)  # fp32 alphas (test_gpu_parity.py)
+    return got
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_transmittance_camera_batch_auto_route(oracle, mode):
+    a, sc = _scene(20_000, 3)
+    o, d = camera_rays(96, 64)
+    _check_trans(oracle, a, sc, o, d, 0.0, TMAX, mode)
+    _check_trans(oracle, a, sc, o, d, 5.0, 7.0, mode)
+    sc.close()
+
+
+def test_transmittance_forced_packets_incoherent_and_sorted(oracle, monkeypatch):
+    a, sc = _scene(10_000, 5)
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
+    o, d = random_rays(np.random.default_rng(4), 8_000)
+    _check_trans(oracle, a, sc, o, d, 0.0, TMAX, 0)
+    monkeypatch.delenv("SRT_PACKET_RAYS")
+    o, d = axis_rays(np.random.default_rng(6), 70_000, lateral=1.5)  # sorted packets
+    o[:, 2] = -5.0
+    _check_trans(oracle, a, sc, o, d, 0.0, TMAX, 0)
+    sc.close()
+
+
+def test_transmittance_routes_agree(monkeypatch):
+    """Packet and per-lane walks multiply the same factors in another order."""
+    a, sc = _scene(30_000, 8)
+    o, d = camera_rays(128, 96)
+    monkeypatch.setenv("SRT_PACKET_RAYS", "0")
+    t0 = sc.transmittance(o, d, 0.0, TMAX, 0, S2)
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
+    t1 = sc.transmittance(o, d, 0.0, TMAX, 0, S2)
+    sc.close()
+    np.testing.assert_allclose(t1, t0, rtol=1e-12, atol=1e-300)

@@ -6,3 +6,5 @@ for k in camera random; do
 done
 python tools/time_trace_e2e.py random 1 trans | tail -1
 SRT_LIBSRT_PATH=build/libsrt_prev.so python tools/time_trace_e2e.py random 1 trans | tail -1 | sed 's/^/prev: /'
+python tools/time_trace_e2e.py camera 1 trans | tail -1
+SRT_PACKET_RAYS=0 python tools/time_trace_e2e.py camera 1 trans | tail -1 | sed 's/^/per-lane: /'
