@@ -1379,6 +1379,14 @@ static srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin,
     return SRT_OK;
 }
 
+// Smallest one-hemisphere batch walked as packets by default: one-origin
+// batches are coherent as given; distinct origins need the sort, which only
+// pays for itself on large batches (parallel jittered rays in the 1M cloud:
+// packets 0.583 vs 0.523 ms per-lane at 60k rays, 2x faster at 2M;
+// tools/exp/prays3.sh, prays4.sh: 1.47x at 131k).
+constexpr int64_t PACKET_MIN_DISTINCT = 65536;
+static int64_t packet_min(bool one_origin) { return one_origin ? 4096 : PACKET_MIN_DISTINCT; }
+
 static srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out,
                             cudaStream_t st) {
     *d_perm_out = nullptr;
@@ -1448,14 +1456,17 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     const int packet_env = env_int("SRT_PACKET_RAYS", -1);  // read per call (tests switch it)
     static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
     bool one_origin = false, one_hemisphere = false;
-    if (R >= 4096 && (R >= sort_min || packet_env < 0)) {
+    if (R >= 4096) {
         srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
         if (rc) return rc;
     }
     const bool packets = p->rng == SRT_RNG_COUNTER &&
-                         (packet_env > 0 || (packet_env < 0 && R >= 4096 && one_hemisphere));
+                         (packet_env > 0 || (packet_env < 0 && one_hemisphere && R >= packet_min(one_origin)));
     void *sort_mem = nullptr;
-    if (R >= sort_min && !one_origin && (nslots == 1 || packets)) {
+    // packets from distinct origins need the sort at any size (unsorted
+    // random-origin packets walk 5x slower)
+    const bool sort_on = sort_min != INT_MAX;
+    if (!one_origin && ((packets && sort_on && R >= 4096) || (R >= sort_min && nslots == 1))) {
         uint32_t *perm = nullptr;
         srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
         if (rc) return rc;
@@ -1654,12 +1665,12 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
     const int packet_env = env_int("SRT_PACKET_RAYS", -1);
     const bool fits = R <= (int64_t)UINT32_MAX;
     bool one_origin = false, one_hemisphere = false;
-    if (fits && R >= 4096 && (R >= sort_min || packet_env < 0)) {
+    if (fits && R >= 4096) {
         srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
         if (rc) return rc;
     }
-    const bool packets = fits && (packet_env > 0 || (packet_env < 0 && R >= 4096 && one_hemisphere));
-    if (fits && R >= sort_min && !one_origin) {
+    const bool packets = fits && (packet_env > 0 || (packet_env < 0 && one_hemisphere && R >= packet_min(one_origin)));
+    if (fits && !one_origin && (R >= sort_min || (packets && sort_min != INT_MAX && R >= 4096))) {
         srt_status rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
         if (rc) return rc;
     }

@@ -72,12 +72,14 @@ def test_camera_batch_auto_route(oracle, nslots):
     sc.close()
 
 
-@pytest.mark.parametrize("nslots", [1, 4])
-def test_jittered_parallel_rays_sorted_packets(oracle, nslots):
+@pytest.mark.parametrize("nslots,nrays", [(1, 70_000), (4, 70_000), (1, 20_000)])
+def test_jittered_parallel_rays_sorted_packets(oracle, monkeypatch, nslots, nrays):
     """The reference's validate.py ray batch (distinct origins, one direction)
-    above the sort threshold: sorted packets, outputs keyed by input index."""
+    as packets (forced: the default takes them from PACKET_MIN_DISTINCT rays):
+    sorted at any size >= 4096, outputs keyed by input index."""
+    monkeypatch.setenv("SRT_PACKET_RAYS", "1")
     a, sc = _scene(10_000, 6)
-    o, d = axis_rays(np.random.default_rng(5), 70_000, lateral=1.5)
+    o, d = axis_rays(np.random.default_rng(5), nrays, lateral=1.5)
     o[:, 2] = -5.0
     _check(oracle, a, sc, o, d, 0.0, TMAX, 0, nslots)
     sc.close()
@@ -139,7 +141,6 @@ def test_transmittance_forced_packets_incoherent_and_sorted(oracle, monkeypatch)
     monkeypatch.setenv("SRT_PACKET_RAYS", "1")
     o, d = random_rays(np.random.default_rng(4), 8_000)
     _check_trans(oracle, a, sc, o, d, 0.0, TMAX, 0)
-    monkeypatch.delenv("SRT_PACKET_RAYS")
     o, d = axis_rays(np.random.default_rng(6), 70_000, lateral=1.5)  # sorted packets
     o[:, 2] = -5.0
     _check_trans(oracle, a, sc, o, d, 0.0, TMAX, 0)
