@@ -399,6 +399,7 @@ struct ArraySource {
     uint32_t fkey, ray_id0, sample0;
     float *out_t;
     int32_t *out_id;
+    int ostride;  // output row length (nslots, or the full slot count of a slot group)
     __host__ __device__ __forceinline__ uint32_t total() const { return R; }
     template <int NS>
     __device__ __forceinline__ bool init(uint32_t idx, RayState &r, Slots<NS> &sl) const {
@@ -416,8 +417,8 @@ struct ArraySource {
 #pragma unroll
         for (int k = 0; k < NS; ++k)
             if (k < nslots) {
-                out_t[(int64_t)idx * nslots + k] = sl.id[k] >= 0 ? sl.t[k] : INFINITY;
-                out_id[(int64_t)idx * nslots + k] = sl.id[k];
+                out_t[(int64_t)idx * ostride + k] = sl.id[k] >= 0 ? sl.t[k] : INFINITY;
+                out_id[(int64_t)idx * ostride + k] = sl.id[k];
             }
     }
     template <int NS>
@@ -1473,17 +1474,31 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
         src.perm = perm;
     }
     WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
-    srt_status rc;
-    if (packets) {
-        PacketArraySource ps;
-        static_cast<ArraySource &>(ps) = src;
-        memset(&ps.cam, 0, sizeof(ps.cam));
-        ps.f_tmin = (float)p->t_min;  // the interval exactly as init_ray rounds it
-        ps.f_tmax = p->t_max >= 3.0e38 ? INFINITY : (float)p->t_max;
-        rc = dispatch<PacketArraySource, SRT_RNG_COUNTER>(s, ps, w, nslots, p->mode, st);
-    } else {
-        rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, src, w, nslots, p->mode, st)
-                                     : dispatch<ArraySource, SRT_RNG_COUNTER>(s, src, w, nslots, p->mode, st);
+    srt_status rc = SRT_OK;
+    // More than 16 slots (counter draws): walks of <= 16 slots each, slot
+    // group g drawing samples sample0 + 16 g + k.  Slots are independent --
+    // the clip only culls entries beyond the farthest slot bound, so a slot's
+    // closest accepted hit never depends on the others -- and the groups
+    // write disjoint columns of the (R, nslots) outputs.
+    const int group = (nslots > 16 && p->rng == SRT_RNG_COUNTER) ? 16 : nslots;
+    src.ostride = nslots;
+    for (int g0 = 0; g0 < nslots && !rc; g0 += group) {
+        ArraySource gs = src;
+        gs.nslots = std::min(group, nslots - g0);
+        gs.sample0 = p->sample0 + (uint32_t)g0;
+        gs.out_t = d_t + g0;
+        gs.out_id = d_id + g0;
+        if (packets) {
+            PacketArraySource ps;
+            static_cast<ArraySource &>(ps) = gs;
+            memset(&ps.cam, 0, sizeof(ps.cam));
+            ps.f_tmin = (float)p->t_min;  // the interval exactly as init_ray rounds it
+            ps.f_tmax = p->t_max >= 3.0e38 ? INFINITY : (float)p->t_max;
+            rc = dispatch<PacketArraySource, SRT_RNG_COUNTER>(s, ps, w, gs.nslots, p->mode, st);
+        } else {
+            rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, gs, w, gs.nslots, p->mode, st)
+                                         : dispatch<ArraySource, SRT_RNG_COUNTER>(s, gs, w, gs.nslots, p->mode, st);
+        }
     }
     if (sort_mem) cudaFreeAsync(sort_mem, st);
     return rc;

@@ -157,3 +157,18 @@ def test_transmittance_routes_agree(monkeypatch):
     t1 = sc.transmittance(o, d, 0.0, TMAX, 0, S2)
     sc.close()
     np.testing.assert_allclose(t1, t0, rtol=1e-12, atol=1e-300)
+
+
+# ---- more than 16 slots (multisample up to 256, config.py:18) ---------------
+
+@pytest.mark.parametrize("kind,nslots", [("random", 40), ("camera", 33), ("camera", 256)])
+def test_trace_rays_beyond_16_slots(oracle, kind, nslots):
+    """Slot groups of <= 16 (sample0 + 16 g + k): identical to one walk of
+    all slots, since each slot's closest accepted hit is independent."""
+    a, sc = _scene(8_000, 14)
+    if kind == "random":
+        o, d = random_rays(np.random.default_rng(3), 3_000)
+    else:
+        o, d = camera_rays(96, 64) if nslots < 100 else camera_rays(32, 24)
+    _check(oracle, a, sc, o, d, 0.0, TMAX, 0, nslots)
+    sc.close()
