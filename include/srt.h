@@ -160,7 +160,9 @@ srt_status srt_bvh_download(const SrtScene *scene, float *node_lo, float *node_h
 srt_status srt_trace_rays(const SrtScene *scene, const SrtTraceParams *params,
                           const double *origins, const double *dirs, int64_t num_rays,
                           int32_t nslots, double *out_t, int64_t *out_id);
-/* Device variant: d_rays is (R, 6) f64 [ox oy oz dx dy dz]; out_t f32, out_id i32. */
+/* Device variant: d_rays is (R, 6) f64 [ox oy oz dx dy dz]; out_t f32, out_id i32.
+ * Batches of >= 4096 rays synchronise `stream` once to read a 64-ray probe
+ * (the packet / sort decision); the walk itself stays asynchronous. */
 srt_status srt_trace_rays_device(const SrtScene *scene, const SrtTraceParams *params,
                                  const double *d_rays, int64_t num_rays, int32_t nslots,
                                  float *d_out_t, int32_t *d_out_id, void *stream);
