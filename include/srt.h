@@ -22,6 +22,8 @@
  *   kernels.render_exact       kernels.py:677-723  -> srt_render_exact
  *   kernels.biased_batch       kernels.py:561-580  -> srt_biased_rays
  *   cli._biased_frame          cli.py:164-203      -> srt_render_biased
+ *   kernels.hash_position_batch kernels.py:119-122 -> srt_hash_positions
+ *   kernels.pixel_jitter_batch kernels.py:125-135  -> srt_pixel_jitter
  *   (new) multi-GPU tile gather                    -> srt_unpack_tiles_device
  */
 #ifndef SRT_H
@@ -156,7 +158,7 @@ srt_status srt_bvh_download(const SrtScene *scene, float *node_lo, float *node_h
  * whose directions share a hemisphere (camera batches, parallel jittered
  * rays) are walked as warp packets; others per lane (sorted when large).
  * The route never changes a result; env SRT_PACKET_RAYS=0/1 pins it.
- * nslots <= 256 with counter draws (slot groups of 16), <= 16 otherwise. */
+ * nslots <= 256 (walked as slot groups of <= 16). */
 srt_status srt_trace_rays(const SrtScene *scene, const SrtTraceParams *params,
                           const double *origins, const double *dirs, int64_t num_rays,
                           int32_t nslots, double *out_t, int64_t *out_id);
@@ -201,6 +203,16 @@ srt_status srt_biased_rays(const SrtScene *scene, const SrtTraceParams *params, 
  * uses the reference hash.  Host output (H,W,3) f64. */
 srt_status srt_render_biased(const SrtScene *scene, const SrtCamera *camera, const SrtRenderParams *params,
                              int32_t kk, double *out_rgb);
+
+/* ---- sampling utilities (the rest of kernels.py's public surface) -------- */
+/* kernels.hash_position_batch (kernels.py:119-122): out[i] = the trig hash of
+ * points[i] (host (n,3) f64) for `slot`, in fp64 on `device` (device sin: equal
+ * to the CPU value up to ~1e-5 after the hash's scaling). */
+srt_status srt_hash_positions(const double *points, int64_t n, int64_t slot, double *out, int32_t device);
+/* kernels.pixel_jitter_batch (kernels.py:125-135): out (n,2) f64 = the scrambled
+ * Sobol jitter of pixel (px, py) for frames[i] (host (n,) i64), integer exact. */
+srt_status srt_pixel_jitter(int64_t px, int64_t py, const int64_t *frames, int64_t n, uint32_t seed, double *out,
+                            int32_t device);
 
 /* ---- full frames (kernels.render_stochastic) ----------------------------- */
 /* Host outputs out_rgb (H,W,3) f64 and out_op (H,W) f64 = per-pixel means.
@@ -249,6 +261,13 @@ srt_status srt_resolve_frame_device(const SrtRenderParams *params, const uint64_
 srt_status srt_render_device(const SrtScene *scene, const SrtCamera *camera,
                              const SrtRenderParams *params, int32_t *d_hits, float *d_accum,
                              float *d_out, void *stream);
+/* Device error flag of the scene (traversal stack overflow), raised by any
+ * launch since the last reset.  Host-pointer entry points clear it when they
+ * start and report it when they finish; the *_device entry points never read
+ * it, so asynchronous callers check here after synchronising.  Synchronises
+ * the scene's device; returns SRT_ERR_STACK_OVERFLOW when set (clearing it if
+ * reset != 0), else SRT_OK. */
+srt_status srt_scene_check(const SrtScene *scene, int32_t reset);
 /* Traversal work counters accumulated while the environment variable
  * SRT_TRACE_STATS=1 is set: out[8] = node visits, leaf visits, screen
  * passes, exact evaluations, accepted slot updates, stack pops, culled

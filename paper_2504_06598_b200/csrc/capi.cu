@@ -143,6 +143,10 @@ srt_status check_flag(const SrtScene *s, cudaStream_t st) {
     return SRT_OK;
 }
 
+srt_status clear_flag(const SrtScene *s, cudaStream_t st) {
+    return cuda_status(cudaMemsetAsync(s->d_flag, 0, sizeof(int), st), "flag reset");
+}
+
 static srt_status validate_render(const SrtScene *s, const SrtRenderParams *p) {
     if (!s) {
         set_error("null scene");
@@ -248,7 +252,6 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
-    if (!rc) rc = cuda_status(cudaMalloc(&s->d_work, sizeof(uint32_t) * 32 * SrtScene::kWorkRing), "work counter alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 8), "stats alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 8), "stats init");
     if (!rc && n > 0) {
@@ -256,6 +259,7 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
         // memory may return before the DMA lands, and the scene's stream does
         // not synchronise with the legacy default stream
         cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
         rc = cuda_status(cudaMalloc(&s->d_means, sizeof(double) * n * 3), "means alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_cov6, sizeof(double) * n * 6), "cov alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_opac, sizeof(double) * n), "opacity alloc");
@@ -319,7 +323,6 @@ srt_status srt_scene_destroy(SrtScene *s) {
     cudaFree(s->d_geom);
     cudaFree(s->d_nodes);
     cudaFree(s->d_nodes4);
-    cudaFree(s->d_work);
     cudaFree(s->d_stats);
     cudaFree(s->d_flag);
     cudaFree(s->d_scratch);
@@ -647,6 +650,7 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     size_t ray_bytes = sizeof(double) * R * 6;
     size_t out_bytes = (sizeof(double) + sizeof(int32_t)) * R * nslots;
     size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
@@ -703,6 +707,7 @@ srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, con
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     size_t ray_bytes = sizeof(double) * R * 6;
     srt_status rc = scratch_reserve(s, 2 * ray_bytes + sizeof(double) * R);
     if (rc) return rc;
@@ -731,6 +736,7 @@ srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const doubl
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     size_t ray_bytes = sizeof(double) * R * 6;
     srt_status rc = scratch_reserve(s, 2 * ray_bytes + sizeof(double) * R * 4);
     if (rc) return rc;
@@ -758,6 +764,7 @@ srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const do
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     size_t ray_bytes = sizeof(double) * R * 6;
     size_t rgb_bytes = sizeof(double) * R * 3;
     size_t table_bytes = p->rng == SRT_RNG_TABLE ? sizeof(double) * s->n * p->table_slots : 0;
@@ -787,6 +794,7 @@ srt_status srt_render_biased(const SrtScene *sc, const SrtCamera *camera, const 
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     const int64_t npix = (int64_t)p->width * p->height;
     rc = scratch_reserve(s, sizeof(double) * npix * 3);
     if (rc) return rc;
@@ -809,6 +817,7 @@ srt_status srt_render_exact(const SrtScene *sc, const SrtCamera *camera, const S
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     const int64_t npix = (int64_t)p->width * p->height;
     rc = scratch_reserve(s, sizeof(double) * npix * 4);
     if (rc) return rc;
@@ -949,6 +958,7 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     SrtScene *s = const_cast<SrtScene *>(sc);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream;
+    if (srt_status frc = clear_flag(s, st)) return frc;  // errors belong to this call
     RenderArgs a = make_render_args(p);
     CamD cam = make_cam(camera);
     const int64_t npix = (int64_t)p->width * p->height;
@@ -1036,6 +1046,23 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
     if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "opacity download");
     if (!rc) rc = check_flag(s, st);
     return rc;
+}
+
+srt_status srt_scene_check(const SrtScene *s, int32_t reset) {
+    if (!s) {
+        set_error("null scene");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    srt_status rc = cuda_status(cudaDeviceSynchronize(), "sync");
+    int flag = 0;
+    if (!rc) rc = cuda_status(cudaMemcpy(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag read");
+    if (rc) return rc;
+    if (!flag) return SRT_OK;
+    if (reset) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag reset");
+    if (rc) return rc;
+    set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
+    return SRT_ERR_STACK_OVERFLOW;
 }
 
 srt_status srt_trace_stats(const SrtScene *s, uint64_t *out, int32_t reset) {

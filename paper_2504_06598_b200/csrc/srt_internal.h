@@ -26,7 +26,6 @@ struct SrtScene {
     int32_t num_nodes = 0;
     srt::Node4 *d_nodes4 = nullptr; // (num_nodes4,) 4-wide tree traced by the kernels
     int32_t num_nodes4 = 0;
-    uint32_t *d_work = nullptr;     // ring of kWorkRing persistent-kernel work counters (128 B apart)
     unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
     bool has_bvh = false;
@@ -36,13 +35,10 @@ struct SrtScene {
     size_t scratch_bytes = 0;
     cudaStream_t stream = nullptr;
     // Host entry points that use the scene's stream and scratch serialise on
-    // `mu` (calls on one handle serialise).  Launches on
-    // caller streams (the *_device entry points) take a fresh work counter
-    // from the ring, so concurrent streams never share one.
+    // `mu` (calls on one handle serialise).  Every persistent
+    // launch takes its own work counter from stream-ordered scratch
+    // (LaunchCounter), so launches on concurrent caller streams never share one.
     mutable std::mutex mu;
-    static constexpr uint32_t kWorkRing = 64;
-    mutable std::atomic<uint32_t> work_next{0};
-    uint32_t *next_work() const { return d_work + 32u * (work_next.fetch_add(1u) % kWorkRing); }
     srt::SceneView view() const {
         srt::SceneView v;
         v.means64 = d_means;
@@ -141,6 +137,25 @@ srt_status launch_resolve_f64(const RenderArgs &a, const float4 *d_out, double *
 srt_status launch_unpack(const float4 *d_gathered, int width, int height, int shard_count, int64_t max_tiles,
                          float4 *d_frame, cudaStream_t st);
 srt_status check_flag(const SrtScene *s, cudaStream_t st);
+srt_status clear_flag(const SrtScene *s, cudaStream_t st);
+
+// Work counter of ONE persistent-kernel launch: 128 B of stream-ordered
+// scratch (cudaMallocAsync from the device pool), zeroed on `st` and released
+// on `st` after the launch.  Launches on different streams therefore never
+// share a counter, whatever their number.
+struct LaunchCounter {
+    uint32_t *p = nullptr;
+    cudaStream_t st = nullptr;
+    srt_status init(cudaStream_t stream) {
+        st = stream;
+        srt_status rc = cuda_status(cudaMallocAsync((void **)&p, 128, st), "work counter alloc");
+        if (!rc) rc = cuda_status(cudaMemsetAsync(p, 0, 128, st), "work counter reset");
+        return rc;
+    }
+    ~LaunchCounter() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
 
 int64_t shard_tiles(int width, int height, int shard_index, int shard_count);
 

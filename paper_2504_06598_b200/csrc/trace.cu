@@ -286,6 +286,12 @@ struct CameraSource {
     // deterministic -- and the whole frame is one balanced launch.
     unsigned long long *acc64;
     uint32_t npass, unit;
+    // Slot group (multisample N > 16 walks as groups of <= 16 slots): this
+    // launch walks slots slot0 .. slot0 + gslots - 1 of the a.nslots; slot
+    // slot0 + k draws sample pass * N + slot0 + k (kernels.py:353-364 keeps
+    // every slot independent, so the split never changes a result).
+    uint32_t slot0;
+    int gslots;
     __host__ __device__ __forceinline__ uint32_t total() const { return unit * npass; }
     // Work items are packet-major: the npass consecutive 32-item packets of
     // a group walk the same 32 pixels, one pass each, so the group's nodes
@@ -308,10 +314,10 @@ struct CameraSource {
         double dx, dy, dz;
         camera_ray(cam, (uint32_t)px, (uint32_t)py, ps, a.seed, a.width, a.height, dx, dy, dz);
         init_ray(r, cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX);
-        init_slots<NS>(sl, a.nslots);
+        init_slots<NS>(sl, gslots);
         uint32_t ray_id = (uint32_t)py * (uint32_t)a.width + (uint32_t)px;
 #pragma unroll
-        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, ps * (uint32_t)a.nslots + k);
+        for (int k = 0; k < NS; ++k) sl.key[k] = walk_key(fkey, ray_id, ps * (uint32_t)a.nslots + slot0 + k);
         return true;
     }
     // fused shading (hits == nullptr): accumulate straight from the walk
@@ -321,10 +327,10 @@ struct CameraSource {
     int first, last;
     template <int NS>
     __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
-        int32_t *h = hits + (int64_t)idx * a.nslots;
+        int32_t *h = hits + (int64_t)idx * a.nslots + slot0;
 #pragma unroll
         for (int k = 0; k < NS; ++k)
-            if (k < a.nslots) h[k] = sl.id[k];
+            if (k < gslots) h[k] = sl.id[k];
     }
     // Walk result -> either the hit buffer (split trace/shade) or, fused, the
     // SH colour of every slot's hit on this ray's direction plus background
@@ -337,7 +343,7 @@ struct CameraSource {
             return;
         }
         float r = 0.f, g = 0.f, b = 0.f, o = 0.f;
-        for (int k = 0; k < NS && k < a.nslots; ++k) {
+        for (int k = 0; k < NS && k < gslots; ++k) {
             int pid = sl.id[k];
             if (pid >= 0) {
                 SRT_DCHECK(pid < s.n);
@@ -1050,14 +1056,14 @@ static srt_status launch_trace_v(const SrtScene *s, const Src &src, const WalkCf
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    uint32_t *work = s->next_work();
-    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
+    LaunchCounter work;
+    srt_status rc = work.init(st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace<NS, MODE, RNG, Src, REFILL, STATS>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace launch");
 }
 
@@ -1074,20 +1080,18 @@ static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const Wal
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    uint32_t *work = s->next_work();
-    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
+    LaunchCounter work;
+    srt_status rc = work.init(st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_coop<NS, MODE, RNG, Src, STATS>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_coop launch");
 }
 
-// Traversal policy, env SRT_TRACE_VARIANT: 2 warp-cooperative leaf
-// compaction (default), 0 per-lane walk with whole-warp refill, 1 per-lane
-// walk with refill at 8 idle lanes; SRT_TRACE_STATS=1 enables counters.
+// SRT_TRACE_STATS=1 enables the traversal counters (srt_trace_stats).
 static int env_int(const char *name, int dflt) {
     const char *e = getenv(name);
     return e ? atoi(e) : dflt;
@@ -1106,14 +1110,14 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    uint32_t *work = s->next_work();
-    srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
+    LaunchCounter work;
+    srt_status rc = work.init(st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
 }
 
@@ -1121,33 +1125,21 @@ static int env_int(const char *name, int dflt);
 
 template <int NS, int MODE, int RNG, class Src, bool STATS>
 static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
-    // SRT_PACKET_CFG (A/B experiments, N=1 mean depth; 0 = the default below,
-    // batch 48, 8 blocks/SM): 1 batch 64 unconstrained, 2 batch 32 7 blocks,
-    // 3 batch 64 8 blocks, 4 octant-ordered children, 5 batch 48 7 blocks,
-    // 6 batch 16, 9 batch 32, 10 batch 24 (7 blocks), 11 batch 64 8 blocks,
-    // 12 / 13 batch 48 at 9 / 10 blocks (56 / 48 registers: 2.03 / 2.13 ms)
+#ifdef SRT_EXPERIMENTS
+    // A/B configurations of the packet kernel, only in the experiments build
+    // (make experiments -> libsrt_exp.so, selected with SRT_LIBSRT_PATH); the
+    // release library has no environment-dependent kernel choice.
+    // SRT_PACKET_CFG (N=1 mean depth): 1 batch 64, 2 batch 32 at 7 blocks/SM,
+    // 3 batch 64 at 8, 12 / 13 batch 48 at 9 / 10 blocks/SM.
     static const int cfg = env_int("SRT_PACKET_CFG", 0);
     if constexpr (NS == 1 && MODE == 0 && !STATS && !Src::kRayOrigin) {
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
-        if (cfg == 4) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 1, 1>(s, src, w, st);
-        if (cfg == 5) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 7, 0>(s, src, w, st);
-        if (cfg == 6) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 16, 7, 0>(s, src, w, st);
-        if (cfg == 9) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7, 0>(s, src, w, st);
-        if (cfg == 10) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 24, 7, 0>(s, src, w, st);
-        if (cfg == 11) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8, 0>(s, src, w, st);
         if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9, 0>(s, src, w, st);
         if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10, 0>(s, src, w, st);
     }
-    if constexpr ((NS == 2 || NS == 4) && MODE == 0 && !STATS && !Src::kRayOrigin) {
-        if (cfg == 14) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 8, 0>(s, src, w, st);
-        if (cfg == 15) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 7, 0>(s, src, w, st);
-    }
-    if constexpr (NS >= 8 && MODE == 0 && !STATS && !Src::kRayOrigin) {
-        if (cfg == 7) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 5, 0>(s, src, w, st);
-        if (cfg == 8) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 6, 0>(s, src, w, st);
-    }
+#endif
     // 8 resident blocks/SM (64 registers, no spills) at N=1: 1.936 vs 1.964 ms
     // at 7 blocks (once the walk had a single job-flush site); 7 blocks were
     // 12% faster than the 90-register build at N=4 (3.16 vs 3.53 ms, C3)
@@ -1164,36 +1156,36 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
 template <int NS, int MODE, int RNG, class Src>
 static srt_status launch_trace_t(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
     if (src.total() == 0) return SRT_OK;
-    static const int variant = env_int("SRT_TRACE_VARIANT", 3);
     static const bool stats = env_int("SRT_TRACE_STATS", 0) != 0 && s->d_stats;
-    if constexpr (Src::kCoherent && Src::kRayOrigin) {
-        // explicit-ray packets (launch_trace_rays decides when)
-        if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
-        return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
-    } else {
-    if constexpr (Src::kCoherent) {
-        if (variant == 3) {
-            if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
-            return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
-        }
-    }
-    // incoherent explicit rays: single-slot walks are fastest per lane with
-    // refill at 8 idle lanes (142 vs 122 Mrays/s on 2M random rays in the 1M
-    // cloud); multi-slot walks gain from the cooperative leaf compaction
-    if (variant == 3 && NS == 1) {
-        if (stats) return launch_trace_v<NS, MODE, RNG, Src, 8, true>(s, src, w, st);
-        return launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st);
-    }
-    if (variant == 2 || variant == 3) {
+#ifdef SRT_EXPERIMENTS
+    // traversal policy A/B (experiments build only): 2 warp-cooperative leaf
+    // compaction for every ray source, 0 / 1 per-lane walks with refill at 32 /
+    // 8 idle lanes; 3 (default) the release policy below
+    static const int variant = env_int("SRT_TRACE_VARIANT", 3);
+    if (variant == 2) {
         if (stats) return launch_trace_coop<NS, MODE, RNG, Src, true>(s, src, w, st);
         return launch_trace_coop<NS, MODE, RNG, Src, false>(s, src, w, st);
     }
-    if (stats) {
-        if (NS == 1 && variant == 1) return launch_trace_v<NS, MODE, RNG, Src, 8, true>(s, src, w, st);
-        return launch_trace_v<NS, MODE, RNG, Src, 32, true>(s, src, w, st);
+    if (variant == 0 || variant == 1) {
+        if (stats) return variant ? launch_trace_v<NS, MODE, RNG, Src, 8, true>(s, src, w, st)
+                                  : launch_trace_v<NS, MODE, RNG, Src, 32, true>(s, src, w, st);
+        return variant ? launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st)
+                       : launch_trace_v<NS, MODE, RNG, Src, 32, false>(s, src, w, st);
     }
-    if (NS == 1 && variant == 1) return launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st);
-    return launch_trace_v<NS, MODE, RNG, Src, 32, false>(s, src, w, st);
+#endif
+    if constexpr (Src::kCoherent) {
+        // camera rays and one-hemisphere explicit batches: warp packets
+        if (stats) return launch_trace_packet<NS, MODE, RNG, Src, true>(s, src, w, st);
+        return launch_trace_packet<NS, MODE, RNG, Src, false>(s, src, w, st);
+    } else if constexpr (NS == 1) {
+        // incoherent single-slot walks are fastest per lane with refill at 8
+        // idle lanes (142 vs 122 Mrays/s on 2M random rays in the 1M cloud)
+        if (stats) return launch_trace_v<NS, MODE, RNG, Src, 8, true>(s, src, w, st);
+        return launch_trace_v<NS, MODE, RNG, Src, 8, false>(s, src, w, st);
+    } else {
+        // multi-slot incoherent walks gain from the cooperative leaf compaction
+        if (stats) return launch_trace_coop<NS, MODE, RNG, Src, true>(s, src, w, st);
+        return launch_trace_coop<NS, MODE, RNG, Src, false>(s, src, w, st);
     }
 }
 
@@ -1220,9 +1212,32 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
 
 // One pass traced AND shaded by the packet kernel (d_hits == nullptr), or
 // traced into d_hits for a separate k_shade_pass.
+// Work items of one persistent launch: the 32-bit work counter is advanced
+// by every warp once more after the last item (up to ~5k warps x 32), so a
+// launch stays far below 2^32 items and the counter can never wrap.
+constexpr uint64_t kMaxLaunchItems = 1ull << 31;
+
+// Slots per walk: multisample N > 16 runs as ceil(N / 16) walks of <= 16
+// slots over the same ray (CameraSource::slot0).
+constexpr int kSlotGroup = 16;
+
+static uint32_t frame_key_host(uint32_t seed) {
+    uint32_t x = seed ^ 0x9E3779B9u;
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
 srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                                    float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
                                    int32_t *d_hits, double *d_rgb64, double *d_op64) {
+    if ((uint64_t)a.local_tiles * 256 > kMaxLaunchItems) {
+        set_error("frame too large for one launch");
+        return SRT_ERR_INVALID_ARG;
+    }
     CameraSource src;
     src.accum = d_accum;
     src.out = d_out;
@@ -1238,18 +1253,20 @@ srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const Re
     src.pass = pass;
     src.fkey = 0;
     src.hits = d_hits;
-    // frame key computed on the host side of the device function (same mixer)
-    {
-        uint32_t x = a.seed ^ 0x9E3779B9u;
-        x ^= x >> 16;
-        x *= 0x7feb352du;
-        x ^= x >> 15;
-        x *= 0x846ca68bu;
-        x ^= x >> 16;
-        src.fkey = x;
-    }
+    src.fkey = frame_key_host(a.seed);  // frame_key() of the device code, on the host
     WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
-    return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
+    srt_status rc = SRT_OK;
+    for (int g0 = 0; g0 < a.nslots && !rc; g0 += kSlotGroup) {
+        const bool lastg = g0 + kSlotGroup >= a.nslots;
+        src.slot0 = (uint32_t)g0;
+        src.gslots = std::min(kSlotGroup, a.nslots - g0);
+        src.first = first && g0 == 0 ? 1 : 0;
+        src.last = last && lastg ? 1 : 0;
+        src.rgb64 = lastg ? d_rgb64 : nullptr;
+        src.op64 = lastg ? d_op64 : nullptr;
+        rc = dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, src.gslots, a.mode, st);
+    }
+    return rc;
 }
 
 // All `npass` passes (pass0 ...) of a frame in ONE packet launch, summed into
@@ -1263,7 +1280,7 @@ srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, con
                                          int npass, unsigned long long *d_acc64, cudaStream_t st) {
     const uint64_t unit = (uint64_t)(a.local_tiles * 256);
     if (unit == 0 || npass <= 0) return SRT_OK;
-    uint64_t limit = 0xFFFFFFFFull;  // work items per launch (32-bit work counter)
+    uint64_t limit = kMaxLaunchItems;  // work items per launch (32-bit work counter, with headroom)
     if (const char *e = getenv("SRT_MULTIPASS_MAX_ITEMS")) limit = std::min<uint64_t>(limit, strtoull(e, nullptr, 10));
     const int per = (int)std::min<uint64_t>((uint64_t)npass, limit / unit);
     if (per < 1) {
@@ -1292,15 +1309,16 @@ static srt_status launch_multipass_chunk(const SrtScene *s, const CamD &cam, con
     src.acc64 = d_acc64;
     src.unit = (uint32_t)(a.local_tiles * 256);
     src.npass = (uint32_t)npass;
-    uint32_t x = a.seed ^ 0x9E3779B9u;
-    x ^= x >> 16;
-    x *= 0x7feb352du;
-    x ^= x >> 15;
-    x *= 0x846ca68bu;
-    x ^= x >> 16;
-    src.fkey = x;
+    src.fkey = frame_key_host(a.seed);
     WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
-    return dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, a.nslots, a.mode, st);
+    // slot groups add into the same integer sums (k_resolve_fixed divides by passes * N)
+    srt_status rc = SRT_OK;
+    for (int g0 = 0; g0 < a.nslots && !rc; g0 += kSlotGroup) {
+        src.slot0 = (uint32_t)g0;
+        src.gslots = std::min(kSlotGroup, a.nslots - g0);
+        rc = dispatch<CameraSource, SRT_RNG_COUNTER>(s, src, w, src.gslots, a.mode, st);
+    }
+    return rc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1428,8 +1446,8 @@ static srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_
 
 srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int nslots,
                              const double *d_table, float *d_t, int32_t *d_id, cudaStream_t st) {
-    if (R > (int64_t)UINT32_MAX) {
-        set_error("too many rays in one call");
+    if ((uint64_t)R > kMaxLaunchItems) {
+        set_error("too many rays in one call (at most 2^31)");
         return SRT_ERR_INVALID_ARG;
     }
     ArraySource src;
@@ -1438,13 +1456,7 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     src.t_min = p->t_min;
     src.t_max = p->t_max;
     src.nslots = nslots;
-    uint32_t x = p->seed ^ 0x9E3779B9u;
-    x ^= x >> 16;
-    x *= 0x7feb352du;
-    x ^= x >> 15;
-    x *= 0x846ca68bu;
-    x ^= x >> 16;
-    src.fkey = x;
+    src.fkey = frame_key_host(p->seed);
     src.ray_id0 = p->ray_id0;
     src.sample0 = p->sample0;
     src.out_t = d_t;
@@ -1475,14 +1487,16 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     }
     WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
     srt_status rc = SRT_OK;
-    // More than 16 slots (counter draws): walks of <= 16 slots each, slot
-    // group g drawing samples sample0 + 16 g + k.  Slots are independent --
+    // More than 16 slots: walks of <= 16 slots each, slot group g drawing
+    // samples sample0 + 16 g + k (or table columns 16 g + k).  Slots are independent --
     // the clip only culls entries beyond the farthest slot bound, so a slot's
     // closest accepted hit never depends on the others -- and the groups
     // write disjoint columns of the (R, nslots) outputs.
-    const int group = (nslots > 16 && p->rng == SRT_RNG_COUNTER) ? 16 : nslots;
+    const int group = kSlotGroup;
     src.ostride = nslots;
     for (int g0 = 0; g0 < nslots && !rc; g0 += group) {
+        WalkCfg wg = w;
+        if (wg.table) wg.table += g0;  // table draws: slot g0 + k reads column g0 + k
         ArraySource gs = src;
         gs.nslots = std::min(group, nslots - g0);
         gs.sample0 = p->sample0 + (uint32_t)g0;
@@ -1494,10 +1508,10 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
             memset(&ps.cam, 0, sizeof(ps.cam));
             ps.f_tmin = (float)p->t_min;  // the interval exactly as init_ray rounds it
             ps.f_tmax = p->t_max >= 3.0e38 ? INFINITY : (float)p->t_max;
-            rc = dispatch<PacketArraySource, SRT_RNG_COUNTER>(s, ps, w, gs.nslots, p->mode, st);
+            rc = dispatch<PacketArraySource, SRT_RNG_COUNTER>(s, ps, wg, gs.nslots, p->mode, st);
         } else {
-            rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, gs, w, gs.nslots, p->mode, st)
-                                         : dispatch<ArraySource, SRT_RNG_COUNTER>(s, gs, w, gs.nslots, p->mode, st);
+            rc = p->rng == SRT_RNG_TABLE ? dispatch<ArraySource, SRT_RNG_TABLE>(s, gs, wg, gs.nslots, p->mode, st)
+                                         : dispatch<ArraySource, SRT_RNG_COUNTER>(s, gs, wg, gs.nslots, p->mode, st);
         }
     }
     if (sort_mem) cudaFreeAsync(sort_mem, st);
@@ -1678,7 +1692,7 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
     // as for srt_trace_rays); one-origin batches are already coherent: no sort
     static const int sort_min = env_int("SRT_RAY_SORT", 1) ? 65536 : INT_MAX;
     const int packet_env = env_int("SRT_PACKET_RAYS", -1);
-    const bool fits = R <= (int64_t)UINT32_MAX;
+    const bool fits = (uint64_t)R <= kMaxLaunchItems;
     bool one_origin = false, one_hemisphere = false;
     if (fits && R >= 4096) {
         srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
@@ -1703,17 +1717,17 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         }
-        uint32_t *work = s->next_work();
-        srt_status rc = cuda_status(cudaMemsetAsync(work, 0, sizeof(uint32_t), st), "work counter reset");
+        LaunchCounter work;
+        srt_status rc = work.init(st);
         int64_t need = (R + kTraceThreads - 1) / kTraceThreads;
         int64_t grid = std::min<int64_t>((int64_t)g_num_sms * blocks_per_sm, need);
         if (!rc) {
             if (mode == 0)
                 k_transmittance_packet<0><<<(unsigned)grid, kTraceThreads, 0, st>>>(
-                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work, s->d_flag);
+                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work.p, s->d_flag);
             else
                 k_transmittance_packet<1><<<(unsigned)grid, kTraceThreads, 0, st>>>(
-                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work, s->d_flag);
+                    s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work.p, s->d_flag);
             rc = cuda_status(cudaGetLastError(), "k_transmittance_packet launch");
         }
         if (sort_mem) cudaFreeAsync(sort_mem, st);

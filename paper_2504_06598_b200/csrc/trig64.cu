@@ -11,6 +11,7 @@
 // conservative boxes; slots and the far bound are fp64.
 //
 // This is a parity mode, not a throughput path: one ray per thread.
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -27,8 +28,10 @@ __device__ __forceinline__ float far32(double far) {
 }
 
 // One walk (kernels.py:312-388) with fp64 slots.
+// Slot j of the walk is slot slot0 + j of the ray (slot groups of <= 16 for
+// multisample N > 16): its draw hashes with slot index slot0 + j.
 template <int NS, int MODE>
-__device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, int nslots, double *slot_t,
+__device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, int nslots, int slot0, double *slot_t,
                      int *slot_id, int *overflow) {
     for (int k = 0; k < NS; ++k) {
         slot_t[k] = k < nslots ? INFINITY : -INFINITY;
@@ -82,7 +85,7 @@ __device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, in
             bool improved = false;
             for (int j = 0; j < NS; ++j) {
                 bool nearer = t < slot_t[j] || (t == slot_t[j] && pid < slot_id[j]);
-                if (nearer && hash_position(px, py, pz, j) < alpha) {
+                if (nearer && hash_position(px, py, pz, slot0 + j) < alpha) {
                     slot_t[j] = t;
                     slot_id[j] = pid;
                     improved = true;
@@ -103,24 +106,25 @@ __device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, in
 template <int NS, int MODE>
 __global__ void __launch_bounds__(128) k_trace_rays_trig64(SceneView s, const double *__restrict__ rays, int64_t R,
                                                            double t_min, double t_max, double s2, int clip,
-                                                           int nslots, double *out_t, int32_t *out_id,
-                                                           int *overflow) {
+                                                           int nslots, int slot0, int ostride, double *out_t,
+                                                           int32_t *out_id, int *overflow) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R) return;
     const double *q = rays + i * 6;
     t64::Ray64 r{q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max};
     double st[NS];
     int sid[NS];
-    t64::walk<NS, MODE>(s, r, s2, clip, nslots, st, sid, overflow);
+    t64::walk<NS, MODE>(s, r, s2, clip, nslots, slot0, st, sid, overflow);
     for (int k = 0; k < nslots && k < NS; ++k) {
-        out_t[i * nslots + k] = sid[k] >= 0 ? st[k] : INFINITY;
-        out_id[i * nslots + k] = sid[k];
+        out_t[i * ostride + slot0 + k] = sid[k] >= 0 ? st[k] : INFINITY;
+        out_id[i * ostride + slot0 + k] = sid[k];
     }
 }
 
 template <int NS, int MODE>
 __global__ void __launch_bounds__(128) k_trace_pass_trig64(SceneView s, CamD cam, RenderArgs a, int pass,
-                                                           double s2, int32_t *hits, int *overflow) {
+                                                           double s2, int slot0, int gslots, int32_t *hits,
+                                                           int *overflow) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= a.local_tiles * 256) return;
     int64_t lt = idx >> 8;
@@ -136,8 +140,8 @@ __global__ void __launch_bounds__(128) k_trace_pass_trig64(SceneView s, CamD cam
     t64::Ray64 r{cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX};
     double st[NS];
     int sid[NS];
-    t64::walk<NS, MODE>(s, r, s2, a.clip, a.nslots, st, sid, overflow);
-    for (int k = 0; k < a.nslots && k < NS; ++k) hits[idx * a.nslots + k] = sid[k];
+    t64::walk<NS, MODE>(s, r, s2, a.clip, gslots, slot0, st, sid, overflow);
+    for (int k = 0; k < gslots && k < NS; ++k) hits[idx * a.nslots + slot0 + k] = sid[k];
 }
 
 #define SRT_T64_NS(MACRO) \
@@ -149,11 +153,8 @@ __global__ void __launch_bounds__(128) k_trace_pass_trig64(SceneView s, CamD cam
         MACRO(4)          \
     } else if (nslots <= 8) { \
         MACRO(8)          \
-    } else if (nslots <= 16) { \
-        MACRO(16)         \
     } else {              \
-        set_error("nslots > 16 is not supported by the GPU tracer yet"); \
-        return SRT_ERR_UNSUPPORTED; \
+        MACRO(16)         \
     }
 
 srt_status launch_trace_rays_trig64(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R,
@@ -161,16 +162,23 @@ srt_status launch_trace_rays_trig64(const SrtScene *s, const SrtTraceParams *p, 
     unsigned blocks = (unsigned)((R + 127) / 128);
     if (blocks == 0) return SRT_OK;
     SceneView v = s->view();
+    const int all = nslots;
+    // slot groups of <= 16 (slots are independent; each group hashes its own slot indices)
+    for (int g0 = 0; g0 < all; g0 += 16) {
+        const int nslots = std::min(16, all - g0);
 #define SRT_L(NS)                                                                                             \
     if (p->mode == 0)                                                                                         \
         k_trace_rays_trig64<NS, 0><<<blocks, 128, 0, st>>>(v, d_rays, R, p->t_min, p->t_max, p->s2, p->clip,  \
-                                                           nslots, d_t, d_id, s->d_flag);                     \
+                                                           nslots, g0, all, d_t, d_id, s->d_flag);            \
     else                                                                                                      \
         k_trace_rays_trig64<NS, 1><<<blocks, 128, 0, st>>>(v, d_rays, R, p->t_min, p->t_max, p->s2, p->clip,  \
-                                                           nslots, d_t, d_id, s->d_flag);
-    SRT_T64_NS(SRT_L)
+                                                           nslots, g0, all, d_t, d_id, s->d_flag);
+        SRT_T64_NS(SRT_L)
 #undef SRT_L
-    return cuda_status(cudaGetLastError(), "k_trace_rays_trig64 launch");
+        srt_status rc = cuda_status(cudaGetLastError(), "k_trace_rays_trig64 launch");
+        if (rc) return rc;
+    }
+    return SRT_OK;
 }
 
 srt_status launch_trace_pass_trig64(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass, double s2,
@@ -179,15 +187,19 @@ srt_status launch_trace_pass_trig64(const SrtScene *s, const CamD &cam, const Re
     unsigned blocks = (unsigned)((n + 127) / 128);
     if (blocks == 0) return SRT_OK;
     SceneView v = s->view();
-    const int nslots = a.nslots;
-#define SRT_L(NS)                                                                                          \
-    if (a.mode == 0)                                                                                       \
-        k_trace_pass_trig64<NS, 0><<<blocks, 128, 0, st>>>(v, cam, a, pass, s2, d_hits, s->d_flag);       \
-    else                                                                                                   \
-        k_trace_pass_trig64<NS, 1><<<blocks, 128, 0, st>>>(v, cam, a, pass, s2, d_hits, s->d_flag);
-    SRT_T64_NS(SRT_L)
+    for (int g0 = 0; g0 < a.nslots; g0 += 16) {
+        const int nslots = std::min(16, a.nslots - g0);
+#define SRT_L(NS)                                                                                             \
+    if (a.mode == 0)                                                                                          \
+        k_trace_pass_trig64<NS, 0><<<blocks, 128, 0, st>>>(v, cam, a, pass, s2, g0, nslots, d_hits, s->d_flag); \
+    else                                                                                                      \
+        k_trace_pass_trig64<NS, 1><<<blocks, 128, 0, st>>>(v, cam, a, pass, s2, g0, nslots, d_hits, s->d_flag);
+        SRT_T64_NS(SRT_L)
 #undef SRT_L
-    return cuda_status(cudaGetLastError(), "k_trace_pass_trig64 launch");
+        srt_status rc = cuda_status(cudaGetLastError(), "k_trace_pass_trig64 launch");
+        if (rc) return rc;
+    }
+    return SRT_OK;
 }
 
 }  // namespace srt

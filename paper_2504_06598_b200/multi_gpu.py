@@ -315,6 +315,8 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
         frame = render_frame_sums(p, gpu_shard_sums(sc, ct, settings, device), settings.multisample, group)
     else:
         frame = render_frame(p, gpu_shard_renderer(sc, ct, settings, device), group)
+    torch.cuda.current_stream(torch.device("cuda", device)).synchronize()
+    sc.check_status()  # a stack overflow in this rank's launch raises here, not silently
     if frame is None:
         return None
     if frame.is_cuda:
@@ -354,9 +356,10 @@ def render_devices(asset, camera, settings, devices, rng: str = "counter"):
     mode = 0 if settings.depth_mode == "mean" else 1
     d0 = torch.device("cuda", devices[0])
     fixed = rng == "counter" and settings.passes > 1  # srt_render's multi-pass path
-    prms, bufs = [], []
+    prms, bufs, scenes = [], [], []
     for i, d in enumerate(devices):
         sc = prepare(asset, settings, device=d)
+        scenes.append(sc)
         dev = torch.device("cuda", d)
         prm = make_render_params(W, H, settings.passes, settings.multisample, mode, settings.cutoff_s ** 2, True,
                                  settings.seed, settings.background, 0, i, G, rng=rng)
@@ -375,6 +378,8 @@ def render_devices(asset, camera, settings, devices, rng: str = "counter"):
         prms.append(prm)
     for d in set(devices):
         torch.cuda.current_stream(torch.device("cuda", d)).synchronize()
+    for sc in scenes:
+        sc.check_status()
     s0 = torch.cuda.current_stream(d0).cuda_stream
     if fixed:
         rgb = torch.zeros((H, W, 3), dtype=torch.float64, device=d0)

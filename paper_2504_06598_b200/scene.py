@@ -32,6 +32,16 @@ def _ci64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.int64)
 
 
+def _rays(origins, dirs):
+    """(R,3) f64 origin and direction arrays with matching row counts (the
+    C ABI copies 24 R bytes from each)."""
+    o = _c64(origins)
+    d = _c64(dirs)
+    if o.ndim != 2 or o.shape[1] != 3 or d.shape != o.shape:
+        raise ValueError(f"origins and directions must both be (R, 3); got {o.shape} and {d.shape}")
+    return o, d
+
+
 def make_camera(cam) -> SrtCamera:
     """SrtCamera from the 14 scalars (ex..ez, rx..rz, ux..uz, fx..fz, half_w, half_h)
     of render.py:144-150."""
@@ -181,8 +191,7 @@ class DeviceScene:
         rng: "counter" (default), "table" (explicit uniforms) or "trig64" (the
         reference's own fp64 trig-hash draw, parity mode).
         Returns (out_t (R,N) f64, +inf on miss; out_id (R,N) i64, -1 on miss)."""
-        o = _c64(origins).reshape(-1, 3)
-        d = _c64(dirs).reshape(-1, 3)
+        o, d = _rays(origins, dirs)
         R = o.shape[0]
         p = SrtTraceParams()
         p.t_min, p.t_max, p.mode, p.clip, p.s2 = float(t_min), float(t_max), int(mode), int(bool(clip)), float(s2)
@@ -214,8 +223,7 @@ class DeviceScene:
                                                 ctypes.c_void_p(stream)))
 
     def transmittance(self, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0) -> np.ndarray:
-        o = _c64(origins).reshape(-1, 3)
-        d = _c64(dirs).reshape(-1, 3)
+        o, d = _rays(origins, dirs)
         out = np.empty(o.shape[0])
         check(_lib.load().srt_transmittance_rays(self.handle, _ptr(o), _ptr(d), o.shape[0], float(t_min),
                                                  float(t_max), int(mode), float(s2), _ptr(out)))
@@ -224,8 +232,7 @@ class DeviceScene:
     def exact_rays(self, origins, dirs, t_min=0.0, t_max=TMAX, mode=0, s2=8.0, background=(0.0, 0.0, 0.0)):
         """kernels.exact_batch semantics (kernels.py:584-604): sorted compositing
         of every valid candidate.  Returns (rgb (R,3) f64, opacity (R,) f64)."""
-        o = _c64(origins).reshape(-1, 3)
-        d = _c64(dirs).reshape(-1, 3)
+        o, d = _rays(origins, dirs)
         bg = _c64(background).reshape(3)
         rgb = np.empty((o.shape[0], 3))
         op = np.empty(o.shape[0])
@@ -240,8 +247,7 @@ class DeviceScene:
         nearest accepted composited with their own alphas.  Returns rgb (R,3)."""
         if int(kk) < 1:
             raise ValueError(f"k must be >= 1, got {kk}")
-        o = _c64(origins).reshape(-1, 3)
-        d = _c64(dirs).reshape(-1, 3)
+        o, d = _rays(origins, dirs)
         bg = _c64(background).reshape(3)
         p = SrtTraceParams()
         p.t_min, p.t_max, p.mode, p.clip, p.s2 = float(t_min), float(t_max), int(mode), 0, float(s2)
@@ -295,6 +301,12 @@ class DeviceScene:
         check(_lib.load().srt_render(self.handle, ctypes.byref(camera), ctypes.byref(prm), _ptr(rgb), _ptr(op),
                                      _ptr(ids)))
         return rgb, op, ids
+
+    def check_status(self, reset: bool = True) -> None:
+        """Raise if any launch on this scene overflowed its traversal stack
+        since the last reset (srt_scene_check; the *_device entry points do
+        not report it themselves)."""
+        check(_lib.load().srt_scene_check(self.handle, int(bool(reset))))
 
     def trace_stats(self, reset: bool = True) -> dict:
         """Traversal counters (collected only when SRT_TRACE_STATS=1 was set)."""

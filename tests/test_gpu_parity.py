@@ -79,13 +79,18 @@ def test_c1_render_vs_oracle(oracle):
 
 def test_c2_render_vs_oracle(oracle):
     """C2: 100k SH3 density-preserving, 512x512, 16 spp (configs[1]); pass-0
-    ids on every pixel, 16-pass means compared on a 4x4-strided sample."""
+    ids and the 16-sample means of every pixel of a 2x2-strided grid (65,536
+    pixels): each pixel's mean colour within 1e-4 relative of the oracle's
+    (the north-star colour gate, per pixel) on >= 99.9% of pixels."""
     from paper_2504_06598_b200.synthetic import density_cloud
 
     asset = density_cloud(100_000)
-    (rgb, op, ids), ref = _render_both(oracle, asset, 512, 512, spp=16, stride=(4, 4))
-    sub = (slice(None, None, 4), slice(None, None, 4))
+    (rgb, op, ids), ref = _render_both(oracle, asset, 512, 512, spp=16, stride=(2, 2))
+    sub = (slice(None, None, 2), slice(None, None, 2))
     assert np.mean(ids[sub] == ref["ids"][sub]) >= ID_AGREE
+    ok = np.all(np.abs(rgb[sub] - ref["rgb"][sub]) <= COLOUR_RTOL * np.abs(ref["rgb"][sub]) + COLOUR_ATOL, axis=2)
+    ok &= np.abs(op[sub] - ref["opacity"][sub]) <= 1e-12
+    assert ok.mean() >= ID_AGREE, ok.mean()
     from paper_2504_06598_b200 import AccumBuffer, image_metrics
 
     m = image_metrics(AccumBuffer(rgb[sub], op[sub], 16), AccumBuffer(ref["rgb"][sub], ref["opacity"][sub], 16))
@@ -121,7 +126,7 @@ def test_center_mode_and_background(oracle):
 
     (rgb, op, ids), ref = _render_both(oracle, anisotropic_sheets(200, seed=3), 48, 40, mode=1, bg=(0.2, 0.4, 0.6))
     agree = ids == ref["ids"]
-    assert agree.mean() >= 0.995
+    assert agree.mean() >= ID_AGREE, agree.mean()
     _check_colours(rgb, ref["rgb"], np.all(agree, axis=2))
 
 
@@ -186,7 +191,7 @@ def test_render_stochastic_shim(oracle):
     ref = oracle.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, 2, np.array(ct), 20, 16, s2=S2, rng="counter",
                         want_ids=True)
     same = np.abs(op - ref["opacity"]) == 0
-    assert same.mean() >= 0.99
+    assert same.mean() >= 0.999
     _check_colours(rgb, ref["rgb"], same)
 
 

@@ -63,7 +63,7 @@ def test_multislot_sh3_frame_matches_reference(golden):
 
     g = golden("render_c1")
     got = _render(random_cloud(10_000, seed=0, sh_degree=3), 48, 40, 8, nslots=2, seed=7, bg=(0.05, 0.1, 0.2))
-    assert _pixel_agreement(got, g["rgb_ms"], g["opacity_ms"]) >= 0.995
+    assert _pixel_agreement(got, g["rgb_ms"], g["opacity_ms"]) >= 0.999
 
 
 def test_small_frames_match_reference(golden):
@@ -71,9 +71,9 @@ def test_small_frames_match_reference(golden):
 
     g = golden("render_small")
     got = _render(random_cloud(300, seed=53, sh_degree=3), 24, 20, 6, nslots=2, seed=5, bg=(0.1, 0.2, 0.3))
-    assert _pixel_agreement(got, g["rgb"], g["opacity"]) >= 0.99
+    assert _pixel_agreement(got, g["rgb"], g["opacity"]) >= 0.999
     got2 = _render(anisotropic_sheets(60, seed=3), 16, 12, 3, seed=11, mode="center")
-    assert _pixel_agreement(got2, g["rgb_center"], g["opacity_center"]) >= 0.99
+    assert _pixel_agreement(got2, g["rgb_center"], g["opacity_center"]) >= 0.999
 
 
 @pytest.mark.parametrize("mode", [0, 1])
@@ -93,7 +93,7 @@ def test_biased_batch_matches_reference(golden, mode, kk):
     rgb = sc.biased_rays(t["origins"], t["dirs"], kk, 0.0, TMAX, mode, S2, (0.15, 0.25, 0.35), rng="trig64")
     sc.close()
     ok = np.all(np.abs(rgb - g[f"rgb_m{mode}_k{kk}"]) <= 1e-5, axis=1)
-    assert ok.mean() >= 0.995
+    assert ok.mean() >= 0.999
 
 
 @pytest.mark.parametrize("kk", [1, 3])
@@ -108,7 +108,7 @@ def test_biased_frame_matches_reference_cli(golden, kk):
     st = RenderSettings(width=20, height=16, spp=2, seed=5, background=[0.15, 0.25, 0.35])
     rgb = render_biased(a, front_camera(), st, kk, rng="trig64")
     ok = np.all(np.abs(rgb - g[f"frame_k{kk}"]) <= 1e-5, axis=2)
-    assert ok.mean() >= 0.99
+    assert ok.mean() >= 0.999
 
 
 def test_c3target_scale_matches_unmodified_reference(golden):
@@ -126,11 +126,11 @@ def test_c3target_scale_matches_unmodified_reference(golden):
     sc = prepare(a, st)
     t, ids = sc.trace_rays(g["origins"], g["dirs"], 0.0, TMAX, 0, S2, True, 1, rng="trig64")
     agree = ids[:, 0] == g["id"][:, 0]
-    assert agree.mean() >= 0.995, agree.mean()
+    assert agree.mean() >= 0.999, agree.mean()  # north-star id gate
     hit = agree & (g["id"][:, 0] >= 0)
     np.testing.assert_array_equal(t[hit, 0], g["t"][hit, 0])  # fp64 depths, bit for bit
     buf = render(a, front_camera(), st, rng="trig64")
     got = buf.rgb[g["py"], g["px"]]
     ok = np.all(np.abs(got - g["rgb"]) <= 1e-4 * np.abs(g["rgb"]) + 1e-6, axis=1)
-    assert ok.mean() >= 0.99, ok.mean()
-    assert np.mean(buf.opacity[g["py"], g["px"]] == g["opacity"]) >= 0.99
+    assert ok.mean() >= 0.999, ok.mean()
+    assert np.mean(buf.opacity[g["py"], g["px"]] == g["opacity"]) >= 0.999
