@@ -4,21 +4,27 @@ BASELINE.md section 3), on N B200s, beside the reference CPU renderer.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun (one rank per GPU, NCCL): each rank traces the
-16x16 tiles t with t % N == rank, and the tile-compact shards are gathered to
-rank 0 with one NCCL gather per frame and unpacked there.
+N > 1: one process per GPU.  Under torchrun (RANK / WORLD_SIZE set) each rank
+is one GPU; without it ``bench.py --gpus N`` re-launches itself under
+``torch.distributed.run`` on 127.0.0.1.  Each rank traces the 16x16 tiles
+t with t % N == rank (fused walk + SH shade), the tile-compact shards are
+gathered to rank 0 with one NCCL gather per frame and unpacked there.
 
 One JSON line on rank 0.  "value" = whole-job Mrays/s with the scene resident
 in HBM, timed on the device with CUDA events (max over ranks).  "e2e" = the
-same metric through the public render() API (libsrt host-pointer entry
-point) with the fp64 AccumBuffer copied back to the host every step.
+same metric through the public render() API with the f64 AccumBuffer landing
+in host memory every step (N > 1: every GPU writes its tiles into one shared
+mapped host frame).  ``--impl reference`` times the reference algorithm on
+the host cores (the oracle's trig-hash restatement, bitwise the reference).
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,13 +38,18 @@ sys.path.insert(0, str(ROOT))
 
 WIDTH, HEIGHT, N_PRIMS, SH_DEG, SPP, NSLOTS = 1920, 1080, 1_000_000, 3, 1, 1
 WORKLOAD = "C3-target: density_cloud(1M, SH3, seed 0), 1920x1080, 1 spp, N=1, front_camera, mean depth"
+L2_FLUSH_BYTES = 256 << 20
+# The one config both arms report (the driver compares them)
+CONFIG = {"workload": WORKLOAD, "width": WIDTH, "height": HEIGHT, "n_gaussians": N_PRIMS, "spp": SPP,
+          "nslots": NSLOTS, "sh_degree": SH_DEG,
+          "l2": "GPU arm: 256 MiB flush written between timed frames, outside the per-frame CUDA events"}
 # Algorithmic bytes per walk: B = 64 I + 24 P + 48 C + S hits + 16/passes with the
 # per-walk counts of the reference SAH BVH on this scene:
 # I = 150.5, P = 167.3, C = 82.4, hits = 0.68, S = 192 B (SH degree 3).
 YARD_I, YARD_P, YARD_C, YARD_HITS, SH_BYTES = 150.5, 167.3, 82.4, 0.68, 192
 BYTES_PER_WALK = 64 * YARD_I + 24 * YARD_P + 48 * YARD_C + SH_BYTES * YARD_HITS + 16 / SPP
-L2_FLUSH_BYTES = 256 << 20
 PROFILE_SUMMARY = ROOT / "profiles" / "ncu_summary.json"
+SEEDS = (0, 1, 2)
 
 
 def _peaks() -> tuple[float, str]:
@@ -51,36 +62,61 @@ def _peaks() -> tuple[float, str]:
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def _traffic_per_launch():
-    if PROFILE_SUMMARY.exists():
-        try:
-            d = json.loads(PROFILE_SUMMARY.read_text())
-            return d.get("trace_dram_bytes_per_launch")
-        except Exception:
-            return None
-    return None
-
-
-def _issue_roofline(kernel_ms: float, clocks):
-    """Issue-slot roofline of the dominant kernel: the walk is bound by SM
-    instruction issue, not bytes.  achieved = warp instructions
-    per launch (ncu, profiles/ncu_summary.json) / the live kernel time; peak =
-    1 warp instruction per cycle per SM sub-partition (148 SMs x 4) at the SM
-    clock sampled during the timed region."""
+def _ncu_profile(build_id: str) -> dict:
+    """The committed ncu capture of the dominant kernel (profiles/ncu_summary.json),
+    with whether it was taken on this very build (source hash, srt_build_id)."""
     try:
         d = json.loads(PROFILE_SUMMARY.read_text())
-        inst = float(d["warp_inst_per_launch"])
     except Exception:
-        return None
+        return {}
+    d["same_build"] = d.get("build_id") == build_id
+    return d
+
+
+def _roofline(kernel_ms: float, walks: float, prof: dict, l2_peak: float | None, clocks) -> tuple[dict, dict]:
+    """Algorithmic roofline (the contract's) plus the physical traffic and issue
+    fractions that explain it."""
     import torch
 
-    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
-    peak = sms * 4 * mhz * 1e6 / 1e9  # G warp-instructions / s
-    achieved = inst / (kernel_ms * 1e-3) / 1e9
-    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "G warp-inst/s", "frac": achieved / peak,
-            "warp_inst_per_launch": inst, "ncu_issue_active_pct": d.get("issue_active_pct"),
-            "source": "warp instructions from profiles/ncu_summary.json, kernel time live"}
+    peak, peak_src = _peaks()
+    alg = BYTES_PER_WALK * walks
+    achieved = alg / (kernel_ms * 1e-3) / 1e9
+    dram = prof.get("dram_bytes_per_launch")
+    l2 = prof.get("l2_bytes_per_launch")
+    scale = walks / prof["walks_per_launch"] if prof.get("walks_per_launch") else 1.0
+    physical = {
+        "source": prof.get("source"), "ncu_build_id": prof.get("build_id"), "same_build": prof.get("same_build"),
+        "dram_bytes_per_launch": dram * scale if dram else None,
+        "l2_bytes_per_launch": l2 * scale if l2 else None,
+    }
+    if dram:
+        physical["dram_gbs"] = dram * scale / (kernel_ms * 1e-3) / 1e9
+        physical["dram_frac_of_hbm_peak"] = physical["dram_gbs"] / peak
+    if l2:
+        physical["l2_gbs"] = l2 * scale / (kernel_ms * 1e-3) / 1e9
+        if l2_peak:
+            physical["l2_peak_gbs"] = l2_peak
+            physical["l2_frac_of_l2_peak"] = physical["l2_gbs"] / l2_peak
+            physical["l2_peak_source"] = "srt_probe_l2_bandwidth: 32 MB L2-resident buffer, ld.global.cg, live"
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": dram * scale if dram else None,
+            "kernel": "k_trace_packet (fused walk + SH shade + accumulate)", "kernel_ms": kernel_ms,
+            "algorithmic_bytes_per_walk": BYTES_PER_WALK, "walks_per_launch": walks, "peak_source": peak_src,
+            "note": "algorithmic bytes count node/record reads that packets serve from L1/L2, so frac > 1; "
+                    "'physical' holds the DRAM and L2 bytes ncu measured for the launch",
+            "physical": physical}
+    issue = None
+    if prof.get("warp_inst_per_launch"):
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        mhz = (clocks or {}).get("sm_mhz") or (clocks or {}).get("sm_max_mhz") or 1965.0
+        ipeak = sms * 4 * mhz * 1e6 / 1e9  # one warp instruction per cycle per SM sub-partition
+        inst = prof["warp_inst_per_launch"] * scale
+        ach = inst / (kernel_ms * 1e-3) / 1e9
+        issue = {"bound": "issue", "achieved": ach, "peak": ipeak, "unit": "G warp-inst/s", "frac": ach / ipeak,
+                 "warp_inst_per_launch": inst, "ncu_issue_active_pct": prof.get("issue_active_pct"),
+                 "same_build": prof.get("same_build"),
+                 "source": "warp instructions of the committed ncu capture, kernel time live"}
+    return roof, issue
 
 
 class ClockSampler:
@@ -128,16 +164,19 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+# ---------------------------------------------------------------------------
+# the reference algorithm on host cores (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------
 _CPU_BVH = {}
 
 
-def _cpu_baseline_sample(asset, threads: int, stride=(2, 2)) -> dict:
-    """The reference algorithm (oracle C restatement, trig hash: bitwise equal to
-    splatray.kernels.render_stochastic) on host cores, over every stride-th
-    pixel of the same frame, prebuilt SAH BVH; returns rays, seconds."""
+def _cpu_frame(asset, threads: int) -> dict:
+    """One full frame of the reference algorithm on host cores: the oracle's C
+    restatement in trig-hash mode (bitwise equal to splatray.kernels.render_stochastic,
+    tests/test_oracle_golden.py) over every pixel, prebuilt SAH BVH."""
     from oracle import oracle as O
-    from paper_2504_06598_b200.synthetic import front_camera
     from paper_2504_06598_b200.scene import camera_tuple
+    from paper_2504_06598_b200.synthetic import front_camera
 
     O.build()
     pk = asset.packed
@@ -149,46 +188,127 @@ def _cpu_baseline_sample(asset, threads: int, stride=(2, 2)) -> dict:
     ct = np.array(camera_tuple(front_camera(), WIDTH, HEIGHT))
     t0 = time.perf_counter()
     O.render(b, pk.means, pk.cov_inv6, pk.opacities, pk.sh, SH_DEG, ct, WIDTH, HEIGHT, passes=SPP, nslots=NSLOTS,
-             s2=8.0, seed=0, rng="trig", stride=stride, threads=threads)
-    secs = time.perf_counter() - t0
-    rays = len(range(0, WIDTH, stride[0])) * len(range(0, HEIGHT, stride[1])) * SPP
-    return {"rays": rays, "seconds": secs, "bvh_build_s": build_s}
+             s2=8.0, seed=0, rng="trig", threads=threads)
+    return {"rays": WIDTH * HEIGHT * SPP, "seconds": time.perf_counter() - t0, "bvh_build_s": build_s}
+
+
+CPU_NOTE = ("oracle/srt_oracle.c in trig-hash mode: the reference's render_stochastic (kernels.py:622-673) "
+            "restated in C, bitwise equal to the unmodified reference on every golden fixture "
+            "(tests/test_oracle_golden.py); OpenMP over 16x16 tiles")
 
 
 def run_reference(args) -> None:
-    """--impl reference: the reference's CPU renderer on the box's host cores."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """--impl reference: the reference's CPU renderer on the box's host cores,
+    the FULL 1920x1080 frame every step (same config as our arm)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     from paper_2504_06598_b200.synthetic import density_cloud
 
     threads = os.cpu_count() or 1
     asset = density_cloud(N_PRIMS, seed=0, sh_degree=SH_DEG)
-    stride = (4, 4)
     for _ in range(args.warmup):
-        _cpu_baseline_sample(asset, threads, stride)
-    times = []
-    for _ in range(args.steps):
-        r = _cpu_baseline_sample(asset, threads, stride)
-        times.append(r["seconds"])
-    rays = r["rays"]
-    mrays = rays / statistics.mean(times) / 1e6
-    frame_ms = WIDTH * HEIGHT * SPP / (mrays * 1e6) * 1e3
-    sample = f"every 4th pixel in x and y of the 1920x1080 frame ({rays} rays/step), prebuilt SAH BVH"
+        _cpu_frame(asset, threads)
+    times = [_cpu_frame(asset, threads)["seconds"] for _ in range(args.steps)]
+    ms = statistics.mean(times) * 1e3
+    mrays = WIDTH * HEIGHT * SPP / (ms * 1e-3) / 1e6
     line = {
         "impl": "reference", "metric": "Mrays/s", "value": mrays, "unit": "Mrays/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": frame_ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "width": WIDTH, "height": HEIGHT, "n_gaussians": N_PRIMS, "spp": SPP,
-                   "sh_degree": SH_DEG, "ms_per_step_is": "extrapolated full-frame ms"},
-        "cpu_baseline": {"value": mrays, "unit": "Mrays/s", "cores": threads, "kind": "port", "sample": sample,
-                         "note": "oracle/srt_oracle.c in trig-hash mode, bitwise equal to the reference's numba "
-                                 "render_stochastic (tests/test_oracle_golden.py); OpenMP over 16x16 tiles"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": dict(CONFIG),
+        "cpu_baseline": {"value": mrays, "unit": "Mrays/s", "cores": threads, "kind": "port",
+                         "sample": f"the full {WIDTH}x{HEIGHT} frame every step ({WIDTH * HEIGHT} rays), "
+                                   f"prebuilt SAH BVH", "note": CPU_NOTE},
         "e2e": {"value": mrays, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# self-launch for N > 1
+# ---------------------------------------------------------------------------
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without torchrun: re-run under torch.distributed.run,
+    one rank per GPU on this node (rank 0 prints the JSON line)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------
+# CPU self-test of the multi-rank plumbing (gloo): launcher, per-rank timing,
+# max-over-ranks, the gather + unpack and the shared host frame
+# ---------------------------------------------------------------------------
+def run_selftest(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_06598_b200 import multi_gpu as mg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist.init_process_group("gloo")
+    W, H = 200, 120
+    p = mg.plan("tiles", rank, world, W, H, 1)
+    px, py, ok = mg.compact_pixels(W, H, rank, world)
+    n = mg.max_shard_tiles(W, H, world) * 256
+
+    def shard(_):  # stands in for the per-rank kernel: tile-compact (r, g, b, a) = (px, py, rank, 1)
+        buf = torch.zeros((n, 4))
+        buf[: px.shape[0]][torch.from_numpy(ok)] = torch.from_numpy(
+            np.stack([px[ok], py[ok], np.full(ok.sum(), rank), np.ones(ok.sum())], 1).astype(np.float32))
+        return buf
+
+    times = []
+    for _ in range(args.warmup + args.steps):
+        dist.barrier()
+        t0 = time.perf_counter()
+        frame = mg.render_frame(p, shard)
+        times.append(time.perf_counter() - t0)
+    local = torch.tensor([statistics.mean(times[args.warmup:]) * 1e3])
+    dist.all_reduce(local, op=dist.ReduceOp.MAX)
+    good = True
+    if rank == 0:
+        f = frame.numpy()
+        yy, xx = np.mgrid[0:H, 0:W]
+        good &= bool(np.array_equal(f[..., 0], xx) and np.array_equal(f[..., 1], yy))
+        tiles = (yy // 16) * ((W + 15) // 16) + xx // 16
+        good &= bool(np.array_equal(f[..., 2], tiles % world))
+    pool = mg.SharedFramePool(register=False)
+
+    def write(pl, rgb, op):
+        rgb[py[ok], px[ok], 0] = pl.rank
+        op[py[ok], px[ok]] = 1.0
+
+    got = mg.render_frame_shared(p, write, pool)
+    if rank == 0:
+        good &= bool(np.all(got[1] == 1.0))
+        del got
+    dist.barrier()
+    pool.close()
+    if rank == 0:
+        print(json.dumps({"selftest": "ok" if good else "FAILED", "backend": "gloo", "n_ranks": world,
+                          "ms_per_step": float(local.item()), "steps": args.steps, "warmup": args.warmup}),
+              flush=True)
+    dist.destroy_process_group()
+    if not good:
+        raise SystemExit(1)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
 def run_ours(args) -> None:
     import torch
     import torch.distributed as dist
@@ -200,118 +320,126 @@ def run_ours(args) -> None:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size visible in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200 import RenderSettings, _lib, front_camera, render
     from paper_2504_06598_b200.render import prepare
     from paper_2504_06598_b200.scene import camera_tuple, make_camera, make_render_params, shard_tiles, \
         unpack_tiles_device
     from paper_2504_06598_b200.synthetic import density_cloud
 
-    asset = density_cloud(N_PRIMS, seed=0, sh_degree=SH_DEG)
+    L = _lib.load()
+    build_id = L.srt_build_id().decode()
     st = RenderSettings(width=WIDTH, height=HEIGHT, spp=SPP, multisample=NSLOTS)
-    t0 = time.perf_counter()
-    sc = prepare(asset, st, device=local)
-    setup_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    sc.build_bvh(st.cutoff_s)
-    lbvh_s = time.perf_counter() - t0
     cam = make_camera(camera_tuple(front_camera(), WIDTH, HEIGHT))
     prm = make_render_params(WIDTH, HEIGHT, st.passes, NSLOTS, 0, st.cutoff_s ** 2, shard_index=rank,
                              shard_count=world)
     dev = torch.device("cuda", local)
     tiles = shard_tiles(WIDTH, HEIGHT, rank, world)
     max_tiles = shard_tiles(WIDTH, HEIGHT, 0, world)
-    hits = torch.empty(max_tiles * 256 * NSLOTS, dtype=torch.int32, device=dev)
     acc = torch.empty(max_tiles * 256 * 4, dtype=torch.float32, device=dev)
     out = torch.zeros(max_tiles * 256 * 4, dtype=torch.float32, device=dev)
     frame = torch.zeros(WIDTH * HEIGHT * 4, dtype=torch.float32, device=dev) if (world > 1 and rank == 0) else None
-    gathered = [torch.empty_like(out) for _ in range(world)] if (world > 1 and rank == 0) else None
+    gathered = torch.empty(world * max_tiles * 256 * 4, dtype=torch.float32, device=dev) \
+        if (world > 1 and rank == 0) else None
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
-    def step(ev=None):
+    def scene_for(seed):
+        asset = density_cloud(N_PRIMS, seed=seed, sh_degree=SH_DEG)
+        t0 = time.perf_counter()
+        sc = prepare(asset, st, device=local)
+        setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        sc.build_bvh(st.cutoff_s)
+        return asset, sc, setup, time.perf_counter() - t0
+
+    asset, sc, setup_s, build_s = scene_for(0)
+
+    def step(scene, ev=None):
         if ev is not None:
             ev[0].record(stream)
         for f in range(st.passes):
             # one fused kernel per pass: packet walk + SH shade + accumulate
-            sc.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), sp)
+            scene.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), sp)
         if ev is not None:
             ev[1].record(stream)
         if world > 1:
-            dist.gather(out, gathered if rank == 0 else None, dst=0)
+            dist.gather(out, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
+            if ev is not None:
+                ev[2].record(stream)
             if rank == 0:
-                packed = torch.cat(gathered)
-                unpack_tiles_device(packed.data_ptr(), WIDTH, HEIGHT, world, max_tiles, frame.data_ptr(), sp)
+                unpack_tiles_device(gathered.data_ptr(), WIDTH, HEIGHT, world, max_tiles, frame.data_ptr(), sp)
         if ev is not None:
-            ev[2].record(stream)
+            ev[3].record(stream)
 
-    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    with sampler:
+    def timed(scene, steps):
+        events = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
         for _ in range(max(args.warmup, 0)):
-            step()
+            step(scene)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        wall0 = time.perf_counter()
-        for i in range(args.steps):
+        for i in range(steps):
             flush.fill_(i & 0xFF)  # evict the scene from L2 between steps (outside the step events)
-            step(events[i])
+            step(scene, events[i])
         torch.cuda.synchronize(dev)
+        walk = [e[0].elapsed_time(e[1]) for e in events]
+        total = [e[0].elapsed_time(e[3]) for e in events]
+        gather = [e[1].elapsed_time(e[2]) for e in events] if world > 1 else [0.0] * steps
+        unpack = [e[2].elapsed_time(e[3]) for e in events] if world > 1 else [0.0] * steps
+        return walk, gather, unpack, total
+
+    sampler = ClockSampler(local)
+    with sampler:
+        wall0 = time.perf_counter()
+        walk, gather, unpack, total = timed(sc, args.steps)
         wall = time.perf_counter() - wall0
         time.sleep(0.25)  # let the sampler record the tail of the timed region
+    sc.check_status()  # a traversal stack overflow in any timed launch raises here
+    mine = [statistics.mean(total), statistics.mean(walk), statistics.mean(gather), statistics.mean(unpack),
+            float(tiles)]
     if world > 1:
-        dist.barrier()
-    step_ms = [e[0].elapsed_time(e[2]) for e in events]
-    trace_ms = [e[0].elapsed_time(e[1]) for e in events]
-    local_ms = float(sum(step_ms))
-    if world > 1:
-        tt = torch.tensor([local_ms, float(sum(trace_ms))], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, trace_total = tt.tolist()
+        t = torch.tensor(mine, device=dev, dtype=torch.float64)
+        allr = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        per_rank = [r.tolist() for r in allr]
     else:
-        total_ms, trace_total = local_ms, float(sum(trace_ms))
-    ms_per_step = total_ms / args.steps
+        per_rank = [mine]
+    ms_per_step = max(r[0] for r in per_rank)  # the slowest rank's frame
     rays_per_frame = WIDTH * HEIGHT * SPP
     value = rays_per_frame / (ms_per_step * 1e-3) / 1e6
+    kernel_ms = statistics.mean(walk) / st.passes
+    walks = min(tiles * 256, WIDTH * HEIGHT) if world > 1 else WIDTH * HEIGHT
 
-    # roofline of the dominant kernel (k_trace_pass) on rank 0's stream
-    trace_avg_ms = trace_total / (args.steps * st.passes)
-    walks_per_launch = tiles * 256 if world > 1 else rays_per_frame / SPP
-    walks_per_launch = min(walks_per_launch, WIDTH * HEIGHT)
-    alg_bytes = BYTES_PER_WALK * walks_per_launch
-    achieved = alg_bytes / (trace_avg_ms * 1e-3) / 1e9
-    peak, peak_src = _peaks()
-
-    # e2e: the public API with host buffers.  N > 1: render_distributed on
-    # every rank (tile shards, one NCCL gather, f64 frame on rank 0's host),
-    # wall clock on rank 0 between barriers
+    # e2e through the public API with host outputs
     e2e = None
     if world > 1:
         from paper_2504_06598_b200.multi_gpu import render_distributed
 
-        render_distributed(asset, front_camera(), st, mode="tiles", device=local)  # warm
-        e2e_t = []
-        buf = None
+        for _ in range(2):
+            render_distributed(asset, front_camera(), st, mode="tiles", device=local)  # warm (pool, registration)
+        e2e_t, buf = [], None
         for _ in range(max(3, min(args.steps, 10))):
             flush.fill_(1)
             torch.cuda.synchronize(dev)
             dist.barrier()
             t0 = time.perf_counter()
-            out_buf = render_distributed(asset, front_camera(), st, mode="tiles", device=local)
-            dist.barrier()
+            buf = render_distributed(asset, front_camera(), st, mode="tiles", device=local)
             e2e_t.append(time.perf_counter() - t0)
-            buf = out_buf if rank == 0 else buf
+            del buf
         if rank == 0:
-            e2e = {"value": rays_per_frame / statistics.median(e2e_t) / 1e6, "unit": "Mrays/s",
-                   "h2d_bytes_per_step": 192 * world, "d2h_bytes_per_step": int(buf.rgb.nbytes + buf.opacity.nbytes),
-                   "ms_per_frame": statistics.median(e2e_t) * 1e3,
-                   "path": "paper_2504_06598_b200.multi_gpu.render_distributed() on every rank: tile shards traced "
-                           "and shaded per GPU, one NCCL gather to rank 0, unpacked on its GPU, f64 AccumBuffer "
-                           "copied to rank 0's host; wall clock on rank 0 between barriers"}
+            med = statistics.median(e2e_t)
+            e2e = {"value": rays_per_frame / med / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": 192 * world,
+                   "d2h_bytes_per_step": WIDTH * HEIGHT * 4 * 8, "ms_per_frame": med * 1e3,
+                   "path": "multi_gpu.render_distributed(transport='host') on every rank: each GPU traces and shades "
+                           "its 16x16 tiles and stores its pixels of the f64 AccumBuffer straight into one POSIX-"
+                           "shared host frame mapped into every rank (cudaHostRegister), over its own PCIe link; "
+                           "one barrier; rank 0 wall clock from a barrier to the frame on its host"}
     elif rank == 0:
         render(asset, front_camera(), st, device=local)  # warm (allocates scratch)
         e2e_t = []
@@ -329,33 +457,49 @@ def run_ours(args) -> None:
                        "memory (device->host over PCIe during the walk), stream synchronised before render() returns; "
                        "h2d = camera + settings kernel parameters (SrtCamera 112 B + SrtRenderParams 80 B), scene resident"}
 
+    # the same frame on the other two scene seeds (tree-quality robustness), N = 1
+    seeds = None
+    if world == 1:
+        seeds = {"0": statistics.mean(total)}
+        for seed in SEEDS[1:]:
+            _, sc_s, _, _ = scene_for(seed)
+            w_s, _, _, t_s = timed(sc_s, max(5, args.steps // 2))
+            seeds[str(seed)] = statistics.mean(t_s)
+            sc_s.close()
+        seeds_mean = statistics.mean(seeds.values())
+        seeds = {"ms_per_frame": seeds, "mean_ms": seeds_mean, "mean_value": rays_per_frame / (seeds_mean * 1e-3) / 1e6,
+                 "note": "density_cloud(1M, seed s): same workload, different scene seed (BVH shape)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        r = _cpu_baseline_sample(asset, threads)
+        r = _cpu_frame(asset, threads)
         cpu = {"value": r["rays"] / r["seconds"] / 1e6, "unit": "Mrays/s", "cores": threads, "kind": "port",
-               "sample": f"every 2nd pixel in x and y of the same 1080p frame ({r['rays']} rays), trig-hash "
-                         f"restatement bitwise equal to the reference, prebuilt SAH BVH "
-                         f"({r['bvh_build_s']:.2f} s C build)"}
+               "sample": f"the full {WIDTH}x{HEIGHT} frame once ({r['rays']} rays), same pixels as the GPU frame, "
+                         f"prebuilt SAH BVH ({r['bvh_build_s']:.2f} s C build)", "note": CPU_NOTE}
 
     if rank == 0:
         clocks = sampler.summary()
+        l2_peak = None
+        try:
+            g = ctypes.c_double()
+            if L.srt_probe_l2_bandwidth(local, 32 << 20, 5, ctypes.byref(g)) == 0:
+                l2_peak = g.value
+        except Exception:
+            pass
+        roof, issue = _roofline(kernel_ms, walks, _ncu_profile(build_id), l2_peak, clocks)
         line = {
             "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "width": WIDTH, "height": HEIGHT, "n_gaussians": N_PRIMS,
-                       "spp": SPP, "nslots": NSLOTS, "sh_degree": SH_DEG,
-                       "parallelism": f"tile-shard x{world}" + (" + NCCL gather" if world > 1 else ""),
-                       "l2": "256 MiB flush written between steps, outside the per-step CUDA events",
-                       "scene_setup_s": setup_s, "lbvh_build_s": lbvh_s, "bvh": sc.bvh_info(),
-                       "ms_per_frame": ms_per_step, "wall_s_timed_region": wall},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic_per_launch(),
-                         "kernel": "k_trace_packet (fused walk + SH shade + accumulate)", "kernel_ms": trace_avg_ms,
-                         "algorithmic_bytes_per_walk": BYTES_PER_WALK, "walks_per_launch": walks_per_launch,
-                         "peak_source": peak_src},
-            "roofline_issue": _issue_roofline(trace_avg_ms, clocks),
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(CONFIG),
+            "parallelism": f"tile-shard x{world}" + (" + NCCL gather to rank 0" if world > 1 else ""),
+            "setup": {"scene_setup_s": setup_s, "bvh_build_s": build_s, "bvh": sc.bvh_info(), "build_id": build_id,
+                      "wall_s_timed_region": wall},
+            "ranks": [{"rank": i, "step_ms": r[0], "walk_ms": r[1], "gather_ms": r[2], "unpack_ms": r[3],
+                       "tiles": int(r[4])} for i, r in enumerate(per_rank)],
+            "seeds": seeds,
+            "roofline": roof,
+            "roofline_issue": issue,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * st.passes + (args.steps if world > 1 else 0),
@@ -363,6 +507,7 @@ def run_ours(args) -> None:
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -373,8 +518,15 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--selftest", choices=["gloo"], help="CPU check of the multi-rank plumbing (no GPU)")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.warmup < 3 and args.impl == "ours" and not args.selftest:
+        args.warmup = 3  # the timing contract: at least 3 untimed frames
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(self_launch(args))
+    if args.selftest:
+        run_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

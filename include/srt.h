@@ -114,12 +114,21 @@ typedef struct {
 /* ---- library ----------------------------------------------------------- */
 const char *srt_last_error(void);      /* thread-local message of the last failure */
 const char *srt_version(void);
+const char *srt_build_id(void);        /* content hash of the sources this library was built from */
+/* Measured L2 read bandwidth (GB/s, best of `reps`) of `device`: a `bytes`
+ * buffer resident in L2 read with L1-bypassing 16-byte loads.  The
+ * denominator of the benchmark's physical L2 fraction. */
+srt_status srt_probe_l2_bandwidth(int32_t device, int64_t bytes, int32_t reps, double *gbs);
 int32_t srt_device_count(void);
 
 /* Page-locked host memory (cudaHostAlloc) for host outputs: device->host
  * copies into it run at full link speed.  srt_host_free releases it. */
 srt_status srt_host_alloc(int64_t bytes, void **out);
 srt_status srt_host_free(void *ptr);
+/* Page-lock and map existing host memory (e.g. a shared-memory frame every
+ * rank of a multi-GPU render writes its tiles into); undo with unregister. */
+srt_status srt_host_register(void *ptr, int64_t bytes);
+srt_status srt_host_unregister(void *ptr);
 
 /* ---- scene ------------------------------------------------------------- */
 /* Upload a packed scene to `device` (fp32 SoA records in HBM). */
@@ -216,7 +225,9 @@ srt_status srt_pixel_jitter(int64_t px, int64_t py, const int64_t *frames, int64
 
 /* ---- full frames (kernels.render_stochastic) ----------------------------- */
 /* Host outputs out_rgb (H,W,3) f64 and out_op (H,W) f64 = per-pixel means.
- * out_ids (optional, may be NULL): (H,W,nslots) i64 slot ids of pass pass0. */
+ * out_ids (optional, may be NULL): (H,W,nslots) i64 slot ids of pass pass0.
+ * With shard_count > 1 only the shard's 16x16 tiles are rendered and written,
+ * which needs mapped host outputs (srt_host_alloc / srt_host_register). */
 srt_status srt_render(const SrtScene *scene, const SrtCamera *camera,
                       const SrtRenderParams *params, double *out_rgb, double *out_op,
                       int64_t *out_ids);

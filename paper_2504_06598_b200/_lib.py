@@ -68,9 +68,13 @@ _f64 = ctypes.c_double
 SYMBOLS = [
     ("srt_last_error", ctypes.c_char_p, []),
     ("srt_version", ctypes.c_char_p, []),
+    ("srt_build_id", ctypes.c_char_p, []),
+    ("srt_probe_l2_bandwidth", _i32, [_i32, _i64, _i32, ctypes.POINTER(_f64)]),
     ("srt_device_count", _i32, []),
     ("srt_host_alloc", _i32, [_i64, ctypes.POINTER(_vp)]),
     ("srt_host_free", _i32, [_vp]),
+    ("srt_host_register", _i32, [_vp, _i64]),
+    ("srt_host_unregister", _i32, [_vp]),
     ("srt_scene_create", _i32, [ctypes.POINTER(SrtSceneDesc), _i32, ctypes.POINTER(_vp)]),
     ("srt_scene_destroy", _i32, [_vp]),
     ("srt_scene_create_from_splats", _i32, [ctypes.POINTER(SrtSplatDesc), _i32, ctypes.POINTER(_vp)]),

@@ -181,7 +181,11 @@ using namespace srt;
 extern "C" {
 
 const char *srt_last_error(void) { return g_last_error.c_str(); }
-const char *srt_version(void) { return "libsrt 0.1 (sm_100a)"; }
+const char *srt_version(void) { return "libsrt 0.2 (sm_100a)"; }
+#ifndef SRT_BUILD_ID
+#define SRT_BUILD_ID "unknown"
+#endif
+const char *srt_build_id(void) { return SRT_BUILD_ID; }
 
 int32_t srt_device_count(void) {
     int n = 0;
@@ -212,6 +216,20 @@ srt_status srt_host_alloc(int64_t bytes, void **out) {
     *out = nullptr;
     return cuda_status(cudaHostAlloc(out, (size_t)(bytes ? bytes : 1), cudaHostAllocPortable | cudaHostAllocMapped),
                        "cudaHostAlloc");
+}
+
+srt_status srt_host_register(void *ptr, int64_t bytes) {
+    if (!ptr || bytes <= 0) {
+        set_error("invalid host registration");
+        return SRT_ERR_INVALID_ARG;
+    }
+    return cuda_status(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterPortable | cudaHostRegisterMapped),
+                       "cudaHostRegister");
+}
+
+srt_status srt_host_unregister(void *ptr) {
+    if (!ptr) return SRT_OK;
+    return cuda_status(cudaHostUnregister(ptr), "cudaHostUnregister");
 }
 
 srt_status srt_host_free(void *ptr) {
@@ -951,8 +969,12 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
         set_error("null camera or output");
         return SRT_ERR_INVALID_ARG;
     }
-    if (p->shard_count > 1) {
-        set_error("srt_render renders whole frames; use the *_device entry points for shards");
+    // A tile shard (shard_count > 1) writes only its own pixels, straight into
+    // mapped host outputs shared by every shard (multi-GPU frames assembled in
+    // one host buffer, each GPU over its own PCIe link).
+    if (p->shard_count > 1 && (!mapped_host(out_rgb) || !mapped_host(out_op) || out_ids || p->rng == SRT_RNG_TRIG64)) {
+        set_error("a shard of srt_render needs mapped host outputs (srt_host_alloc / srt_host_register), "
+                  "the counter stream and no ids");
         return SRT_ERR_INVALID_ARG;
     }
     SrtScene *s = const_cast<SrtScene *>(sc);

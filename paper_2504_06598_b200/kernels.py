@@ -48,7 +48,7 @@ def _fingerprint(a) -> tuple:
     if a is None:
         return (None,)
     if not isinstance(a, np.ndarray):
-        return ("scalar", float(a))
+        return ("value", repr(a))
     flat = a.reshape(-1)
     step = max(1, flat.shape[0] // 64)
     return (id(a), a.__array_interface__["data"][0], a.shape, a.dtype.str, flat[::step][:64].tobytes())

@@ -294,9 +294,177 @@ def gpu_shard_renderer(scene, camera_tuple, settings, device):
     return run
 
 
-def render_distributed(asset, camera, settings, mode: str = "tiles", group=None, device: int | None = None):
+# ---------------------------------------------------------------------------
+# one host frame shared by every rank (multi-GPU e2e)
+# ---------------------------------------------------------------------------
+
+def _bcast_ints(values, group=None, src: int = 0) -> list:
+    """Broadcast a few ints from `src` (a device tensor under NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(values), dtype=torch.int64, device=dev)
+    dist.broadcast(t, src, group=group)
+    return [int(v) for v in t.tolist()]
+
+
+class _SharedBlock:
+    """Numpy-visible view of one pooled shared frame; returns the frame to the
+    pool when the last array viewing it is collected (rank 0)."""
+
+    def __init__(self, pool, key: int, base: np.ndarray):
+        self._pool, self._key, self._base = pool, key, base
+        self.__array_interface__ = {"shape": base.shape, "typestr": "|u1",
+                                    "data": (base.__array_interface__["data"][0], False), "version": 3}
+
+    def __del__(self):
+        try:
+            self._pool._release(self._key)
+        except Exception:
+            pass
+
+
+class SharedFramePool:
+    """Host frames in POSIX shared memory (/dev/shm), mapped by every rank of
+    the group and page-locked + device-mapped on each (srt_host_register):
+    each GPU writes its own 16x16 tiles of the f64 frame straight into the one
+    buffer over its own PCIe link, so the frame is assembled on the host
+    without a gather through rank 0's GPU and link.
+
+    Rank 0 owns the pool: per frame it picks a free block (or creates one) and
+    broadcasts its index; blocks return to the pool when rank 0's AccumBuffer
+    arrays are collected.  ``register=False`` skips the CUDA registration
+    (CPU tests of the protocol)."""
+
+    SHM_DIR = "/dev/shm"
+
+    def __init__(self, register: bool = True):
+        self.register = register
+        self._prefix = None
+        self._attached: dict = {}  # key -> (mmap, uint8 array, nbytes)
+        self._free: dict = {}      # nbytes -> [key]   (rank 0)
+        self._next = 0
+        self._owner = False
+
+    def _path(self, key: int) -> str:
+        return f"{self.SHM_DIR}/{self._prefix}_{key}"
+
+    def _attach(self, key: int, nbytes: int, create: bool):
+        import mmap
+        import os
+
+        flags = os.O_RDWR | (os.O_CREAT | os.O_EXCL if create else 0)
+        fd = os.open(self._path(key), flags, 0o600)
+        try:
+            if create:
+                os.ftruncate(fd, nbytes)
+            mm = mmap.mmap(fd, nbytes)
+        finally:
+            os.close(fd)
+        arr = np.frombuffer(mm, dtype=np.uint8)
+        if self.register:
+            import ctypes
+
+            from . import _lib
+
+            _lib.check(_lib.load().srt_host_register(ctypes.c_void_p(arr.__array_interface__["data"][0]), nbytes))
+        self._attached[key] = (mm, arr, nbytes)
+
+    def acquire(self, nbytes: int, rank: int, group=None):
+        """(key, writable uint8 view of the block) on every rank; collective."""
+        import os
+        import uuid
+
+        import torch.distributed as dist
+
+        if self._prefix is None:
+            box = [f"srt{os.getpid()}_{uuid.uuid4().hex[:8]}" if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0, group=group)
+            self._prefix = box[0]
+            if rank == 0:
+                import atexit
+
+                self._owner = True
+                atexit.register(self.close)
+        key = -1
+        if rank == 0:
+            free = self._free.setdefault(nbytes, [])
+            if free:
+                key = free.pop()
+            else:
+                key = self._next
+                self._next += 1
+                self._attach(key, nbytes, create=True)
+        key = _bcast_ints([key], group)[0]
+        if key not in self._attached:
+            self._attach(key, nbytes, create=False)
+        _, arr, _ = self._attached[key]
+        if rank == 0:
+            return key, np.asarray(_SharedBlock(self, key, arr))
+        return key, arr
+
+    def _release(self, key: int) -> None:
+        if key in self._attached:
+            self._free.setdefault(self._attached[key][2], []).append(key)
+
+    def close(self) -> None:
+        import os
+
+        for key, (mm, arr, nb) in self._attached.items():
+            if self.register:
+                try:
+                    import ctypes
+
+                    from . import _lib
+
+                    _lib.load().srt_host_unregister(ctypes.c_void_p(arr.__array_interface__["data"][0]))
+                except Exception:
+                    pass
+            if self._owner:
+                try:
+                    os.unlink(self._path(key))
+                except OSError:
+                    pass
+        self._attached.clear()  # the mappings go with the last array that views them
+
+
+_SHARED = None
+
+
+def shared_frame_pool() -> SharedFramePool:
+    global _SHARED
+    if _SHARED is None:
+        _SHARED = SharedFramePool()
+    return _SHARED
+
+
+def render_frame_shared(p: ShardPlan, shard_write: Callable, pool: SharedFramePool, group=None):
+    """One tile-sharded frame assembled in host shared memory: every rank
+    calls ``shard_write(plan, rgb (H,W,3) f64 view, opacity (H,W) f64 view)``,
+    which writes exactly its own tiles; one barrier; rank 0 returns the
+    (rgb, opacity) arrays (pooled), the others None."""
+    import torch.distributed as dist
+
+    H, W = p.height, p.width
+    nbytes = H * W * 4 * 8
+    _, raw = pool.acquire(nbytes, p.rank, group)
+    f = raw.view(np.float64)
+    rgb, op = f[: H * W * 3].reshape(H, W, 3), f[H * W * 3:].reshape(H, W)
+    shard_write(p, rgb, op)
+    dist.barrier(group=group)
+    return (rgb, op) if p.rank == 0 else None
+
+
+def render_distributed(asset, camera, settings, mode: str = "tiles", group=None, device: int | None = None,
+                       transport: str | None = None):
     """Drop-in multi-GPU render: call on every rank of an initialised process
-    group (NCCL).  Returns the AccumBuffer on rank 0, None on the others."""
+    group (NCCL).  Returns the AccumBuffer on rank 0, None on the others.
+
+    ``transport`` (tiles mode): ``"host"`` (default at world size > 1) -- every
+    rank writes its tiles of the f64 frame into one shared, mapped host buffer
+    (SharedFramePool); ``"nccl"`` -- tile buffers gathered to rank 0's GPU with
+    one NCCL gather, then one device->host copy."""
     import torch
     import torch.distributed as dist
 
@@ -310,6 +478,20 @@ def render_distributed(asset, camera, settings, mode: str = "tiles", group=None,
     sc = prepare(asset, settings, device=device)
     ct = camera_tuple(camera, settings.width, settings.height)
     p = plan(mode, rank, world, settings.width, settings.height, settings.passes)
+    if transport is None:
+        transport = "host" if (mode == "tiles" and world > 1) else "nccl"
+    if transport not in ("host", "nccl"):
+        raise ValueError(f"unknown transport {transport!r}")
+    if transport == "host" and mode == "tiles" and world > 1:
+        m = 0 if settings.depth_mode == "mean" else 1
+
+        def write(plan_, rgb, op):
+            sc.render(ct, plan_.width, plan_.height, settings.passes, settings.multisample, m,
+                      settings.cutoff_s ** 2, True, settings.seed, settings.background, out_rgb=rgb, out_op=op,
+                      shard_index=plan_.rank, shard_count=plan_.world)
+
+        got = render_frame_shared(p, write, shared_frame_pool(), group)
+        return None if got is None else AccumBuffer(got[0], got[1], settings.samples_per_pixel)
     if settings.passes > 1 or mode == "samples":
         # exact fixed-point sums: bitwise the single-GPU render() frame
         frame = render_frame_sums(p, gpu_shard_sums(sc, ct, settings, device), settings.multisample, group)

@@ -290,11 +290,15 @@ class DeviceScene:
 
     # -- frames ----------------------------------------------------------------
     def render(self, cam, width, height, passes=1, nslots=1, mode=0, s2=8.0, clip=True, seed=0,
-               background=(0.0, 0.0, 0.0), pass0=0, want_ids=False, out_rgb=None, out_op=None, rng="counter"):
+               background=(0.0, 0.0, 0.0), pass0=0, want_ids=False, out_rgb=None, out_op=None, rng="counter",
+               shard_index=0, shard_count=1):
         """kernels.render_stochastic semantics (kernels.py:622-673) on the GPU.
-        Returns (rgb (H,W,3) f64, opacity (H,W) f64, ids (H,W,N) i64 of pass pass0 or None)."""
+        Returns (rgb (H,W,3) f64, opacity (H,W) f64, ids (H,W,N) i64 of pass pass0 or None).
+        shard_count > 1 renders only the 16x16 tiles t with t % shard_count ==
+        shard_index, into mapped host outputs (multi_gpu.SharedFramePool)."""
         camera = make_camera(cam)
-        prm = make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background, pass0, rng=rng)
+        prm = make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background, pass0,
+                                 shard_index=shard_index, shard_count=shard_count, rng=rng)
         rgb = np.empty((height, width, 3)) if out_rgb is None else out_rgb
         op = np.empty((height, width)) if out_op is None else out_op
         ids = np.full((height, width, nslots), -1, np.int64) if want_ids else None

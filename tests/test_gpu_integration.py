@@ -16,6 +16,7 @@ Skipped when ``baseline/_ref`` is absent (the reference is not part of the
 repository) -- never reads /root/reference at run time.
 """
 
+import importlib
 import os
 import sys
 from pathlib import Path
@@ -37,8 +38,11 @@ def splatray():
     sys.path.insert(0, str(REF_INSTALL))
     try:
         import splatray
-        import splatray.render as sr
-        import splatray.validate as sv
+
+        # the package re-exports a function named ``render``, which shadows the
+        # submodule attribute: take the modules from importlib
+        sr = importlib.import_module("splatray.render")
+        sv = importlib.import_module("splatray.validate")
     except Exception as e:  # numba/scipy missing on this box
         pytest.skip(f"reference package not importable: {e}")
     saved = (sr.kernels, sv.kernels)
@@ -47,10 +51,10 @@ def splatray():
 
 
 def _swap(splatray):
-    import splatray.render as sr
-    import splatray.validate as sv
-
     from paper_2504_06598_b200 import kernels as gpu_kernels
+
+    sr = importlib.import_module("splatray.render")
+    sv = importlib.import_module("splatray.validate")
 
     sr.kernels = gpu_kernels
     sv.kernels = gpu_kernels

@@ -195,3 +195,69 @@ def test_gloo_world2_fixed_point_sums_are_bitwise_single_frame(mode):
     same, err = q.get(timeout=5)
     assert same
     assert err <= 1e-9, err
+
+
+def _shared_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, h = 70, 50
+        pool = mg.SharedFramePool(register=False)
+        keys = []
+
+        def write(p, rgb, op):
+            # each rank writes exactly its own tiles (as srt_render does for a shard)
+            px, py, ok = mg.compact_pixels(p.width, p.height, p.rank, p.world)
+            rgb[py[ok], px[ok]] = [p.rank + 1.0, frame_no, 0.5]
+            op[py[ok], px[ok]] = p.rank + 1.0
+
+        results = []
+        for frame_no in range(3):
+            p = mg.plan("tiles", rank, world, w, h, 1)
+            got = mg.render_frame_shared(p, write, pool)
+            if rank == 0:
+                rgb, op = got
+                results.append((rgb.copy(), op.copy()))
+                keys.append(rgb.__array_interface__["data"][0])
+                if frame_no == 0:
+                    keep = got  # frame 0 stays referenced: frame 1 must use another block
+                del got, rgb, op
+        if rank == 0:
+            q.put((results, keys))
+        dist.barrier()
+        pool.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_shared_host_frame_assembles_every_tile():
+    """multi_gpu.SharedFramePool / render_frame_shared (the multi-GPU e2e path)
+    with gloo at world size 3: every rank writes only its tiles into one
+    POSIX-shared frame; rank 0 sees the whole frame, blocks still referenced
+    by a returned frame are not reused, released ones are."""
+    import multiprocessing as mp
+
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shared_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results, keys = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    w, h = 70, 50
+    owner = np.zeros((h, w))
+    for r in range(world):
+        px, py, ok = mg.compact_pixels(w, h, r, world)
+        owner[py[ok], px[ok]] = r + 1.0
+    for i, (rgb, op) in enumerate(results):
+        np.testing.assert_array_equal(op, owner)
+        np.testing.assert_array_equal(rgb[..., 0], owner)
+        assert np.all(rgb[..., 1] == i)
+    assert keys[1] != keys[0]  # frame 0 was still referenced
+    assert keys[2] == keys[1]  # frame 1 was released and reused

@@ -1,6 +1,11 @@
 """Summarise an ncu --set full report (+ optional launch-list CSV) into profiles/.
 
-    python tools/ncu_summary.py gpurun_out/prof_trace.ncu-rep gpurun_out/launches.csv profiles/r01_xxx
+    python tools/ncu_summary.py gpurun_out/prof_trace.ncu-rep gpurun_out/launches.csv profiles/r02_xxx \
+        [--bench BUILD_ID_FILE]
+
+--bench also writes profiles/ncu_summary.json, the pointer bench.py reads: the
+first k_trace_packet launch's DRAM / L2 bytes and warp instructions, stamped
+with the srt_build_id of the profiled library (tools/profile_trace.py writes it).
 """
 import csv
 import io
@@ -84,6 +89,31 @@ def main():
             lines.append(f"  {name[:70]:70s} n={d['launches']:3d} total={d['total_ns']/1e3:10.1f} us share={d['share']:.3f}")
     (outdir / "ncu_summary.txt").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
+    if "--bench" in sys.argv:
+        bid = Path(sys.argv[sys.argv.index("--bench") + 1]).read_text().strip()
+        k = next(x for x in summary["full"] if "k_trace_packet" in x["kernel"])
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def val(m):
+            return float(k[m][0]) * unit.get(k[m][1], 1.0)
+
+        pointer = {
+            "kernel": k["kernel"],
+            "source": f"{outdir}/ncu_summary.json (ncu --set full --clock-control none, one launch of "
+                      f"tools/profile_trace.py: C3-target 1080p, 2,073,600 walks)",
+            "build_id": bid,
+            "walks_per_launch": 2073600,
+            "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+            "dram_read_bytes": val("dram__bytes_read.sum"),
+            "dram_write_bytes": val("dram__bytes_write.sum"),
+            "l2_bytes_per_launch": float(k["lts__t_sectors.sum"][0]) * 32,
+            "warp_inst_per_launch": float(k["smsp__inst_executed.sum"][0]),
+            "issue_active_pct": float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+            "kernel_ms_ncu": float(k["gpu__time_duration.sum"][0]) * (1e-3 if k["gpu__time_duration.sum"][1] == "us"
+                                                                       else 1.0),
+        }
+        (Path(__file__).resolve().parent.parent / "profiles" / "ncu_summary.json").write_text(
+            json.dumps(pointer, indent=1) + "\n")
 
 
 if __name__ == "__main__":
