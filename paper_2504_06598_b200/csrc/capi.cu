@@ -341,6 +341,7 @@ srt_status srt_scene_destroy(SrtScene *s) {
     cudaFree(s->d_geom);
     cudaFree(s->d_nodes);
     cudaFree(s->d_nodes4);
+    cudaFree(s->d_nodes8);
     cudaFree(s->d_stats);
     cudaFree(s->d_flag);
     cudaFree(s->d_scratch);
@@ -539,8 +540,8 @@ srt_status srt_bvh_info(const SrtScene *s, int64_t *num_nodes, int32_t *depth, i
     if (depth) *depth = s->depth;
     if (num_prims) *num_prims = s->n;
     if (device_bytes)
-        *device_bytes = (int64_t)sizeof(Node2) * s->num_nodes + (int64_t)sizeof(Geom) * s->n +
-                        (int64_t)sizeof(float) * s->n * 3 * s->sh_k;
+        *device_bytes = (int64_t)sizeof(Node2) * s->num_nodes + (int64_t)sizeof(Node4) * 9 * s->num_nodes4 +
+                        (int64_t)sizeof(Geom) * s->n + (int64_t)sizeof(float) * s->n * 3 * s->sh_k;
     return SRT_OK;
 }
 

@@ -645,7 +645,42 @@ static srt_status collapse4_dp(SrtScene *s, float cv, float ct, float cj) {
     return rc;
 }
 
+// The 4-wide tree per direction octant (SceneView::nodes8): record j of copy
+// `oct` is node j with the lo / hi plane arrays of every axis that is
+// negative in `oct` swapped, so the first array of an axis holds the planes a
+// ray of that octant enters through.  Empty slots (lo = +3e38, hi = -3e38)
+// stay empty in every copy.
+__global__ void k_octant_nodes(const Node4 *__restrict__ n4, int m, Node4 *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)m * 8) return;
+    const int oct = (int)(i / m), j = (int)(i % m);
+    Node4 a = n4[j];
+    Node4 o = a;
+    if (oct & 1) { o.lox = a.hix; o.hix = a.lox; }
+    if (oct & 2) { o.loy = a.hiy; o.hiy = a.loy; }
+    if (oct & 4) { o.loz = a.hiz; o.hiz = a.loz; }
+    out[i] = o;
+}
+
+static srt_status collapse4_tree(SrtScene *s);
+
 srt_status collapse4(SrtScene *s) {
+    srt_status rc = collapse4_tree(s);
+    if (rc) return rc;
+    if (s->d_nodes8) cudaFree(s->d_nodes8);
+    s->d_nodes8 = nullptr;
+    const int m = s->num_nodes4;
+    if (m == 0) return SRT_OK;
+    rc = cuda_status(cudaMalloc(&s->d_nodes8, sizeof(Node4) * 8 * (size_t)m), "octant node alloc");
+    if (rc) return rc;
+    const int64_t total = (int64_t)m * 8;
+    k_octant_nodes<<<(unsigned)((total + 255) / 256), 256, 0, s->stream>>>(s->d_nodes4, m, s->d_nodes8);
+    rc = cuda_status(cudaGetLastError(), "k_octant_nodes");
+    if (!rc) rc = cuda_status(cudaStreamSynchronize(s->stream), "octant nodes");
+    return rc;
+}
+
+static srt_status collapse4_tree(SrtScene *s) {
     if (s->num_nodes > 0) {
         static const char *mode = getenv("SRT_COLLAPSE");
         if (mode && !strcmp(mode, "dp")) {

@@ -28,7 +28,11 @@ struct __align__(16) Node2 {
 
 // 4-wide node, one 128-B line: child boxes SoA + child codes.  Produced by
 // collapsing the binary tree (greedy largest-area expansion); unused slots
-// have an empty box and code kLeafEmpty.
+// have an empty box and code kLeafEmpty.  The octant copies (nodes8) hold
+// the same record with, per axis whose direction sign is negative in that
+// octant, the lo and hi plane arrays swapped: the first array of each axis is
+// then the near planes of a ray in that octant.  pad.x = valid child mask |
+// leaf child mask << 4.
 struct __align__(128) Node4 {
     float4 lox, hix, loy, hiy, loz, hiz;
     int4 kids;
@@ -63,6 +67,7 @@ struct SceneView {
     const double *opac64;
     const Node2 *nodes;
     const Node4 *nodes4;
+    const Node4 *nodes8;  // 8 x num_nodes4: the tree laid out per direction octant (packet kernel)
     int32_t num_nodes4;
     const Geom *geom;
     const float *sh;  // (n, 3, K) fp32, original id order

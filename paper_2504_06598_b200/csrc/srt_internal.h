@@ -25,6 +25,7 @@ struct SrtScene {
     srt::Node2 *d_nodes = nullptr; // (num_nodes,) binary tree (build / upload output)
     int32_t num_nodes = 0;
     srt::Node4 *d_nodes4 = nullptr; // (num_nodes4,) 4-wide tree traced by the kernels
+    srt::Node4 *d_nodes8 = nullptr; // (8, num_nodes4) the same tree per direction octant (packet kernel)
     int32_t num_nodes4 = 0;
     unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
@@ -46,6 +47,7 @@ struct SrtScene {
         v.opac64 = d_opac;
         v.nodes = d_nodes;
         v.nodes4 = d_nodes4;
+        v.nodes8 = d_nodes8;
         v.num_nodes4 = num_nodes4;
         v.geom = d_geom;
         v.sh = d_sh;

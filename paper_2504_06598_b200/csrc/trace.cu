@@ -779,10 +779,20 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
 // into every child that any lane hits, nearest (warp-min entry) first, and
 // culls a popped node when its warp-min entry lies beyond every lane's far.
 // Leaf work is compacted across the warp exactly as in k_trace_coop.
+//
+// The packet reads the copy of the tree laid out for its direction octant
+// (SceneView::nodes8): per axis the near planes of the 4 children first, the
+// far planes second, so a lane's slab test is 6 FMAs, a 3-way max and a 3-way
+// min -- no per-axis min/max to sort the two planes.  A packet whose lanes do
+// not all share the octant (a pixel block straddling an axis of the view)
+// takes the order-agnostic min/max slab on the same record.  Child handling
+// is driven by warp-uniform masks: one OR-reduction of the lanes' hit masks,
+// one ballot per hit leaf child, one min-reduction per inner child when more
+// than one must be ordered.
 // ---------------------------------------------------------------------------
 // BATCH: leaf jobs are run once at least BATCH are queued; MINB: minimum
 // resident blocks per SM requested from the register allocator.
-template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1, int ORDER = 1>
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1>
 __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
                                                                        int *overflow, unsigned long long *stats) {
     constexpr int W = kTraceThreads / 32;
@@ -791,8 +801,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
     __shared__ unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
-    __shared__ int sjob[W][BATCH + 128];
-    __shared__ unsigned char sown[W][BATCH + 128];
+    __shared__ uint32_t sjob[W][BATCH + 128];  // leaf job: (slot << 5) | owner lane
     __shared__ int sstk_node[W][PSTACK];
     __shared__ int sstk_key[W][PSTACK];
     // explicit-ray packets (Src::kRayOrigin): each lane's own origin
@@ -801,6 +810,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     __shared__ double sdo[RO ? W : 1][32][4];  // fp64 origin + 1/|d|^2 (exact stage)
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     const uint32_t total = src.total();
     const float cfox = (float)src.cam.e[0], cfoy = (float)src.cam.e[1], cfoz = (float)src.cam.e[2];
     const float comag = fmaxf(fabsf(cfox), fmaxf(fabsf(cfoy), fabsf(cfoz)));
@@ -837,24 +847,26 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             init_ray(r, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
             far = -INFINITY;  // hits nothing
         }
+        // direction octant of the packet, from the signs of the reciprocal
+        // directions the slab uses (a -0 component counts as negative)
+        const unsigned vm = __ballot_sync(FULL, valid);
+        const unsigned nx_m = __ballot_sync(FULL, valid && signbit(r.idx));
+        const unsigned ny_m = __ballot_sync(FULL, valid && signbit(r.idy));
+        const unsigned nz_m = __ballot_sync(FULL, valid && signbit(r.idz));
+        const int oct = (nx_m ? 1 : 0) | (ny_m ? 2 : 0) | (nz_m ? 4 : 0);
+        const bool mixed = (nx_m && nx_m != vm) || (ny_m && ny_m != vm) || (nz_m && nz_m != vm);
+        const Node4 *tree = s.nodes8 + (size_t)oct * (size_t)s.num_nodes4;
         int sp = 0;
-        int njobs = 0;  // leaf jobs queued for the warp (processed in batches of >= 32)
-        int oct = 0;    // direction octant of the packet (child order hint)
-        {
-            unsigned vm = __ballot_sync(FULL, valid);
-            int rep = vm ? __ffs(vm) - 1 : 0;
-            float ex = __shfl_sync(FULL, r.fdx, rep), ey = __shfl_sync(FULL, r.fdy, rep),
-                  ez = __shfl_sync(FULL, r.fdz, rep);
-            oct = (ex < 0.f ? 1 : 0) | (ey < 0.f ? 2 : 0) | (ez < 0.f ? 4 : 0);
-        }
-        int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
+        int njobs = 0;  // leaf jobs queued for the warp (processed in batches of >= BATCH)
+        int node = (s.num_nodes4 > 0 && vm) ? 0 : kDone;
         auto run_jobs = [&]() {
             sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
             __syncwarp();
             for (int jb = 0; jb < njobs; jb += 32) {
                 int j = jb + lane;
                 if (j < njobs) {
-                    int o = sown[wid][j];
+                    const uint32_t job = sjob[wid][j];
+                    const int o = (int)(job & 31u), slot = (int)(job >> 5);
                     float4 dv = sdir[wid][o];
                     ScreenRay sr;
                     sr.fdx = dv.x; sr.fdy = dv.y; sr.fdz = dv.z;
@@ -864,15 +876,15 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                         sr.inv_dd = sdo[wid][o][3];
                         sr.t_min = src.f_tmin;
                         sr.t_max0 = src.f_tmax;
-                        packet_job<NS, MODE, STATS, true>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
+                        packet_job<NS, MODE, STATS, true>(s, src.cam, sr, sdd[wid][o], w, slot, sbest[wid][o],
                                                           skey[wid][o], dv.w, ct, sdo[wid][o]);
                     } else {
                         sr.fox = cfox; sr.foy = cfoy; sr.foz = cfoz; sr.omag = comag;
                         sr.inv_dd = 1.0;  // camera directions are unit in fp64
                         sr.t_min = 0.0f;
                         sr.t_max0 = INFINITY;
-                        packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, sjob[wid][j], sbest[wid][o],
-                                                    skey[wid][o], dv.w, ct);
+                        packet_job<NS, MODE, STATS>(s, src.cam, sr, sdd[wid][o], w, slot, sbest[wid][o], skey[wid][o],
+                                                    dv.w, ct);
                     }
                 }
             }
@@ -908,116 +920,96 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 if (node == kDone) continue;  // all culled: flush what is queued, then finish
             }
             if (lane == 0) ct.add(0, 1);
-            int4 kids;
-            int key[4];
             SRT_DCHECK(node >= 0 && node < s.num_nodes4);
-            const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
-            unsigned hitm = slab4<true>(r, np, far, kids, key);
-            const unsigned lt = (1u << lane) - 1u;
+            const float4 *np = reinterpret_cast<const float4 *>(tree + node);
+            // near / far planes of the 4 children along the packet's octant
+            const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
+                         az = __ldg(np + 4), bz = __ldg(np + 5);
+            const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+            const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
+            const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
+            const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
+            const float paz[4] = {az.x, az.y, az.z, az.w}, pbz[4] = {bz.x, bz.y, bz.z, bz.w};
+            unsigned hitm = 0;
+            int key[4];
+            if (!mixed) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float tn = fmaxf(fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
+                                                 fmaf(paz[k], r.idz, -r.oidz)), r.t_min);
+                    const float tf = fminf(fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
+                                                 fmaf(pbz[k], r.idz, -r.oidz)), far);
+                    hitm |= tn <= tf ? (1u << k) : 0u;
+                    key[k] = (__float_as_int(tn) & ~3) | k;  // tn >= t_min >= 0: orderable as int
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float xa = fmaf(pax[k], r.idx, -r.oidx), xb = fmaf(pbx[k], r.idx, -r.oidx);
+                    const float ya = fmaf(pay[k], r.idy, -r.oidy), yb = fmaf(pby[k], r.idy, -r.oidy);
+                    const float za = fmaf(paz[k], r.idz, -r.oidz), zb = fmaf(pbz[k], r.idz, -r.oidz);
+                    const float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
+                    const float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
+                    hitm |= tn <= tf ? (1u << k) : 0u;
+                    key[k] = (__float_as_int(tn) & ~3) | k;
+                }
+            }
+            const unsigned validm = hint & 15u, leafm = (hint >> 4) & 15u;
+            hitm &= validm;  // empty slots: inverted boxes
+            const unsigned any = __reduce_or_sync(FULL, hitm);
             node = kDone;
-            if (ORDER == 1) {
-                // octant order precomputed per node (lbvh.cu): one OR-reduce gives the
-                // children any lane hits; leaves are compacted, inner children pushed
-                // far-to-near along the packet's direction octant
-                int4 hint = __ldg(reinterpret_cast<const int4 *>(np + 7));
-                unsigned anyhit = __reduce_or_sync(FULL, hitm);
-                unsigned leafm = ((unsigned)hint.x >> 4) & 15u;
-                unsigned lhit = anyhit & leafm;
-                while (lhit) {
-                    int k = __ffs(lhit) - 1;
-                    lhit &= lhit - 1;
-                    bool h = (hitm >> k) & 1u;
-                    unsigned bm = __ballot_sync(FULL, h);
+            // leaf children any lane hits: one ballot each compacts the hitting
+            // lanes into the job queue (jobs run in batches at the loop top:
+            // deferring them only delays the far-bound clip, never a result)
+            const unsigned lh = hitm & leafm, al = any & leafm;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (al & (1u << k)) {
+                    const bool h = (lh >> k) & 1u;
+                    const unsigned bm = __ballot_sync(FULL, h);
                     if (h) {
-                        int o = njobs + __popc(bm & lt);
-                        SRT_DCHECK(o < BATCH + 128);
-                        sjob[wid][o] = ~pick(kids, k);
-                        sown[wid][o] = (unsigned char)lane;
+                        SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
+                        sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~pick(kids, k) << 5) | (uint32_t)lane;
                     }
                     njobs += __popc(bm);
                 }
-                unsigned ihit = anyhit & ~leafm;
-                if (ihit) {
-                    unsigned ordb = ((unsigned)(oct < 4 ? hint.y : hint.z) >> ((oct & 3) * 8)) & 0xFFu;
-                    int order[4], n = 0;
+            }
+            // inner children any lane hits: descend into the nearest (warp-min
+            // entry), push the others far-to-near with their warp-min entries
+            const unsigned ai = any & ~leafm;
+            if (ai) {
+                if (!(ai & (ai - 1))) {
+                    node = pick(kids, __ffs(ai) - 1);  // one: nothing to order or push
+                } else {
+                    const unsigned ih = hitm & ~leafm;
+                    int wk[4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        int c = (ordb >> (2 * j)) & 3;
-                        if ((ihit >> c) & 1u) order[n++] = c;
-                    }
-                    if (sp + n - 1 > PSTACK) {
+                    for (int k = 0; k < 4; ++k) wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? key[k] : 0x7FFFFFFF);
+#define SRT_CX(a, b)                  \
+    {                                 \
+        int lo_ = min(wk[a], wk[b]);  \
+        int hi_ = max(wk[a], wk[b]);  \
+        wk[a] = lo_;                  \
+        wk[b] = hi_;                  \
+    }
+                    SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
+#undef SRT_CX
+                    const int nin = __popc(ai);
+                    if (sp + nin - 1 > PSTACK) {
                         if (lane == 0) atomicExch(overflow, 1);
                         break;
                     }
-                    if (lane == 0)
-                        for (int j = n - 1; j >= 1; --j) {
-                            SRT_DCHECK(sp < PSTACK);
-                            sstk_node[wid][sp] = pick(kids, order[j]);
-                            sstk_key[wid][sp] = 0;
-                            ++sp;
-                        }
-                    else
-                        sp += n - 1;
-                    node = pick(kids, order[0]);
-                }
-            } else {
-            // Child codes are warp-uniform, so leaf/inner is a uniform branch per
-            // child: one collective each (ballot for leaves, min-reduce for inner).
-            int wkey[4];
+                    if (lane == 0) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                int code = pick(kids, k);
-                bool h = (hitm >> k) & 1u;
-                wkey[k] = 0x7FFFFFFF;
-                if (code == kLeafEmpty) continue;
-                if (code < 0) {
-                    unsigned bm = __ballot_sync(FULL, h);
-                    if (h) {
-                        int o = njobs + __popc(bm & lt);
-                        SRT_DCHECK(o < BATCH + 128);
-                        sjob[wid][o] = ~code;
-                        sown[wid][o] = (unsigned char)lane;
+                        for (int j = 3; j >= 1; --j)
+                            if (j < nin) {
+                                sstk_node[wid][sp + nin - 1 - j] = pick(kids, wk[j] & 3);
+                                sstk_key[wid][sp + nin - 1 - j] = wk[j] & ~3;
+                            }
                     }
-                    njobs += __popc(bm);
-                } else {
-                    wkey[k] = __reduce_min_sync(FULL, h ? key[k] : 0x7FFFFFFF);
+                    sp += nin - 1;
+                    node = pick(kids, wk[0] & 3);
                 }
-            }
-            // leaf jobs run in batches (loop top): deferring them a node or two
-            // only delays the far-bound clip, never changes a result
-            // ---- inner children: warp-uniform order by the warp-min entry ----
-            int nin = (wkey[0] != 0x7FFFFFFF) + (wkey[1] != 0x7FFFFFFF) + (wkey[2] != 0x7FFFFFFF) +
-                      (wkey[3] != 0x7FFFFFFF);
-            if (nin == 1) {
-                // one inner child hit: descend, nothing to order or push
-                int k = wkey[0] != 0x7FFFFFFF ? 0 : (wkey[1] != 0x7FFFFFFF ? 1 : (wkey[2] != 0x7FFFFFFF ? 2 : 3));
-                node = pick(kids, k);
-            } else if (nin > 1) {
-#define SRT_CX(a, b)                      \
-    {                                     \
-        int lo_ = min(wkey[a], wkey[b]);  \
-        int hi_ = max(wkey[a], wkey[b]);  \
-        wkey[a] = lo_;                    \
-        wkey[b] = hi_;                    \
-    }
-                SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
-#undef SRT_CX
-                if (sp + nin - 1 > PSTACK) {
-                    if (lane == 0) atomicExch(overflow, 1);
-                    break;
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int j = 3; j >= 1; --j)
-                        if (j < nin) {
-                            SRT_DCHECK(sp + nin - 1 - j < PSTACK);
-                            sstk_node[wid][sp + nin - 1 - j] = pick(kids, wkey[j] & 3);
-                            sstk_key[wid][sp + nin - 1 - j] = wkey[j] & ~3;
-                        }
-                }
-                sp += nin - 1;
-                node = pick(kids, wkey[0] & 3);
-            }
             }
             __syncwarp();
         }
@@ -1097,12 +1089,12 @@ static int env_int(const char *name, int dflt) {
     return e ? atoi(e) : dflt;
 }
 
-template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH, int MINB, int ORDER = 1>
+template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH, int MINB>
 static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const WalkCfg &w, cudaStream_t st) {
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>, kTraceThreads, 0);
+            &blocks_per_sm, k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>, kTraceThreads, 0);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     if (!g_num_sms) {
@@ -1116,7 +1108,7 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
-    k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB, ORDER>
+    k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>
         <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
 }
@@ -1136,8 +1128,8 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
         if (cfg == 1) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 1>(s, src, w, st);
         if (cfg == 2) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 32, 7>(s, src, w, st);
         if (cfg == 3) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 64, 8>(s, src, w, st);
-        if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9, 0>(s, src, w, st);
-        if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10, 0>(s, src, w, st);
+        if (cfg == 12) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 9>(s, src, w, st);
+        if (cfg == 13) return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, 48, 10>(s, src, w, st);
     }
 #endif
     // 8 resident blocks/SM (64 registers, no spills) at N=1: 1.936 vs 1.964 ms
@@ -1150,7 +1142,7 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     // leaf jobs per batch: 48 for N=1 (1.964 vs 1.976 ms at 32) and N=4
     // (2.957 vs 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
     constexpr int kBatch = (NS == 1 || (NS == 4 && MODE == 0)) ? 48 : 32;
-    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB, 0>(s, src, w, st);
+    return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB>(s, src, w, st);
 }
 
 template <int NS, int MODE, int RNG, class Src>
