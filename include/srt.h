@@ -284,6 +284,10 @@ srt_status srt_scene_check(const SrtScene *scene, int32_t reset);
  * passes, exact evaluations, accepted slot updates, stack pops, culled
  * pops, walks.  reset != 0 zeroes them. */
 srt_status srt_trace_stats(const SrtScene *scene, uint64_t *out, int32_t reset);
+/* The first n (<= 16) counters; 8.. are packet-walk diagnostics: visits with a
+ * leaf child hit, leaf / inner children hit by any lane, lanes with a hit per
+ * visit, lanes without an accepted hit per visit, job rounds, empty visits. */
+srt_status srt_trace_counters(const SrtScene *scene, uint64_t *out, int32_t n, int32_t reset);
 /* Number of 16x16 tiles a shard owns (buffer sizing for tile-compact layout). */
 int64_t srt_shard_tiles(int32_t width, int32_t height, int32_t shard_index,
                         int32_t shard_count);

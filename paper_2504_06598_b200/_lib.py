@@ -107,6 +107,7 @@ SYMBOLS = [
     ("srt_hash_positions", _i32, [_vp, _i64, _i64, _vp, _i32]),
     ("srt_pixel_jitter", _i32, [_i64, _i64, _vp, _i64, ctypes.c_uint32, _vp, _i32]),
     ("srt_trace_stats", _i32, [_vp, _vp, _i32]),
+    ("srt_trace_counters", _i32, [_vp, _vp, _i32, _i32]),
     ("srt_shard_tiles", _i64, [_i32, _i32, _i32, _i32]),
     ("srt_unpack_tiles_device", _i32, [_vp, _i32, _i32, _i32, _i64, _vp, _vp]),
 ]

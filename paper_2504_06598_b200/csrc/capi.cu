@@ -270,8 +270,8 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
-    if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 8), "stats alloc");
-    if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 8), "stats init");
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 16), "stats alloc");
+    if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 16), "stats init");
     if (!rc && n > 0) {
         // uploads are ordered on the scene's stream: cudaMemcpy from pageable
         // memory may return before the DMA lands, and the scene's stream does
@@ -1088,16 +1088,20 @@ srt_status srt_scene_check(const SrtScene *s, int32_t reset) {
     return SRT_ERR_STACK_OVERFLOW;
 }
 
-srt_status srt_trace_stats(const SrtScene *s, uint64_t *out, int32_t reset) {
-    if (!s || !out) {
-        set_error("null scene or output");
+srt_status srt_trace_counters(const SrtScene *s, uint64_t *out, int32_t n, int32_t reset) {
+    if (!s || !out || n < 1 || n > 16) {
+        set_error("null scene or output, or n outside 1..16");
         return SRT_ERR_INVALID_ARG;
     }
     DeviceGuard g(s->device);
     srt_status rc = cuda_status(cudaDeviceSynchronize(), "sync");
-    if (!rc) rc = cuda_status(cudaMemcpy(out, s->d_stats, sizeof(uint64_t) * 8, cudaMemcpyDeviceToHost), "stats");
-    if (!rc && reset) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(uint64_t) * 8), "stats reset");
+    if (!rc) rc = cuda_status(cudaMemcpy(out, s->d_stats, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost), "stats");
+    if (!rc && reset) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(uint64_t) * 16), "stats reset");
     return rc;
+}
+
+srt_status srt_trace_stats(const SrtScene *s, uint64_t *out, int32_t reset) {
+    return srt_trace_counters(s, out, 8, reset);
 }
 
 srt_status srt_unpack_tiles_device(const float *d_gathered, int32_t width, int32_t height, int32_t shard_count,

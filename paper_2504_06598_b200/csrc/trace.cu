@@ -70,14 +70,19 @@ struct Counters {
     __device__ __forceinline__ void add(int, unsigned) {}
     __device__ __forceinline__ void flush(unsigned long long *) {}
 };
+// Packet-kernel extras (warp-level, counted by lane 0): 8 visits with a leaf
+// child hit, 9 leaf children hit (any lane), 10 inner children hit (any lane),
+// 11 lanes with a hit per visit, 12 lanes without an accepted hit yet per
+// visit, 13 job rounds, 14 visits no lane hits anything.
+constexpr int kNumCounters = 16;
 template <>
 struct Counters<true> {
-    unsigned c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned c[kNumCounters] = {};
     __device__ __forceinline__ void add(int i, unsigned v) { c[i] += v; }
     __device__ __forceinline__ void flush(unsigned long long *out) {
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < kNumCounters; ++i)
             if (c[i]) atomicAdd(out + i, (unsigned long long)c[i]);
-        for (int i = 0; i < 8; ++i) c[i] = 0;
+        for (int i = 0; i < kNumCounters; ++i) c[i] = 0;
     }
 };
 
@@ -142,6 +147,12 @@ __device__ __forceinline__ float key_t(int key) {
 
 __device__ __forceinline__ int pick(const int4 &v, int k) {
     return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+// pick() for a run-time k as three selects (no branches)
+__device__ __forceinline__ int sel4(const int4 &v, int k) {
+    const int a = (k & 1) ? v.y : v.x;
+    const int b = (k & 1) ? v.w : v.z;
+    return (k & 2) ? b : a;
 }
 
 // Per-lane traversal state (registers + a local-memory stack).
@@ -863,6 +874,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
             __syncwarp();
             for (int jb = 0; jb < njobs; jb += 32) {
+                if (lane == 0) ct.add(13, 1);
                 int j = jb + lane;
                 if (j < njobs) {
                     const uint32_t job = sjob[wid][j];
@@ -935,12 +947,14 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             if (!mixed) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const float tn = fmaxf(fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
-                                                 fmaf(paz[k], r.idz, -r.oidz)), r.t_min);
+                    // entry not clamped to t_min: a box wholly before t_min may
+                    // pass (conservative), keys of boxes behind the origin sort first
+                    const float tn = fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
+                                           fmaf(paz[k], r.idz, -r.oidz));
                     const float tf = fminf(fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
                                                  fmaf(pbz[k], r.idz, -r.oidz)), far);
                     hitm |= tn <= tf ? (1u << k) : 0u;
-                    key[k] = (__float_as_int(tn) & ~3) | k;  // tn >= t_min >= 0: orderable as int
+                    key[k] = (__float_as_int(tn) & ~3) | k;  // orderable as an int when tn >= 0
                 }
             } else {
 #pragma unroll
@@ -956,11 +970,24 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             }
             const unsigned validm = hint & 15u, leafm = (hint >> 4) & 15u;
             hitm &= validm;  // empty slots: inverted boxes
-            const unsigned any = __reduce_or_sync(FULL, hitm);
             node = kDone;
+            if constexpr (STATS) {
+                const unsigned anyh = __reduce_or_sync(FULL, hitm);
+                const unsigned hl = __ballot_sync(FULL, hitm != 0u);
+                const unsigned nohit = __ballot_sync(FULL, valid && far == r.t_max0);
+                if (lane == 0) {
+                    ct.add(8, (anyh & leafm) ? 1u : 0u);
+                    ct.add(9, __popc(anyh & leafm));
+                    ct.add(10, __popc(anyh & ~leafm));
+                    ct.add(11, __popc(hl));
+                    ct.add(12, __popc(nohit));
+                    ct.add(14, anyh ? 0u : 1u);
+                }
+            }
             // leaf children any lane hits: one ballot each compacts the hitting
             // lanes into the job queue (jobs run in batches at the loop top:
             // deferring them only delays the far-bound clip, never a result)
+            const unsigned any = __reduce_or_sync(FULL, hitm);
             const unsigned lh = hitm & leafm, al = any & leafm;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -976,12 +1003,12 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             }
             // inner children any lane hits: descend into the nearest (warp-min
             // entry), push the others far-to-near with their warp-min entries
+            const unsigned ih = hitm & ~leafm;
             const unsigned ai = any & ~leafm;
             if (ai) {
                 if (!(ai & (ai - 1))) {
-                    node = pick(kids, __ffs(ai) - 1);  // one: nothing to order or push
+                    node = sel4(kids, __ffs(ai) - 1);  // one: nothing to order or push
                 } else {
-                    const unsigned ih = hitm & ~leafm;
                     int wk[4];
 #pragma unroll
                     for (int k = 0; k < 4; ++k) wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? key[k] : 0x7FFFFFFF);
@@ -999,16 +1026,15 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                         if (lane == 0) atomicExch(overflow, 1);
                         break;
                     }
-                    if (lane == 0) {
+                    // far-to-near: entries nin-1 .. 1 (unused sort slots hold INT_MAX)
 #pragma unroll
-                        for (int j = 3; j >= 1; --j)
-                            if (j < nin) {
-                                sstk_node[wid][sp + nin - 1 - j] = pick(kids, wk[j] & 3);
-                                sstk_key[wid][sp + nin - 1 - j] = wk[j] & ~3;
-                            }
-                    }
+                    for (int j = 3; j >= 1; --j)
+                        if (lane == 0 && j < nin) {
+                            sstk_node[wid][sp + nin - 1 - j] = sel4(kids, wk[j] & 3);
+                            sstk_key[wid][sp + nin - 1 - j] = wk[j] & ~3;
+                        }
                     sp += nin - 1;
-                    node = pick(kids, wk[0] & 3);
+                    node = sel4(kids, wk[0] & 3);
                 }
             }
             __syncwarp();
@@ -1137,11 +1163,18 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
     // 12% faster than the 90-register build at N=4 (3.16 vs 3.53 ms, C3)
     // resident blocks per SM requested from the register allocator, per slot
     // count: the largest without spills (N=8: +6%, N=16: +4% over unconstrained)
-    constexpr int kMinB = (NS == 1 || (NS == 2 && MODE == 0)) ? 8
-                          : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5));
+#ifndef SRT_N1_MINB
+#define SRT_N1_MINB 8
+#endif
+#ifndef SRT_N1_BATCH
+#define SRT_N1_BATCH 48
+#endif
+    constexpr int kMinB = NS == 1 ? SRT_N1_MINB
+                          : ((NS == 2 && MODE == 0) ? 8
+                             : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5)));
     // leaf jobs per batch: 48 for N=1 (1.964 vs 1.976 ms at 32) and N=4
     // (2.957 vs 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
-    constexpr int kBatch = (NS == 1 || (NS == 4 && MODE == 0)) ? 48 : 32;
+    constexpr int kBatch = NS == 1 ? SRT_N1_BATCH : ((NS == 4 && MODE == 0) ? 48 : 32);
     return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB>(s, src, w, st);
 }
 

@@ -314,10 +314,11 @@ class DeviceScene:
 
     def trace_stats(self, reset: bool = True) -> dict:
         """Traversal counters (collected only when SRT_TRACE_STATS=1 was set)."""
-        out = np.zeros(8, np.uint64)
-        check(_lib.load().srt_trace_stats(self.handle, _ptr(out), int(bool(reset))))
+        out = np.zeros(16, np.uint64)
+        check(_lib.load().srt_trace_counters(self.handle, _ptr(out), 16, int(bool(reset))))
         names = ("node_visits", "leaf_visits", "screen_pass", "exact_evals", "accepts", "pops", "culled_pops",
-                 "walks")
+                 "walks", "visits_with_leaf_hit", "leaf_children_hit", "inner_children_hit", "lanes_hitting",
+                 "lanes_without_hit", "job_rounds", "empty_visits", "unused")
         return dict(zip(names, (int(v) for v in out)))
 
     # device-pointer variants (bench.py, multi_gpu.py); pointers are ints
