@@ -288,6 +288,12 @@ struct Screen {
     float t_lo;      // lower bound of the candidate depth
     float alpha_hi;  // upper bound of alpha
     bool maybe;      // could be a valid candidate inside (t_min, far]
+    // decided by the screen alone (no exact stage): the candidate is valid
+    // for certain (dAd > 0, mah + error <= s^2, t +- error inside the open
+    // interval) and alpha >= alpha_lo; t is the screen's depth estimate
+    bool sure;
+    float alpha_lo;
+    float t;
 };
 
 // Minimal fp32 ray for the screen (camera rays share one origin).
@@ -340,7 +346,13 @@ __device__ __forceinline__ Screen screen(const R &r, const float4 &m, const floa
     float mt = e + es * rs + 2.0e-6f * (fabsf(t) + 1.0f);
     sc.t_lo = t - mt;
     sc.maybe = (dad > 0.0f) && (mah - mr <= s2) && (t - mt <= far) && (t + mt > r.t_min) && (t - mt < r.t_max0);
-    sc.alpha_hi = m.w * __expf(-0.5f * fmaxf(resid - mr, 0.0f)) * 1.0001f + 1e-7f;
+    const float ea = __expf(-0.5f * fmaxf(resid - mr, 0.0f));
+    sc.alpha_hi = m.w * ea * 1.0001f + 1e-7f;
+    // lower bound of alpha: the same error terms the other way (exp(-mr)
+    // widens the band by the residual's bound; the opacity is fp32-rounded)
+    sc.alpha_lo = m.w * ea * __expf(-mr) * 0.9999f - 1e-7f;
+    sc.sure = (dad > 0.0f) && isfinite(dad) && (mah + mr <= s2) && (t - mt > r.t_min) && (t + mt < r.t_max0);
+    sc.t = t;
     return sc;
 }
 

@@ -596,6 +596,28 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
         if (sc.t_lo <= unpack_t(best[k]))
             need |= (NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid)) <= sc.alpha_hi;
     if (!need) return;
+    if (sc.sure) {
+        // Valid for certain and every draw outside [alpha_lo, alpha_hi]: the
+        // screen decides (u < alpha_lo <= alpha: accepted, at the screen's
+        // depth, ~1e-6 from the exact one).  Only draws inside the error band
+        // -- a few in 1e4 -- need the exact stage, which keeps the divergent
+        // fp64 code off the common path.
+        const unsigned long long key = pack_hit(sc.t, pid);
+        bool band = false;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            const float u = NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid);
+            if (u < sc.alpha_lo) {
+                if (key < best[k]) {
+                    atomicMin(best + k, key);
+                    ct.add(4, 1);
+                }
+            } else {
+                band |= u <= sc.alpha_hi;
+            }
+        }
+        if (!band) return;
+    }
     ct.add(3, 1);
     // the camera ray's fields the exact candidate reads; camera directions are
     // unit in fp64 to an ulp, and 1/|d|^2 only sets the re-centring point,
