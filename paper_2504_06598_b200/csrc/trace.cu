@@ -1010,18 +1010,16 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             // lanes into the job queue (jobs run in batches at the loop top:
             // deferring them only delays the far-bound clip, never a result)
             const unsigned any = __reduce_or_sync(FULL, hitm);
-            const unsigned lh = hitm & leafm, al = any & leafm;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (al & (1u << k)) {
-                    const bool h = (lh >> k) & 1u;
-                    const unsigned bm = __ballot_sync(FULL, h);
-                    if (h) {
-                        SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
-                        sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~pick(kids, k) << 5) | (uint32_t)lane;
-                    }
-                    njobs += __popc(bm);
+            const unsigned lh = hitm & leafm;
+            for (unsigned al = any & leafm; al; al &= al - 1) {
+                const int k = __ffs(al) - 1;
+                const bool h = (lh >> k) & 1u;
+                const unsigned bm = __ballot_sync(FULL, h);
+                if (h) {
+                    SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
+                    sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
                 }
+                njobs += __popc(bm);
             }
             // inner children any lane hits: descend into the nearest (warp-min
             // entry), push the others far-to-near with their warp-min entries
