@@ -98,20 +98,30 @@ __device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r
     if (!sc.maybe) return;
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
-    bool need = false;
+    bool need = false, band = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         if (sc.t_lo <= sl.t[k]) {
-            float u = RNG == SRT_RNG_TABLE ? (float)__ldg(w.table + (int64_t)pid * w.tstride + k)
-                                           : counter_u(sl.key[k], (uint32_t)pid);
-            need |= u <= sc.alpha_hi;
+            const double u = RNG == SRT_RNG_TABLE ? __ldg(w.table + (int64_t)pid * w.tstride + k)
+                                                  : (double)counter_u(sl.key[k], (uint32_t)pid);
+            need |= u <= (double)sc.alpha_hi;
+            band |= u >= (double)sc.alpha_lo && u <= (double)sc.alpha_hi;
         }
     }
     if (!need) return;
-    ct.add(3, 1);
-    // stage 2: exact evaluation (fp64 re-centring, kernels.py:139-189)
-    Cand c = candidate<MODE>(r, m, a, b, w.s2);
-    if (!c.valid) return;
+    Cand c;
+    if (sc.sure && !band) {
+        // decided by the screen (see packet_job): valid for certain, every
+        // relevant draw below alpha_lo or above alpha_hi
+        c.t = sc.t;
+        c.alpha = sc.alpha_lo;
+        c.valid = 1;
+    } else {
+        ct.add(3, 1);
+        // stage 2: exact evaluation (fp64 re-centring, kernels.py:139-189)
+        c = candidate<MODE>(r, m, a, b, w.s2);
+        if (!c.valid) return;
+    }
     bool improved = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -542,19 +552,27 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
     if (!sc.maybe) return;
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
-    bool need = false;
+    bool need = false, band = false;
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         if (sc.t_lo <= unpack_t(best[k])) {
-            float u = RNG == SRT_RNG_TABLE ? (float)__ldg(w.table + (int64_t)pid * w.tstride + k)
-                                           : counter_u(keys[k], (uint32_t)pid);
-            need |= u <= sc.alpha_hi;
+            const double u = RNG == SRT_RNG_TABLE ? __ldg(w.table + (int64_t)pid * w.tstride + k)
+                                                  : (double)counter_u(keys[k], (uint32_t)pid);
+            need |= u <= (double)sc.alpha_hi;
+            band |= u >= (double)sc.alpha_lo && u <= (double)sc.alpha_hi;
         }
     }
     if (!need) return;
-    ct.add(3, 1);
-    Cand c = candidate<MODE>(r, m, a, b, w.s2);
-    if (!c.valid) return;
+    Cand c;
+    if (sc.sure && !band) {
+        c.t = sc.t;  // decided by the screen (see packet_job)
+        c.alpha = sc.alpha_lo;
+        c.valid = 1;
+    } else {
+        ct.add(3, 1);
+        c = candidate<MODE>(r, m, a, b, w.s2);
+        if (!c.valid) return;
+    }
     unsigned long long key = pack_hit(c.t, pid);
 #pragma unroll
     for (int k = 0; k < NS; ++k)
