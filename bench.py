@@ -7,8 +7,10 @@ BASELINE.md section 3), on N B200s, beside the reference CPU renderer.
 N > 1: one process per GPU.  Under torchrun (RANK / WORLD_SIZE set) each rank
 is one GPU; without it ``bench.py --gpus N`` re-launches itself under
 ``torch.distributed.run`` on 127.0.0.1.  Each rank traces the 16x16 tiles
-t with t % N == rank (fused walk + SH shade), the tile-compact shards are
-gathered to rank 0 with one NCCL gather per frame and unpacked there.
+t with t % N == rank (fused walk + SH shade) and stores its pixels straight
+into one frame in rank 0's HBM (CUDA IPC over NVLink: the frame assembly
+overlaps the walk); one tiny all-reduce per frame marks it complete.  Without
+IPC the tile-compact shards go to rank 0 with one NCCL gather + unpack.
 
 One JSON line on rank 0.  "value" = whole-job Mrays/s with the scene resident
 in HBM, timed on the device with CUDA events (max over ranks).  "e2e" = the
@@ -359,19 +361,39 @@ def run_ours(args) -> None:
 
     asset, sc, setup_s, build_s = scene_for(0)
 
+    # N > 1: every rank stores its tiles straight into one frame in rank 0's
+    # HBM (CUDA IPC over NVLink, multi_gpu.PeerFrame) and one tiny all-reduce
+    # per frame tells rank 0 the frame is complete; without IPC, the tile-
+    # compact shards are gathered to rank 0 with NCCL and unpacked there
+    peer = None
+    if world > 1:
+        from paper_2504_06598_b200.multi_gpu import PeerFrame
+
+        peer = PeerFrame(WIDTH * HEIGHT * 16, rank, local)
+        if not peer.ok:
+            peer = None
+    done_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+
     def step(scene, ev=None):
         if ev is not None:
             ev[0].record(stream)
         for f in range(st.passes):
             # one fused kernel per pass: packet walk + SH shade + accumulate
-            scene.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), sp)
+            if peer is not None:
+                scene.render_pass_frame_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, peer.ptr,
+                                               rank > 0, sp)
+            else:
+                scene.render_pass_device(cam, prm, f, acc.data_ptr(), f == 0, f == st.passes - 1, out.data_ptr(), sp)
         if ev is not None:
             ev[1].record(stream)
         if world > 1:
-            dist.gather(out, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
+            if peer is not None:
+                dist.all_reduce(done_flag)  # stream-ordered after every rank's fenced kernel
+            else:
+                dist.gather(out, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
             if ev is not None:
                 ev[2].record(stream)
-            if rank == 0:
+            if rank == 0 and peer is None:
                 unpack_tiles_device(gathered.data_ptr(), WIDTH, HEIGHT, world, max_tiles, frame.data_ptr(), sp)
         if ev is not None:
             ev[3].record(stream)
@@ -492,7 +514,9 @@ def run_ours(args) -> None:
             "metric": "Mrays/s", "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(CONFIG),
-            "parallelism": f"tile-shard x{world}" + (" + NCCL gather to rank 0" if world > 1 else ""),
+            "parallelism": f"tile-shard x{world}" + ("" if world == 1 else (
+                " + fused peer stores into rank 0's frame (CUDA IPC over NVLink) + one all-reduce per frame"
+                if peer is not None else " + NCCL gather to rank 0 + unpack")),
             "setup": {"scene_setup_s": setup_s, "bvh_build_s": build_s, "bvh": sc.bvh_info(), "build_id": build_id,
                       "wall_s_timed_region": wall},
             "ranks": [{"rank": i, "step_ms": r[0], "walk_ms": r[1], "gather_ms": r[2], "unpack_ms": r[3],
@@ -502,11 +526,14 @@ def run_ours(args) -> None:
             "roofline_issue": issue,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * st.passes + (args.steps if world > 1 else 0),
+            "gpu_launches": args.steps * st.passes + (args.steps if (world > 1 and peer is None) else 0),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
+        if peer is not None:
+            peer.close()
         dist.barrier()
         dist.destroy_process_group()
 

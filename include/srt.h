@@ -251,6 +251,23 @@ srt_status srt_shade_pass_device(const SrtScene *scene, const SrtCamera *camera,
 srt_status srt_render_pass_device(const SrtScene *scene, const SrtCamera *camera,
                                   const SrtRenderParams *params, int32_t pass, float *d_accum,
                                   int32_t first, int32_t last, float *d_out, void *stream);
+/* srt_render_pass_device writing the ROW-MAJOR full (H*W) float4 frame even
+ * for a shard: each shard stores only its own pixels, so several GPUs can
+ * assemble one frame in place.  d_frame may be a peer GPU's buffer (CUDA IPC,
+ * srt_ipc_open): with peer != 0 the kernel ends with a system-scope fence, so
+ * its stores are visible to the peer before any later signal from this GPU
+ * (e.g. a collective on the same stream). */
+srt_status srt_render_pass_frame_device(const SrtScene *scene, const SrtCamera *camera,
+                                        const SrtRenderParams *params, int32_t pass, float *d_accum,
+                                        int32_t first, int32_t last, float *d_frame, int32_t peer,
+                                        void *stream);
+/* Device buffers shared between processes (one rank per GPU): srt_ipc_alloc
+ * allocates on `device` and returns a 64-byte handle, srt_ipc_open maps a
+ * handle from another process on `device` (peer access over NVLink). */
+srt_status srt_ipc_alloc(int32_t device, int64_t bytes, void **d_ptr, uint8_t *handle);
+srt_status srt_ipc_open(int32_t device, const uint8_t *handle, void **d_ptr);
+srt_status srt_ipc_close(int32_t device, void *d_ptr);
+srt_status srt_ipc_free(int32_t device, void *d_ptr);
 /* Whole frame on device: all passes, d_out (H*W) float4 rgba means. */
 /* All params->passes passes of a frame in ONE launch over every (packet,
  * pass): samples are summed in 2^-32 fixed point with integer atomics (order

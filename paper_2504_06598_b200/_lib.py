@@ -101,6 +101,12 @@ SYMBOLS = [
     ("srt_render_frame_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp,
                                        _vp]),
     ("srt_resolve_frame_device", _i32, [ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp, _vp]),
+    ("srt_render_pass_frame_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _i32,
+                                            _vp, _i32, _i32, _vp, _i32, _vp]),
+    ("srt_ipc_alloc", _i32, [_i32, _i64, ctypes.POINTER(_vp), _vp]),
+    ("srt_ipc_open", _i32, [_i32, _vp, ctypes.POINTER(_vp)]),
+    ("srt_ipc_close", _i32, [_i32, _vp]),
+    ("srt_ipc_free", _i32, [_i32, _vp]),
     ("srt_render_device", _i32, [_vp, ctypes.POINTER(SrtCamera), ctypes.POINTER(SrtRenderParams), _vp, _vp, _vp,
                                  _vp]),
     ("srt_scene_check", _i32, [_vp, _i32]),

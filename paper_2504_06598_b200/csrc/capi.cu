@@ -898,6 +898,68 @@ srt_status srt_render_pass_device(const SrtScene *s, const SrtCamera *camera, co
                                     last != 0, (float4 *)d_out, (cudaStream_t)stream);
 }
 
+srt_status srt_render_pass_frame_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p,
+                                        int32_t pass, float *d_accum, int32_t first, int32_t last, float *d_frame,
+                                        int32_t peer, void *stream) {
+    srt_status rc = validate_render(s, p);
+    if (rc) return rc;
+    if (!camera || !d_accum || (last && !d_frame)) {
+        set_error("null camera or buffer");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (p->rng == SRT_RNG_TRIG64) {
+        set_error("the fused pass draws the counter stream");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(s->device);
+    return launch_render_pass_fused(s, make_cam(camera), make_render_args(p), pass, (float4 *)d_accum, first != 0,
+                                    last != 0, (float4 *)d_frame, (cudaStream_t)stream, nullptr, nullptr, nullptr,
+                                    true, peer != 0);
+}
+
+srt_status srt_ipc_alloc(int32_t device, int64_t bytes, void **d_ptr, uint8_t *handle) {
+    if (!d_ptr || !handle || bytes <= 0) {
+        set_error("invalid IPC allocation");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(device);
+    *d_ptr = nullptr;
+    srt_status rc = cuda_status(cudaMalloc(d_ptr, (size_t)bytes), "IPC buffer");
+    cudaIpcMemHandle_t h;
+    if (!rc) rc = cuda_status(cudaIpcGetMemHandle(&h, *d_ptr), "cudaIpcGetMemHandle");
+    if (rc) {
+        if (*d_ptr) cudaFree(*d_ptr);
+        *d_ptr = nullptr;
+        return rc;
+    }
+    std::memcpy(handle, &h, sizeof(h));
+    return SRT_OK;
+}
+
+srt_status srt_ipc_open(int32_t device, const uint8_t *handle, void **d_ptr) {
+    if (!d_ptr || !handle) {
+        set_error("invalid IPC handle");
+        return SRT_ERR_INVALID_ARG;
+    }
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    *d_ptr = nullptr;
+    return cuda_status(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+srt_status srt_ipc_close(int32_t device, void *d_ptr) {
+    if (!d_ptr) return SRT_OK;
+    DeviceGuard g(device);
+    return cuda_status(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+}
+
+srt_status srt_ipc_free(int32_t device, void *d_ptr) {
+    if (!d_ptr) return SRT_OK;
+    DeviceGuard g(device);
+    return cuda_status(cudaFree(d_ptr), "cudaFree");
+}
+
 srt_status srt_render_device(const SrtScene *s, const SrtCamera *camera, const SrtRenderParams *p, int32_t *d_hits,
                              float *d_accum, float *d_out, void *stream) {
     srt_status rc = validate_render(s, p);

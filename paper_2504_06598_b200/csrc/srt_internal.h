@@ -110,7 +110,8 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
                              cudaStream_t st);
 srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                                    float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
-                                   int32_t *d_hits = nullptr, double *d_rgb64 = nullptr, double *d_op64 = nullptr);
+                                   int32_t *d_hits = nullptr, double *d_rgb64 = nullptr, double *d_op64 = nullptr,
+                                   bool out_rowmajor = false, bool sys_fence = false);
 srt_status launch_render_frame_multipass(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass0,
                                          int npass, unsigned long long *d_acc64, cudaStream_t st);
 srt_status launch_resolve_fixed(const RenderArgs &a, const unsigned long long *d_acc, int npass, float4 *d_out,

@@ -346,6 +346,14 @@ struct CameraSource {
     float4 *out;
     double *rgb64, *op64;  // optional final f64 frame (e.g. mapped page-locked host memory)
     int first, last;
+    // out is the row-major full frame even for a shard (multi-GPU frames
+    // assembled in place: out may be a peer GPU's buffer, CUDA IPC over
+    // NVLink), and the kernel ends with a system-scope fence so the stores
+    // are visible to the peer before any later signal of this GPU
+    int out_rowmajor, sys_fence;
+    __device__ __forceinline__ void done() const {
+        if (sys_fence) __threadfence_system();
+    }
     template <int NS>
     __device__ __forceinline__ void finish(uint32_t idx, const Slots<NS> &sl) const {
         int32_t *h = hits + (int64_t)idx * a.nslots + slot0;
@@ -407,7 +415,7 @@ struct CameraSource {
                 op64[pix] = (double)(acc.w * inv);
                 return;
             }
-            int64_t oidx = a.shard_count > 1 ? (int64_t)idx : (int64_t)py * a.width + px;
+            int64_t oidx = (a.shard_count > 1 && !out_rowmajor) ? (int64_t)idx : (int64_t)py * a.width + px;
             out[oidx] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
         } else {
             accum[idx] = acc;
@@ -453,6 +461,7 @@ struct ArraySource {
                                                   float) const {
         finish<NS>(idx, sl);
     }
+    __device__ __forceinline__ void done() const {}
 };
 
 // Explicit rays that point into one hemisphere (camera batches, the
@@ -1088,6 +1097,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
         }
         __syncwarp();
     }
+    src.done();
     ct.flush(stats);
 }
 
@@ -1296,7 +1306,8 @@ static uint32_t frame_key_host(uint32_t seed) {
 
 srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const RenderArgs &a, int pass,
                                    float4 *d_accum, bool first, bool last, float4 *d_out, cudaStream_t st,
-                                   int32_t *d_hits, double *d_rgb64, double *d_op64) {
+                                   int32_t *d_hits, double *d_rgb64, double *d_op64, bool out_rowmajor,
+                                   bool sys_fence) {
     if ((uint64_t)a.local_tiles * 256 > kMaxLaunchItems) {
         set_error("frame too large for one launch");
         return SRT_ERR_INVALID_ARG;
@@ -1316,6 +1327,8 @@ srt_status launch_render_pass_fused(const SrtScene *s, const CamD &cam, const Re
     src.pass = pass;
     src.fkey = 0;
     src.hits = d_hits;
+    src.out_rowmajor = out_rowmajor ? 1 : 0;
+    src.sys_fence = sys_fence ? 1 : 0;
     src.fkey = frame_key_host(a.seed);  // frame_key() of the device code, on the host
     WalkCfg w{a.s2, sqrtf(a.s2), a.clip, nullptr, 0};
     srt_status rc = SRT_OK;
@@ -1369,6 +1382,8 @@ static srt_status launch_multipass_chunk(const SrtScene *s, const CamD &cam, con
     src.a = a;
     src.pass = pass0;
     src.hits = nullptr;
+    src.out_rowmajor = 0;
+    src.sys_fence = 0;
     src.acc64 = d_acc64;
     src.unit = (uint32_t)(a.local_tiles * 256);
     src.npass = (uint32_t)npass;

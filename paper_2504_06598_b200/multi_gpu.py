@@ -295,6 +295,64 @@ def gpu_shard_renderer(scene, camera_tuple, settings, device):
 
 
 # ---------------------------------------------------------------------------
+# one device frame every rank stores into (multi-GPU frames on rank 0's GPU)
+# ---------------------------------------------------------------------------
+
+class PeerFrame:
+    """A row-major (H*W) float4 frame in rank 0's HBM that every rank maps
+    with CUDA IPC (srt_ipc_alloc / srt_ipc_open): each rank's fused walk
+    stores its own tiles' pixels straight into it over NVLink
+    (srt_render_pass_frame_device), so the frame gather of the NCCL path
+    and its unpack kernel disappear -- the transfer overlaps the walk, tile
+    by tile.  Collective construction; ``ok`` is False on every rank when
+    any rank could not map the buffer (callers then fall back to the NCCL
+    gather).  ``ptr`` is the device address valid on this rank."""
+
+    def __init__(self, nbytes: int, rank: int, device: int, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        L = _lib.load()
+        self.rank, self.device, self.ptr, self._owned = rank, device, 0, False
+        p = ctypes.c_void_p()
+        err = ""
+        box = [None]
+        if rank == 0:
+            h = (ctypes.c_uint8 * 64)()
+            if L.srt_ipc_alloc(device, int(nbytes), ctypes.byref(p), h) == 0:
+                self.ptr, self._owned = p.value, True
+                box = [bytes(h)]
+            else:
+                err = L.srt_last_error().decode(errors="replace")
+        dist.broadcast_object_list(box, src=0, group=group)
+        if rank != 0 and box[0] is not None:
+            h = (ctypes.c_uint8 * 64).from_buffer_copy(box[0])
+            if L.srt_ipc_open(device, h, ctypes.byref(p)) == 0:
+                self.ptr = p.value
+            else:
+                err = L.srt_last_error().decode(errors="replace")
+        dev = torch.device("cuda", device) if dist.get_backend(group) == "nccl" else "cpu"
+        flag = torch.tensor([1 if self.ptr else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        self.ok = bool(flag.item())
+        self.error = err
+        if not self.ok:
+            self.close()
+
+    def close(self) -> None:
+        from . import _lib
+
+        if self.ptr:
+            L = _lib.load()
+            (L.srt_ipc_free if self._owned else L.srt_ipc_close)(self.device, __import__("ctypes").c_void_p(self.ptr))
+        self.ptr = 0
+
+
+# ---------------------------------------------------------------------------
 # one host frame shared by every rank (multi-GPU e2e)
 # ---------------------------------------------------------------------------
 

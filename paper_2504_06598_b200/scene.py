@@ -338,6 +338,15 @@ class DeviceScene:
                                                  int(pass_index), ctypes.c_void_p(d_accum), int(bool(first)),
                                                  int(bool(last)), ctypes.c_void_p(d_out), ctypes.c_void_p(stream)))
 
+    def render_pass_frame_device(self, camera, prm, pass_index, d_accum, first, last, d_frame, peer, stream) -> None:
+        """srt_render_pass_frame_device: the fused pass writing the row-major
+        full frame (a shard writes only its pixels; d_frame may be a peer
+        GPU's IPC-mapped buffer when peer is set)."""
+        check(_lib.load().srt_render_pass_frame_device(self.handle, ctypes.byref(camera), ctypes.byref(prm),
+                                                       int(pass_index), ctypes.c_void_p(d_accum), int(bool(first)),
+                                                       int(bool(last)), ctypes.c_void_p(d_frame), int(bool(peer)),
+                                                       ctypes.c_void_p(stream)))
+
     def render_frame_device(self, camera, prm, d_acc, d_out, stream) -> None:
         """srt_render_frame_device: every pass of the frame in one launch;
         d_acc: (local tiles * 256, 4) uint64 scratch, d_out: float4 means."""

@@ -552,3 +552,34 @@ def test_one_launch_frame_vs_oracle(oracle, w, h, spp, nslots):
     ok = np.all(np.abs(got.rgb - ref["rgb"]) <= 1e-5 * np.abs(ref["rgb"]) + 1e-6, axis=2)
     ok &= np.abs(got.opacity - ref["opacity"]) <= 1e-12
     assert ok.mean() >= 0.99, ok.mean()
+
+
+def test_shards_store_into_one_rowmajor_frame():
+    """srt_render_pass_frame_device: every tile shard (t % G == rank) stores
+    its pixels straight into ONE row-major frame -- the in-place multi-GPU
+    assembly of bench.py / multi_gpu.PeerFrame -- and the result equals the
+    single-shard frame bit for bit (here all shards on one device)."""
+    import torch
+
+    from paper_2504_06598_b200 import RenderSettings, front_camera
+    from paper_2504_06598_b200.render import prepare
+    from paper_2504_06598_b200.scene import camera_tuple, make_camera, make_render_params, shard_tiles
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    asset = random_cloud(6_000, seed=3, sh_degree=2)
+    w, h = 150, 70
+    st = RenderSettings(width=w, height=h, spp=1)
+    sc = prepare(asset, st)
+    cam = make_camera(camera_tuple(front_camera(), w, h))
+    stream = torch.cuda.current_stream().cuda_stream
+    acc = torch.empty(shard_tiles(w, h) * 256 * 4, device="cuda")
+    full = torch.zeros(w * h * 4, device="cuda")
+    sc.render_pass_device(cam, make_render_params(w, h, 1, 1, 0, S2), 0, acc.data_ptr(), True, True,
+                          full.data_ptr(), stream)
+    for G in (2, 3, 8):
+        frame = torch.full((w * h * 4,), -1.0, device="cuda")
+        for r in range(G):
+            prm = make_render_params(w, h, 1, 1, 0, S2, shard_index=r, shard_count=G)
+            sc.render_pass_frame_device(cam, prm, 0, acc.data_ptr(), True, True, frame.data_ptr(), r > 0, stream)
+        torch.cuda.synchronize()
+        assert torch.equal(frame, full), G
