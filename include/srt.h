@@ -167,7 +167,7 @@ srt_status srt_bvh_download(const SrtScene *scene, float *node_lo, float *node_h
  * whose directions share a hemisphere (camera batches, parallel jittered
  * rays) are walked as warp packets; others per lane (sorted when large).
  * The route never changes a result; env SRT_PACKET_RAYS=0/1 pins it.
- * nslots <= 256 (walked as slot groups of <= 16). */
+ * nslots <= 256 (walked as slot groups of <= 8). */
 srt_status srt_trace_rays(const SrtScene *scene, const SrtTraceParams *params,
                           const double *origins, const double *dirs, int64_t num_rays,
                           int32_t nslots, double *out_t, int64_t *out_id);

@@ -307,7 +307,7 @@ struct CameraSource {
     // deterministic -- and the whole frame is one balanced launch.
     unsigned long long *acc64;
     uint32_t npass, unit;
-    // Slot group (multisample N > 16 walks as groups of <= 16 slots): this
+    // Slot group (multisample N > 8 walks as groups of <= 8 slots): this
     // launch walks slots slot0 .. slot0 + gslots - 1 of the a.nslots; slot
     // slot0 + k draws sample pass * N + slot0 + k (kernels.py:353-364 keeps
     // every slot independent, so the split never changes a result).
@@ -1271,9 +1271,8 @@ static srt_status dispatch(const SrtScene *s, const Src &src, const WalkCfg &w, 
     if (nslots <= 2) SRT_NS(2)
     if (nslots <= 4) SRT_NS(4)
     if (nslots <= 8) SRT_NS(8)
-    if (nslots <= 16) SRT_NS(16)
 #undef SRT_NS
-    set_error("nslots > 16 is not supported by the GPU tracer yet");
+    set_error("a walk holds at most 8 slots (callers split larger N into slot groups)");
     return SRT_ERR_UNSUPPORTED;
 }
 
@@ -1290,9 +1289,11 @@ srt_status launch_trace_pass(const SrtScene *s, const CamD &cam, const RenderArg
 // launch stays far below 2^32 items and the counter can never wrap.
 constexpr uint64_t kMaxLaunchItems = 1ull << 31;
 
-// Slots per walk: multisample N > 16 runs as ceil(N / 16) walks of <= 16
-// slots over the same ray (CameraSource::slot0).
-constexpr int kSlotGroup = 16;
+// Slots per walk: multisample N > 8 runs as ceil(N / 8) walks of <= 8 slots
+// over the same ray (CameraSource::slot0).  Two 8-slot walks beat one 16-slot
+// walk (3.88 vs 2.95 G samples/s at 1080p in the 1M cloud): the 16-slot walk
+// keeps its slots in local memory.
+constexpr int kSlotGroup = 8;
 
 static uint32_t frame_key_host(uint32_t seed) {
     uint32_t x = seed ^ 0x9E3779B9u;
@@ -1565,8 +1566,8 @@ srt_status launch_trace_rays(const SrtScene *s, const SrtTraceParams *p, const d
     }
     WalkCfg w{(float)p->s2, (float)std::sqrt(p->s2), p->clip, d_table, p->table_slots};
     srt_status rc = SRT_OK;
-    // More than 16 slots: walks of <= 16 slots each, slot group g drawing
-    // samples sample0 + 16 g + k (or table columns 16 g + k).  Slots are independent --
+    // More than 8 slots: walks of <= 8 slots each (kSlotGroup), slot group g
+    // drawing samples sample0 + 8 g + k (or table columns 8 g + k).  Slots are independent --
     // the clip only culls entries beyond the farthest slot bound, so a slot's
     // closest accepted hit never depends on the others -- and the groups
     // write disjoint columns of the (R, nslots) outputs.

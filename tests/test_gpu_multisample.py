@@ -1,9 +1,10 @@
-"""multisample N > 16 (the reference allows N <= 256: config.py:18,79-80, the
+"""multisample N > 8 (the reference allows N <= 256: config.py:18,79-80, the
 slot loop of kernels.py:353-364) through frames and explicit rays, and frames
 whose (pixel, pass) work items exceed one persistent launch.
 
-A walk holds at most 16 slots; N > 16 runs as ceil(N/16) walks of <= 16 slots
-over the same ray, slot 16 g + k drawing sample pass * N + 16 g + k.  Every
+A walk holds at most 8 slots; N > 8 runs as ceil(N/8) walks of <= 8 slots
+over the same ray, slot 8 g + k drawing sample pass * N + 8 g + k (the trig64
+walk uses groups of 16, hashing slot index 16 g + k).  Every
 slot is independent (the clip culls only beyond the farthest slot bound), so
 the split reproduces the N-slot walk of the reference exactly.
 """
@@ -91,7 +92,7 @@ def test_single_pass_multisample_beyond_16_mapped_and_device_paths_agree():
 @pytest.mark.parametrize("rng", ["table", "trig64"])
 def test_trace_batch_beyond_16_slots_table_and_trig64(oracle, rng):
     """Explicit rays with N = 20 slots under scripted uniforms (table columns
-    16 g + k) and under the reference's own trig-hash draw (slot index 16 g + k
+    8 g + k) and under the reference's own trig-hash draw (slot index 16 g + k
     in the hash, kernels.py:354)."""
     from paper_2504_06598_b200.scene import DeviceScene
     from paper_2504_06598_b200.synthetic import random_cloud

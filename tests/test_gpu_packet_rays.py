@@ -163,7 +163,7 @@ def test_transmittance_routes_agree(monkeypatch):
 
 @pytest.mark.parametrize("kind,nslots", [("random", 40), ("camera", 33), ("camera", 256)])
 def test_trace_rays_beyond_16_slots(oracle, kind, nslots):
-    """Slot groups of <= 16 (sample0 + 16 g + k): identical to one walk of
+    """Slot groups of <= 8 (sample0 + 8 g + k): identical to one walk of
     all slots, since each slot's closest accepted hit is independent."""
     a, sc = _scene(8_000, 14)
     if kind == "random":
