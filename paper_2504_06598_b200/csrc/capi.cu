@@ -129,22 +129,21 @@ CamD make_cam(const SrtCamera *c) {
     return d;
 }
 
+// The flag lives in mapped host memory: synchronise, then read it directly.
 srt_status check_flag(const SrtScene *s, cudaStream_t st) {
-    int flag = 0;
-    srt_status rc = cuda_status(cudaMemcpyAsync(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st), "flag read");
+    srt_status rc = cuda_status(cudaStreamSynchronize(st), "stream sync");
     if (rc) return rc;
-    rc = cuda_status(cudaStreamSynchronize(st), "stream sync");
-    if (rc) return rc;
-    if (flag) {
-        cudaMemsetAsync(s->d_flag, 0, sizeof(int), st);
+    if (*(volatile int32_t *)s->h_flag) {
+        *(volatile int32_t *)s->h_flag = 0;
         set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
         return SRT_ERR_STACK_OVERFLOW;
     }
     return SRT_OK;
 }
 
-srt_status clear_flag(const SrtScene *s, cudaStream_t st) {
-    return cuda_status(cudaMemsetAsync(s->d_flag, 0, sizeof(int), st), "flag reset");
+srt_status clear_flag(const SrtScene *s, cudaStream_t) {
+    *(volatile int32_t *)s->h_flag = 0;  // host memory: no stream operation
+    return SRT_OK;
 }
 
 static srt_status validate_render(const SrtScene *s, const SrtRenderParams *p) {
@@ -268,8 +267,13 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
     srt_status rc = SRT_OK;
     std::vector<float> shf;
     rc = cuda_status(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "stream create");
-    if (!rc) rc = cuda_status(cudaMalloc(&s->d_flag, sizeof(int)), "flag alloc");
-    if (!rc) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag init");
+    if (!rc) rc = cuda_status(cudaHostAlloc(&s->h_flag, sizeof(int32_t), cudaHostAllocMapped), "flag alloc");
+    if (!rc) {
+        *s->h_flag = 0;
+        rc = cuda_status(cudaHostGetDevicePointer(&s->d_flag, s->h_flag, 0), "flag map");
+    }
+    if (!rc) rc = cuda_status(cudaMalloc(&s->d_counter, 128), "work counter alloc");
+    if (!rc) rc = cuda_status(cudaMemset(s->d_counter, 0, 128), "work counter init");
     if (!rc) rc = cuda_status(cudaMalloc(&s->d_stats, sizeof(unsigned long long) * 16), "stats alloc");
     if (!rc) rc = cuda_status(cudaMemset(s->d_stats, 0, sizeof(unsigned long long) * 16), "stats init");
     if (!rc && n > 0) {
@@ -343,7 +347,8 @@ srt_status srt_scene_destroy(SrtScene *s) {
     cudaFree(s->d_nodes4);
     cudaFree(s->d_nodes8);
     cudaFree(s->d_stats);
-    cudaFree(s->d_flag);
+    if (s->h_flag) cudaFreeHost(s->h_flag);
+    cudaFree(s->d_counter);
     cudaFree(s->d_scratch);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
@@ -1140,12 +1145,9 @@ srt_status srt_scene_check(const SrtScene *s, int32_t reset) {
     }
     DeviceGuard g(s->device);
     srt_status rc = cuda_status(cudaDeviceSynchronize(), "sync");
-    int flag = 0;
-    if (!rc) rc = cuda_status(cudaMemcpy(&flag, s->d_flag, sizeof(int), cudaMemcpyDeviceToHost), "flag read");
     if (rc) return rc;
-    if (!flag) return SRT_OK;
-    if (reset) rc = cuda_status(cudaMemset(s->d_flag, 0, sizeof(int)), "flag reset");
-    if (rc) return rc;
+    if (!*(volatile int32_t *)s->h_flag) return SRT_OK;
+    if (reset) *(volatile int32_t *)s->h_flag = 0;
     set_error("traversal stack overflow (BVH deeper than the 128-entry stack)");
     return SRT_ERR_STACK_OVERFLOW;
 }

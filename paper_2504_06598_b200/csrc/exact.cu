@@ -50,7 +50,7 @@ __device__ __forceinline__ void for_each_leaf(const SceneView &s, const RayState
             if (!(tn <= tf) || tf < lo) continue;
             if (kid[k] >= 0) {
                 if (sp >= kStackSize) {
-                    atomicExch(overflow, 1);
+                    raise_flag(overflow);
                     return;
                 }
                 stk[sp++] = kid[k];

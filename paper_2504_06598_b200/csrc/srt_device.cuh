@@ -61,6 +61,11 @@ struct __align__(16) Geom {
     } while (0)
 #endif
 
+// Device error flag (traversal stack overflow): one int in mapped page-locked
+// host memory, set with a plain store (idempotent), read by the host after
+// the stream synchronises -- no device->host copy, no memset on the stream.
+__device__ __forceinline__ void raise_flag(int *flag) { *(volatile int *)flag = 1; }
+
 struct SceneView {
     const double *means64;  // fp64 records in original id order (trig64 bridge mode)
     const double *cov64;

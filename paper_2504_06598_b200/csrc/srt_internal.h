@@ -30,7 +30,11 @@ struct SrtScene {
     unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
     bool has_bvh = false;
-    int32_t *d_flag = nullptr;  // device error flag (stack overflow)
+    int32_t *h_flag = nullptr;  // error flag (stack overflow) in mapped page-locked host memory
+    int32_t *d_flag = nullptr;  // its device alias
+    // work counter pair (work, done) of launches on the scene's own stream:
+    // stream-ordered, reset by the last block of each launch (release_counter)
+    uint32_t *d_counter = nullptr;
     // cached scratch for the host-pointer entry points
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -142,21 +146,30 @@ srt_status launch_unpack(const float4 *d_gathered, int width, int height, int sh
 srt_status check_flag(const SrtScene *s, cudaStream_t st);
 srt_status clear_flag(const SrtScene *s, cudaStream_t st);
 
-// Work counter of ONE persistent-kernel launch: 128 B of stream-ordered
-// scratch (cudaMallocAsync from the device pool), zeroed on `st` and released
-// on `st` after the launch.  Launches on different streams therefore never
-// share a counter, whatever their number.
+// Work counter of ONE persistent-kernel launch on a caller's stream: 128 B of
+// stream-ordered scratch (cudaMallocAsync from the device pool), zeroed on
+// `st` and released on `st` after the launch.  Launches on different streams
+// therefore never share a counter, whatever their number.
+// Launches on the scene's own stream (the serialised host entry points) reuse
+// the scene's counter pair, which every persistent kernel leaves zeroed
+// (release_counter), so they add no allocation and no memset to the stream.
 struct LaunchCounter {
     uint32_t *p = nullptr;
     cudaStream_t st = nullptr;
-    srt_status init(cudaStream_t stream) {
+    bool owned = false;
+    srt_status init(const SrtScene *s, cudaStream_t stream) {
         st = stream;
+        if (stream == s->stream && s->d_counter) {
+            p = s->d_counter;
+            return SRT_OK;
+        }
+        owned = true;
         srt_status rc = cuda_status(cudaMallocAsync((void **)&p, 128, st), "work counter alloc");
         if (!rc) rc = cuda_status(cudaMemsetAsync(p, 0, 128, st), "work counter reset");
         return rc;
     }
     ~LaunchCounter() {
-        if (p) cudaFreeAsync(p, st);
+        if (owned && p) cudaFreeAsync(p, st);
     }
 };
 

@@ -29,6 +29,21 @@ namespace srt {
 
 constexpr int kDone = kLeafEmpty;  // "no item" code for the next node / postponed leaf
 
+// End of a persistent launch: the last block out zeroes the (work, done)
+// counter pair, so a counter reused by the next launch on the same stream
+// needs no memset (LaunchCounter).
+__device__ __forceinline__ void release_counter(uint32_t *work) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            work[0] = 0u;
+            work[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
 template <int NS>
 struct Slots {
     float t[NS];
@@ -256,7 +271,7 @@ __device__ __forceinline__ int visit_node(const SceneView &s, const RayState &r,
         SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
 #undef SRT_CX
         if (wk.sp + ni - 1 > kStackSize) {
-            atomicExch(overflow, 1);
+            raise_flag(overflow);
             wk.sp = 0;
             return kDone;
         }
@@ -526,6 +541,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace(SceneView s, Src src, W
             }
         }
     }
+    release_counter(work);
 }
 
 // ---------------------------------------------------------------------------
@@ -699,7 +715,7 @@ __device__ __forceinline__ int descend(Walk &wk, const int4 &kids, int key[4], u
         SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
 #undef SRT_CX
         if (wk.sp + ni - 1 > kStackSize) {
-            atomicExch(overflow, 1);
+            raise_flag(overflow);
             wk.sp = 0;
             return kDone;
         }
@@ -829,6 +845,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
         }
     }
     ct.flush(stats);
+    release_counter(work);
 }
 
 // ---------------------------------------------------------------------------
@@ -1070,7 +1087,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
 #undef SRT_CX
                     const int nin = __popc(ai);
                     if (sp + nin - 1 > PSTACK) {
-                        if (lane == 0) atomicExch(overflow, 1);
+                        if (lane == 0) raise_flag(overflow);
                         break;
                     }
                     // far-to-near: entries nin-1 .. 1 (unused sort slots hold INT_MAX)
@@ -1099,6 +1116,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     }
     src.done();
     ct.flush(stats);
+    release_counter(work);
 }
 
 template <int NS, int MODE, int RNG, class Src, bool STATS>
@@ -1123,7 +1141,7 @@ static srt_status launch_trace_v(const SrtScene *s, const Src &src, const WalkCf
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     LaunchCounter work;
-    srt_status rc = work.init(st);
+    srt_status rc = work.init(s, st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
@@ -1147,7 +1165,7 @@ static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const Wal
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     LaunchCounter work;
-    srt_status rc = work.init(st);
+    srt_status rc = work.init(s, st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
@@ -1177,7 +1195,7 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
         cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     LaunchCounter work;
-    srt_status rc = work.init(st);
+    srt_status rc = work.init(s, st);
     if (rc) return rc;
     int64_t need = ((int64_t)src.total() + kTraceThreads - 1) / kTraceThreads;
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
@@ -1637,7 +1655,7 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
             } else if (sp < kStackSize) {
                 stk[sp++] = code;
             } else {
-                atomicExch(overflow, 1);
+                raise_flag(overflow);
             }
         }
         if (node == kDone && sp > 0) node = stk[--sp];
@@ -1749,7 +1767,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
                     if (lane == 0) sstk[wid][sp] = code;
                     ++sp;
                 } else {
-                    if (lane == 0) atomicExch(overflow, 1);
+                    if (lane == 0) raise_flag(overflow);
                     ovf = true;
                 }
             }
@@ -1759,6 +1777,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
         if (valid) out[ri] = __longlong_as_double(sprod[wid][lane]);
         __syncwarp();
     }
+    release_counter(work);
 }
 
 srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max,
@@ -1797,7 +1816,7 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
             cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
         }
         LaunchCounter work;
-        srt_status rc = work.init(st);
+        srt_status rc = work.init(s, st);
         int64_t need = (R + kTraceThreads - 1) / kTraceThreads;
         int64_t grid = std::min<int64_t>((int64_t)g_num_sms * blocks_per_sm, need);
         if (!rc) {

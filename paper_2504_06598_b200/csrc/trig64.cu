@@ -67,7 +67,7 @@ __device__ void walk(const SceneView &s, const Ray64 &r, double s2, int clip, in
             if (!(tn <= tf)) continue;
             if (kid[k] >= 0) {
                 if (sp >= kStackSize) {
-                    atomicExch(overflow, 1);
+                    raise_flag(overflow);
                     return;
                 }
                 stk[sp++] = kid[k];

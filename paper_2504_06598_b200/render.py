@@ -54,12 +54,12 @@ class AccumBuffer:
 
 
 class _PinnedBlock:
-    """Page-locked host block exposed to numpy; returned to the pool when the
-    last array viewing it is collected."""
+    """Page-locked host block exposed to numpy as an array of `shape` and
+    `dtype`; returned to the pool when the last array viewing it is collected."""
 
-    def __init__(self, pool, ptr: int, nbytes: int):
+    def __init__(self, pool, ptr: int, nbytes: int, shape, typestr: str):
         self._pool, self._ptr, self._nbytes = pool, ptr, nbytes
-        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+        self.__array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3}
 
     def __del__(self):
         try:
@@ -77,7 +77,8 @@ class PinnedPool:
         self._lock = threading.Lock()
 
     def array(self, shape, dtype=np.float64) -> np.ndarray:
-        nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        dt = np.dtype(dtype)
+        nbytes = math.prod(shape) * dt.itemsize
         with self._lock:
             lst = self._free.get(nbytes)
             ptr = lst.pop() if lst else None
@@ -85,7 +86,7 @@ class PinnedPool:
             p = ctypes.c_void_p()
             _lib.check(_lib.load().srt_host_alloc(nbytes, ctypes.byref(p)))
             ptr = p.value
-        return np.asarray(_PinnedBlock(self, ptr, nbytes)).view(dtype).reshape(shape)
+        return np.asarray(_PinnedBlock(self, ptr, nbytes, tuple(shape), dt.str))
 
     def release(self, ptr: int, nbytes: int) -> None:
         with self._lock:

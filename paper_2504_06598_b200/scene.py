@@ -21,7 +21,7 @@ RNG = {"counter": _lib.SRT_RNG_COUNTER, "table": _lib.SRT_RNG_TABLE, "trig64": _
 
 
 def _ptr(a) -> ctypes.c_void_p:
-    return ctypes.c_void_p(0 if a is None else a.ctypes.data)
+    return ctypes.c_void_p(0 if a is None else a.__array_interface__["data"][0])
 
 
 def _c64(a) -> np.ndarray:
@@ -42,9 +42,27 @@ def _rays(origins, dirs):
     return o, d
 
 
+_STRUCT_CACHE: dict = {}
+
+
+def _cached(key, make):
+    """ctypes argument structs memoised on their values (a render loop passes
+    the same camera and settings every frame; building them costs ~5 us each)."""
+    hit = _STRUCT_CACHE.get(key)
+    if hit is None:
+        if len(_STRUCT_CACHE) > 4096:
+            _STRUCT_CACHE.clear()
+        hit = _STRUCT_CACHE[key] = make()
+    return hit
+
+
 def make_camera(cam) -> SrtCamera:
     """SrtCamera from the 14 scalars (ex..ez, rx..rz, ux..uz, fx..fz, half_w, half_h)
     of render.py:144-150."""
+    return _cached(("cam", tuple(cam)), lambda: _make_camera(cam))
+
+
+def _make_camera(cam) -> SrtCamera:
     c = SrtCamera()
     v = [float(x) for x in cam]
     for k in range(3):
@@ -58,6 +76,14 @@ def make_camera(cam) -> SrtCamera:
 
 def make_render_params(width, height, passes, nslots, mode, s2, clip=True, seed=0, background=(0.0, 0.0, 0.0),
                        pass0=0, shard_index=0, shard_count=1, rng="counter") -> SrtRenderParams:
+    key = ("prm", width, height, passes, nslots, mode, s2, clip, seed, tuple(float(b) for b in background), pass0,
+           shard_index, shard_count, rng)
+    return _cached(key, lambda: _make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background,
+                                                    pass0, shard_index, shard_count, rng))
+
+
+def _make_render_params(width, height, passes, nslots, mode, s2, clip, seed, background, pass0, shard_index,
+                        shard_count, rng) -> SrtRenderParams:
     p = SrtRenderParams()
     p.width, p.height, p.passes, p.nslots = int(width), int(height), int(passes), int(nslots)
     p.mode, p.clip, p.s2 = int(mode), int(bool(clip)), float(s2)
@@ -384,7 +410,7 @@ _CAMERA_CACHE: dict = {}
 def camera_tuple(camera, width: int, height: int) -> tuple:
     """The 14 camera scalars of render.py:140-150 from a CameraConfig
     (memoised on the camera's values: the numpy basis costs ~90 us a frame)."""
-    key = (*map(float, camera.position), *map(float, camera.look_at), *map(float, camera.up), float(camera.fov_deg),
+    key = (camera.position.tobytes(), camera.look_at.tobytes(), camera.up.tobytes(), float(camera.fov_deg),
            int(width), int(height))
     hit = _CAMERA_CACHE.get(key)
     if hit is None:

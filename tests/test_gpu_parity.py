@@ -583,3 +583,73 @@ def test_shards_store_into_one_rowmajor_frame():
             sc.render_pass_frame_device(cam, prm, 0, acc.data_ptr(), True, True, frame.data_ptr(), r > 0, stream)
         torch.cuda.synchronize()
         assert torch.equal(frame, full), G
+
+
+def test_stack_overflow_is_reported_by_the_call_that_caused_it():
+    """A BVH deeper than the 128-entry traversal stack (an uploaded comb: each
+    level pushes a sibling subtree every ray enters) raises SRT_ERR_STACK_OVERFLOW
+    from the call that overflowed -- the flag lives in mapped host memory and
+    is cleared when a host entry point starts -- and the next call on a sane
+    scene is clean."""
+    from paper_2504_06598_b200 import _lib
+    from paper_2504_06598_b200.scene import DeviceScene
+
+    D = 250  # binary depth ~250 (srt_bvh_upload accepts <= 256); ~83 four-wide levels x 3 pushes
+    n = 2 * D + 2
+    means = np.zeros((n, 3))
+    cov6 = np.tile([25.0, 0.0, 0.0, 25.0, 0.0, 25.0], (n, 1))  # sigma 0.2
+    opac = np.full(n, 1e-6)  # nothing is accepted: no far-bound clip
+    lo, hi = np.full(3, -1.0), np.full(3, 1.0)
+    # side subtrees start deeper along the ray (z >= 0) than the chain (z >= -1):
+    # every level descends the chain first and pushes its side subtrees
+    slo = np.array([-1.0, -1.0, 0.0])
+
+    class Comb:  # reference layout (bvh.py:29-47): c_k -> (s_k, c_k+1), s_k -> two leaves
+        pass
+
+    nl, nh, left, right, count = [], [], [], [], []
+
+    def node(box_lo=lo):
+        nl.append(box_lo), nh.append(hi), left.append(-1), right.append(-1), count.append(0)
+        return len(nl) - 1
+
+    prim = 0
+    chain = [node() for _ in range(D)]
+    for k in range(D):
+        s = node(slo)
+        for side in (0, 1):
+            leaf = node(slo)
+            left[leaf], count[leaf] = prim, 1
+            prim += 1
+            (left if side == 0 else right)[s] = leaf
+        left[chain[k]] = s
+        if k + 1 < D:
+            right[chain[k]] = chain[k + 1]
+        else:
+            tail = node()
+            left[tail], count[tail] = prim, 2
+            prim += 2
+            right[chain[k]] = tail
+    b = Comb()
+    b.node_lo, b.node_hi = np.array(nl), np.array(nh)
+    b.node_left, b.node_right, b.node_count = np.array(left), np.array(right), np.array(count)
+    b.prim_order = np.arange(n)
+    b.prim_lo, b.prim_hi = np.tile(slo, (n, 1)), np.tile(hi, (n, 1))
+    sc = DeviceScene(means, cov6, opac)
+    sc.upload_bvh(b)
+    o = np.tile([[0.0, 0.0, -5.0]], (64, 1))
+    d = np.tile([[0.0, 0.0, 1.0]], (64, 1))
+    with pytest.raises(_lib.SrtError, match="stack overflow"):
+        sc.trace_rays(o, d, nslots=1)  # per-lane walk
+    from paper_2504_06598_b200.scene import camera_tuple
+    from paper_2504_06598_b200.synthetic import front_camera
+
+    with pytest.raises(_lib.SrtError, match="stack overflow"):
+        sc.render(camera_tuple(front_camera(fov_deg=5.0), 32, 32), 32, 32)  # packet walk
+    sc.close()
+    from paper_2504_06598_b200.synthetic import random_cloud
+
+    ok = DeviceScene.from_packed(random_cloud(500, seed=2).packed)
+    ok.build_bvh(CUTOFF)
+    ok.trace_rays(o, d, nslots=1)  # clean
+    ok.check_status()
