@@ -320,11 +320,21 @@ def run_ours(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SRT_BENCH_SAME_GPU=1: a FUNCTIONAL check of the N > 1 code path on a
+    # one-GPU box (every rank on cuda:0, gloo, host-side frame barrier); its
+    # timings mean nothing and the line says so
+    same_gpu = os.environ.get("SRT_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if same_gpu else "nccl"
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size visible in the log
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2504_06598_b200 import RenderSettings, _lib, front_camera, render
     from paper_2504_06598_b200.render import prepare
@@ -372,7 +382,7 @@ def run_ours(args) -> None:
         peer = PeerFrame(WIDTH * HEIGHT * 16, rank, local)
         if not peer.ok:
             peer = None
-    done_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    done_flag = torch.zeros(1, dtype=torch.int32, device=dev if backend == "nccl" else "cpu")
 
     def step(scene, ev=None):
         if ev is not None:
@@ -388,6 +398,8 @@ def run_ours(args) -> None:
             ev[1].record(stream)
         if world > 1:
             if peer is not None:
+                if backend != "nccl":
+                    stream.synchronize()  # gloo is host-side: wait for this rank's kernel first
                 dist.all_reduce(done_flag)  # stream-ordered after every rank's fenced kernel
             else:
                 dist.gather(out, list(gathered.chunk(world)) if rank == 0 else None, dst=0)
@@ -426,7 +438,7 @@ def run_ours(args) -> None:
     mine = [statistics.mean(total), statistics.mean(walk), statistics.mean(gather), statistics.mean(unpack),
             float(tiles)]
     if world > 1:
-        t = torch.tensor(mine, device=dev, dtype=torch.float64)
+        t = torch.tensor(mine, device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         allr = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(allr, t)
         per_rank = [r.tolist() for r in allr]
@@ -527,6 +539,8 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * st.passes + (args.steps if (world > 1 and peer is None) else 0),
+            **({"functional_check_only": "SRT_BENCH_SAME_GPU=1: every rank on cuda:0 over gloo; not a "
+                                         "performance number"} if same_gpu else {}),
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
