@@ -293,12 +293,17 @@ struct Screen {
     float t_lo;      // lower bound of the candidate depth
     float alpha_hi;  // upper bound of alpha
     bool maybe;      // could be a valid candidate inside (t_min, far]
-    // decided by the screen alone (no exact stage): the candidate is valid
-    // for certain (dAd > 0, mah + error <= s^2, t +- error inside the open
-    // interval) and alpha >= alpha_lo; t is the screen's depth estimate
-    bool sure;
-    float alpha_lo;
-    float t;
+    float t;         // the screen's depth estimate
+    // the bounds behind the decision below
+    float mt, mah, mr, dad, alpha_base;  // alpha_base = opacity * exp(-max(resid - mr, 0) / 2)
+    // Decided by the screen alone (no exact stage)?  True when the candidate
+    // is valid for certain (dAd > 0, mah + error <= s^2, t +- error inside the
+    // open interval); alpha_lo then bounds alpha from below.  Evaluated only
+    // for the few candidates whose draw passed alpha_hi.
+    __device__ __forceinline__ bool sure(float s2, float t_min, float t_max0) const {
+        return (dad > 0.0f) && isfinite(dad) && (mah + mr <= s2) && (t - mt > t_min) && (t + mt < t_max0);
+    }
+    __device__ __forceinline__ float alpha_lo() const { return alpha_base * __expf(-mr) * 0.9999f - 1e-7f; }
 };
 
 // Minimal fp32 ray for the screen (camera rays share one origin).
@@ -351,13 +356,15 @@ __device__ __forceinline__ Screen screen(const R &r, const float4 &m, const floa
     float mt = e + es * rs + 2.0e-6f * (fabsf(t) + 1.0f);
     sc.t_lo = t - mt;
     sc.maybe = (dad > 0.0f) && (mah - mr <= s2) && (t - mt <= far) && (t + mt > r.t_min) && (t - mt < r.t_max0);
-    const float ea = __expf(-0.5f * fmaxf(resid - mr, 0.0f));
-    sc.alpha_hi = m.w * ea * 1.0001f + 1e-7f;
-    // lower bound of alpha: the same error terms the other way (exp(-mr)
-    // widens the band by the residual's bound; the opacity is fp32-rounded)
-    sc.alpha_lo = m.w * ea * __expf(-mr) * 0.9999f - 1e-7f;
-    sc.sure = (dad > 0.0f) && isfinite(dad) && (mah + mr <= s2) && (t - mt > r.t_min) && (t + mt < r.t_max0);
+    sc.alpha_base = m.w * __expf(-0.5f * fmaxf(resid - mr, 0.0f));
+    sc.alpha_hi = sc.alpha_base * 1.0001f + 1e-7f;
+    // alpha_lo(): the same error terms the other way (exp(-mr) widens the
+    // band by the residual's bound; the opacity is fp32-rounded)
     sc.t = t;
+    sc.mt = mt;
+    sc.mah = mah;
+    sc.mr = mr;
+    sc.dad = dad;
     return sc;
 }
 

@@ -114,22 +114,23 @@ __device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
     bool need = false, band = false;
+    const float alpha_lo = sc.alpha_lo();
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         if (sc.t_lo <= sl.t[k]) {
             const double u = RNG == SRT_RNG_TABLE ? __ldg(w.table + (int64_t)pid * w.tstride + k)
                                                   : (double)counter_u(sl.key[k], (uint32_t)pid);
             need |= u <= (double)sc.alpha_hi;
-            band |= u >= (double)sc.alpha_lo && u <= (double)sc.alpha_hi;
+            band |= u >= (double)alpha_lo && u <= (double)sc.alpha_hi;
         }
     }
     if (!need) return;
     Cand c;
-    if (sc.sure && !band) {
+    if (sc.sure(w.s2, r.t_min, r.t_max0) && !band) {
         // decided by the screen (see packet_job): valid for certain, every
         // relevant draw below alpha_lo or above alpha_hi
         c.t = sc.t;
-        c.alpha = sc.alpha_lo;
+        c.alpha = alpha_lo;
         c.valid = 1;
     } else {
         ct.add(3, 1);
@@ -578,20 +579,21 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
     ct.add(2, 1);
     int pid = __float_as_int(b.z);
     bool need = false, band = false;
+    const float alpha_lo = sc.alpha_lo();
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
         if (sc.t_lo <= unpack_t(best[k])) {
             const double u = RNG == SRT_RNG_TABLE ? __ldg(w.table + (int64_t)pid * w.tstride + k)
                                                   : (double)counter_u(keys[k], (uint32_t)pid);
             need |= u <= (double)sc.alpha_hi;
-            band |= u >= (double)sc.alpha_lo && u <= (double)sc.alpha_hi;
+            band |= u >= (double)alpha_lo && u <= (double)sc.alpha_hi;
         }
     }
     if (!need) return;
     Cand c;
-    if (sc.sure && !band) {
+    if (sc.sure(w.s2, r.t_min, r.t_max0) && !band) {
         c.t = sc.t;  // decided by the screen (see packet_job)
-        c.alpha = sc.alpha_lo;
+        c.alpha = alpha_lo;
         c.valid = 1;
     } else {
         ct.add(3, 1);
@@ -639,7 +641,8 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
         if (sc.t_lo <= unpack_t(best[k]))
             need |= (NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid)) <= sc.alpha_hi;
     if (!need) return;
-    if (sc.sure) {
+    if (sc.sure(w.s2, sr.t_min, sr.t_max0)) {
+        const float alpha_lo = sc.alpha_lo();
         // Valid for certain and every draw outside [alpha_lo, alpha_hi]: the
         // screen decides (u < alpha_lo <= alpha: accepted, at the screen's
         // depth, ~1e-6 from the exact one).  Only draws inside the error band
@@ -650,7 +653,7 @@ __device__ __forceinline__ void packet_job(const SceneView &s, const CamD &cam, 
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
             const float u = NS == 1 ? u0 : counter_u(keys[k], (uint32_t)pid);
-            if (u < sc.alpha_lo) {
+            if (u < alpha_lo) {
                 if (key < best[k]) {
                     atomicMin(best + k, key);
                     ct.add(4, 1);
