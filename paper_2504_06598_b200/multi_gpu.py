@@ -344,11 +344,13 @@ class PeerFrame:
             self.close()
 
     def close(self) -> None:
+        import ctypes
+
         from . import _lib
 
         if self.ptr:
             L = _lib.load()
-            (L.srt_ipc_free if self._owned else L.srt_ipc_close)(self.device, __import__("ctypes").c_void_p(self.ptr))
+            (L.srt_ipc_free if self._owned else L.srt_ipc_close)(self.device, ctypes.c_void_p(self.ptr))
         self.ptr = 0
 
 
