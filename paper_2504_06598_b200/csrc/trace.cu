@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
             const float paz[4] = {az.x, az.y, az.z, az.w}, pbz[4] = {bz.x, bz.y, bz.z, bz.w};
             unsigned hitm = 0;
-            int key[4];
+            float tn4[4];  // entry distances (ordering keys are built only when inner children compete)
             if (!mixed) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -1023,7 +1023,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     const float tf = fminf(fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
                                                  fmaf(pbz[k], r.idz, -r.oidz)), far);
                     hitm |= tn <= tf ? (1u << k) : 0u;
-                    key[k] = (__float_as_int(tn) & ~3) | k;  // orderable as an int when tn >= 0
+                    tn4[k] = tn;
                 }
             } else {
 #pragma unroll
@@ -1034,7 +1034,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     const float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
                     const float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
                     hitm |= tn <= tf ? (1u << k) : 0u;
-                    key[k] = (__float_as_int(tn) & ~3) | k;
+                    tn4[k] = tn;
                 }
             }
             const unsigned validm = hint & 15u, leafm = (hint >> 4) & 15u;
@@ -1078,7 +1078,8 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 } else {
                     int wk[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? key[k] : 0x7FFFFFFF);
+                    for (int k = 0; k < 4; ++k)  // entry bits with the child index in the low 2 bits (orderable when >= 0)
+                        wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? ((__float_as_int(tn4[k]) & ~3) | k) : 0x7FFFFFFF);
 #define SRT_CX(a, b)                  \
     {                                 \
         int lo_ = min(wk[a], wk[b]);  \
