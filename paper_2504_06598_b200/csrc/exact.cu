@@ -11,6 +11,7 @@
 // unclipped walk per chunk, so rays through thousands of candidates need no
 // per-ray buffer beyond the chunk.
 #include <cfloat>
+#include <algorithm>
 #include <climits>
 
 #include "srt_internal.h"
@@ -147,6 +148,8 @@ __device__ void exact_ray(const SceneView &s, const RayState &r, float s2, const
         for_each_leaf(
             s, r, overflow,
             [&](const float4 &gm, const float4 &ga, const float4 &gb) {
+                // fp32 screen first: certainly-invalid candidates skip the fp64 stage
+                if (!screen<MODE>(r, gm, ga, gb, s2, sqrtf(s2), r.t_max0).maybe) return;
                 Cand c = candidate<MODE>(r, gm, ga, gb, s2);
                 if (!c.valid) return;
                 const int id = __float_as_int(gb.z);
@@ -194,31 +197,6 @@ __global__ void __launch_bounds__(128) k_exact_rays(SceneView s, const double *_
     rgb[i * 3 + 1] = o[1];
     rgb[i * 3 + 2] = o[2];
     op[i] = o[3];
-}
-
-// render_exact (kernels.py:677-723): per pixel, the mean over `passes`
-// jittered rays of the exact composite.  Row-major fp64 outputs.
-template <int MODE>
-__global__ void __launch_bounds__(128) k_exact_frame(SceneView s, CamD cam, RenderArgs a, double *rgb, double *op,
-                                                     int *overflow) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (int64_t)a.width * a.height) return;
-    int px = (int)(i % a.width), py = (int)(i / a.width);
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int f = 0; f < a.passes; ++f) {
-        double dx, dy, dz;
-        camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)(a.pass0 + f), a.seed, a.width, a.height, dx, dy, dz);
-        RayState r;
-        init_ray(r, cam.e[0], cam.e[1], cam.e[2], dx, dy, dz, 0.0, DBL_MAX);
-        double o[4];
-        exact_ray<MODE>(s, r, a.s2, a.bg, o, overflow);
-        for (int c = 0; c < 4; ++c) acc[c] += o[c];
-    }
-    double inv = 1.0 / (double)a.passes;
-    rgb[i * 3] = acc[0] * inv;
-    rgb[i * 3 + 1] = acc[1] * inv;
-    rgb[i * 3 + 2] = acc[2] * inv;
-    op[i] = acc[3] * inv;
 }
 
 // ---------------------------------------------------------------------------
@@ -273,6 +251,13 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
                 alpha = t64::mul(s.opac64[pid], exp(t64::mul(-0.5, resid)));
                 acc = t64::hash_position(hx, hy, hz, 0) < alpha;
             } else {
+                // fp32 screen first: certainly invalid, or a draw above the
+                // screen's alpha bound (certainly rejected), skips the fp64 stage
+                const Screen sc = screen<MODE>(r, gm, ga, gb, s2f, sqrtf(s2f), r.t_max0);
+                if (!sc.maybe) return;
+                const float u = RNG == SRT_RNG_TABLE ? (float)__ldg(a.table + (int64_t)pid * a.tstride)
+                                                     : counter_u(key, (uint32_t)pid);
+                if (RNG != SRT_RNG_TABLE && u >= sc.alpha_hi) return;
                 Cand c = candidate<MODE>(r, gm, ga, gb, s2f);
                 if (!c.valid) return;
                 t = c.t;
@@ -280,7 +265,7 @@ __device__ void biased_ray(const SceneView &s, const double *q, uint32_t key, co
                 if (RNG == SRT_RNG_TABLE)
                     acc = __ldg(a.table + (int64_t)pid * a.tstride) < alpha;
                 else
-                    acc = counter_u(key, (uint32_t)pid) < c.alpha;
+                    acc = u < c.alpha;
             }
             if (!acc || !decltype(h)::less(lo_t, lo_id, t, pid)) return;
             h.offer(t, pid, alpha);
@@ -372,6 +357,467 @@ static BiasedArgs biased_args(double t_min, double t_max, double s2, int mode, i
         if ((MODEV) == 0) LAUNCH(0, SRT_RNG_COUNTER); else LAUNCH(1, SRT_RNG_COUNTER); \
     }
 
+
+// ---------------------------------------------------------------------------
+// Exact compositing as warp packets (render(reference_mode=True) frames and
+// one-hemisphere exact_batch rays).  The 32 rays of a packet (an 8x4 pixel
+// block, or 32 consecutive rays of a coherence-sorted batch) walk the
+// octant tree together WITHOUT clipping (kernels.py:441-475 composites
+// every valid candidate); leaf children any lane hits are compacted into a
+// warp job queue as in k_trace_packet.  A job screens the owner's ray in
+// fp32 (Screen: certainly-invalid candidates never reach fp64), evaluates
+// the exact candidate exactly as exact_ray does, and appends a valid one as
+// (hit key, alpha) to the owner's list in global scratch (lanes
+// interleaved).  Once the walk ends, each lane sorts its list by key --
+// (t, prim id), the stable mergesort order -- and composites front to back
+// in fp64 with the same arithmetic as exact_ray.  A ray with more than
+// kExactCap valid candidates composites through exact_ray's chunked peeling
+// instead (kept out of line).
+// ---------------------------------------------------------------------------
+constexpr int kExactCap = 1024;      // list entries per ray (C3-target: mean 261, max ~720 valid candidates)
+constexpr int kExactThreads = 128;
+constexpr int kExactBlocksPerSM = 6;  // bounds the list scratch: 148 x 6 x 128 lanes x 12 KB = 1.4 GB
+
+// Rays of a packet: camera frames (all passes of an 8x4 pixel block, summed
+// in the warp in pass order, mean written once: deterministic).
+struct ExactFrameSrc {
+    CamD cam;
+    int width, height, passes, pass0, bw;
+    uint32_t seed;
+    double *rgb, *op;
+    double t_min, t_max;
+    __device__ uint32_t packets() const { return (uint32_t)bw * (uint32_t)((height + 3) / 4); }
+    __device__ bool ray(uint32_t p, int lane, int f, double o[3], double d[3]) const {
+        const int px = (int)(p % (uint32_t)bw) * 8 + (lane & 7), py = (int)(p / (uint32_t)bw) * 4 + (lane >> 3);
+        if (px >= width || py >= height) return false;
+        camera_ray(cam, (uint32_t)px, (uint32_t)py, (uint32_t)(pass0 + f), seed, width, height, d[0], d[1], d[2]);
+        o[0] = cam.e[0], o[1] = cam.e[1], o[2] = cam.e[2];
+        return true;
+    }
+    __device__ void write(uint32_t p, int lane, const double acc[4]) const {
+        const int px = (int)(p % (uint32_t)bw) * 8 + (lane & 7), py = (int)(p / (uint32_t)bw) * 4 + (lane >> 3);
+        const int64_t i = (int64_t)py * width + px;
+        const double inv = 1.0 / (double)passes;
+        rgb[i * 3] = acc[0] * inv;
+        rgb[i * 3 + 1] = acc[1] * inv;
+        rgb[i * 3 + 2] = acc[2] * inv;
+        op[i] = acc[3] * inv;
+    }
+};
+
+// Explicit rays (exact_batch, kernels.py:584-604), walked in the order of
+// an optional coherence permutation and written in the caller's.
+struct ExactRaySrc {
+    const double *rays;
+    const uint32_t *perm;
+    uint32_t R;
+    int passes;
+    double *rgb, *op;
+    double t_min, t_max;
+    __device__ uint32_t packets() const { return (R + 31u) / 32u; }
+    __device__ uint32_t index(uint32_t p, int lane) const {
+        const uint32_t k = p * 32u + (uint32_t)lane;
+        return perm ? __ldg(perm + k) : k;
+    }
+    __device__ bool ray(uint32_t p, int lane, int, double o[3], double d[3]) const {
+        if (p * 32u + (uint32_t)lane >= R) return false;
+        const double *q = rays + (int64_t)index(p, lane) * 6;
+        o[0] = q[0], o[1] = q[1], o[2] = q[2], d[0] = q[3], d[1] = q[4], d[2] = q[5];
+        return true;
+    }
+    __device__ void write(uint32_t p, int lane, const double acc[4]) const {
+        const int64_t i = index(p, lane);
+        rgb[i * 3] = acc[0];
+        rgb[i * 3 + 1] = acc[1];
+        rgb[i * 3 + 2] = acc[2];
+        op[i] = acc[3];
+    }
+};
+
+template <int MODE>
+__device__ __noinline__ void exact_ray_long(const SceneView &s, const RayState &r, float s2, const float *bg,
+                                            double out[4], int *overflow) {
+    exact_ray<MODE>(s, r, s2, bg, out, overflow);
+}
+
+// Sort ray o's list (m <= kExactCap entries, key[0..m), alpha[0..m)) and
+// composite it front to back, the whole warp on one ray:
+//  1. depth range of the list (warp min / max of the orderable keys);
+//  2. counting sort into kExactBuckets depth buckets in shared memory
+//     (bucket index monotone in t, so bucket order is depth order), keys
+//     and list positions scattered into sk / sx;
+//  3. insertion sort inside each bucket (a few entries; exact (t, id) order);
+//  4. compositing in chunks of 32: lane i of a chunk takes entry c + i, the
+//     transmittance before it is the chunk's base times an exclusive warp
+//     prefix product of (1 - alpha); sum of T_i alpha_i c_i over the warp.
+// Same fp64 terms as exact_ray, products and sums associated differently
+// (relative 1e-15).
+constexpr int kExactBuckets = 512;
+constexpr int kExactSortSmem = 512;  // lists up to this long sort in shared memory, longer ones in global scratch
+__device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsigned long long *key,
+                                                const float *alpha, int m, float fdx, float fdy, float fdz,
+                                                const float *bg, unsigned *sk, uint16_t *sx, int *scn,
+                                                double out[4]) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    constexpr int NB = kExactBuckets, PER = kExactBuckets / 32;
+    // 1. depth range
+    unsigned kmin = 0xffffffffu, kmax = 0u;
+    for (int i = lane; i < m; i += 32) {
+        const unsigned hi = (unsigned)(key[i] >> 32);
+        kmin = min(kmin, hi);
+        kmax = max(kmax, hi);
+    }
+    kmin = __reduce_min_sync(FULL, kmin);
+    kmax = __reduce_max_sync(FULL, kmax);
+    const float t_lo = unpack_t((unsigned long long)kmin << 32), t_hi = unpack_t((unsigned long long)kmax << 32);
+    const float span = t_hi - t_lo;
+    const float scale = span > 0.0f && isfinite(span) ? (float)NB / span : 0.0f;
+    auto bucket = [&](unsigned long long k) {
+        const float b = (unpack_t(k) - t_lo) * scale;
+        return b >= (float)(NB - 1) ? NB - 1 : (b > 0.0f ? (int)b : 0);
+    };
+    // 2. counting sort: counts, exclusive scan, scatter
+#pragma unroll
+    for (int j = 0; j < PER; ++j) scn[lane * PER + j] = 0;
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) atomicAdd(&scn[bucket(key[i])], 1);
+    __syncwarp();
+    int c[PER], run = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        c[j] = scn[lane * PER + j];
+        run += c[j];
+    }
+    int incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += v;
+    }
+    int base = incl - run;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        scn[lane * PER + j] = base;
+        base += c[j];
+    }
+    __syncwarp();
+    for (int i = lane; i < m; i += 32) {
+        const unsigned long long k = key[i];
+        const int pos = atomicAdd(&scn[bucket(k)], 1);
+        sk[pos] = (unsigned)(k >> 32);  // orderable depth; ties resolved on the list's prim id
+        sx[pos] = (uint16_t)i;
+    }
+    __syncwarp();
+    // 3. insertion sort inside each bucket [end of bucket b-1, end of bucket b)
+    //    by (t, prim id)
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int b = lane * PER + j;
+        const int lo = b == 0 ? 0 : scn[b - 1], hi = scn[b];
+        for (int i = lo + 1; i < hi; ++i) {
+            const unsigned k = sk[i];
+            const uint16_t x = sx[i];
+            int q = i - 1;
+            while (q >= lo && (sk[q] > k || (sk[q] == k && key[sx[q]] > key[x]))) {
+                sk[q + 1] = sk[q];
+                sx[q + 1] = sx[q];
+                --q;
+            }
+            sk[q + 1] = k;
+            sx[q + 1] = x;
+        }
+    }
+    __syncwarp();
+    // 4. front-to-back compositing, 32 entries per step
+    double T = 1.0, rr = 0.0, gg = 0.0, bb = 0.0;
+    for (int c0 = 0; c0 < m; c0 += 32) {
+        const int i = c0 + lane;
+        double a = 0.0;
+        float3 col = make_float3(0.0f, 0.0f, 0.0f);
+        if (i < m) {
+            const int x = sx[i];
+            const int id = (int)(unsigned)key[x];
+            SRT_DCHECK(id >= 0 && id < s.n);
+            a = (double)alpha[x];
+            col = sh_color_v(s.sh, s.sh_k, s.sh_deg, id, fdx, fdy, fdz);
+        }
+        double p = 1.0 - a;  // inclusive prefix product of (1 - alpha)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double q = __shfl_up_sync(FULL, p, d);
+            if (lane >= d) p *= q;
+        }
+        double ex = __shfl_up_sync(FULL, p, 1);
+        if (lane == 0) ex = 1.0;
+        const double w = T * ex * a;
+        rr += w * col.x;
+        gg += w * col.y;
+        bb += w * col.z;
+        T *= __shfl_sync(FULL, p, 31);
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        rr += __shfl_xor_sync(FULL, rr, d);
+        gg += __shfl_xor_sync(FULL, gg, d);
+        bb += __shfl_xor_sync(FULL, bb, d);
+    }
+    out[0] = rr + T * bg[0];
+    out[1] = gg + T * bg[1];
+    out[2] = bb + T * bg[2];
+    out[3] = 1.0 - T;
+}
+
+template <int MODE, class Src>
+__global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_packet(SceneView s, Src src, float s2, float3 bgc,
+                                                                 unsigned long long *lkey, float *lalpha,
+                                                                 unsigned *gsort, uint32_t *work, int *overflow) {
+    constexpr int W = kExactThreads / 32, PSTACK = 128, BATCH = 32;
+    __shared__ double sray[W][32][7];  // fp64 origin, direction, 1/|d|^2 of each lane's ray
+    __shared__ int scnt[W][32];        // valid candidates found per ray
+    __shared__ uint32_t sjob[W][BATCH + 128];
+    __shared__ int sstk[W][PSTACK];
+    // one ray's list at a time, bucket-sorted: in shared memory up to
+    // kExactSortSmem entries, else in the warp's global sort scratch
+    __shared__ unsigned ssk[W][kExactSortSmem];
+    __shared__ uint16_t ssx[W][kExactSortSmem];
+    __shared__ int sscn[W][kExactBuckets];
+    const unsigned FULL = 0xffffffffu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const float sqrt_s2 = sqrtf(s2);
+    const float bg[3] = {bgc.x, bgc.y, bgc.z};
+    const size_t lbase = ((size_t)blockIdx.x * W + wid) * 32u * (size_t)kExactCap;
+    unsigned long long *wkey = lkey + lbase;
+    float *walpha = lalpha + lbase;
+    unsigned *gsk = gsort + ((size_t)blockIdx.x * W + wid) * kExactCap * 2;  // u32 keys, then u16 positions
+    uint16_t *gsx = reinterpret_cast<uint16_t *>(gsk + kExactCap);
+    const RayState r0 = [] {
+        RayState z;
+        init_ray(z, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
+        return z;
+    }();
+    const uint32_t npk = src.packets();
+    while (true) {
+        uint32_t p = 0;
+        if (lane == 0) p = atomicAdd(work, 1u);
+        p = __shfl_sync(FULL, p, 0);
+        if (p >= npk) break;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        bool any_valid = false;
+        for (int f = 0; f < src.passes; ++f) {
+            double o[3], d[3];
+            const bool valid = src.ray(p, lane, f, o, d);
+            any_valid |= valid;
+            RayState r = r0;
+            float far = -INFINITY;  // idle lanes hit nothing
+            if (valid) {
+                init_ray(r, o[0], o[1], o[2], d[0], d[1], d[2], src.t_min, src.t_max);
+                far = r.t_max0;
+                double *q = sray[wid][lane];
+                q[0] = o[0], q[1] = o[1], q[2] = o[2], q[3] = d[0], q[4] = d[1], q[5] = d[2], q[6] = r.inv_dd;
+            }
+            scnt[wid][lane] = 0;
+            const unsigned vm = __ballot_sync(FULL, valid);
+            const unsigned nx_m = __ballot_sync(FULL, valid && signbit(r.idx));
+            const unsigned ny_m = __ballot_sync(FULL, valid && signbit(r.idy));
+            const unsigned nz_m = __ballot_sync(FULL, valid && signbit(r.idz));
+            const int oct = (nx_m ? 1 : 0) | (ny_m ? 2 : 0) | (nz_m ? 4 : 0);
+            const bool mixed = (nx_m && nx_m != vm) || (ny_m && ny_m != vm) || (nz_m && nz_m != vm);
+            const Node4 *tree = s.nodes8 + (size_t)oct * (size_t)s.num_nodes4;
+            int sp = 0, njobs = 0;
+            int node = (s.num_nodes4 > 0 && vm) ? 0 : kLeafEmpty;
+            auto run_jobs = [&]() {
+                __syncwarp();
+                for (int jb = 0; jb < njobs; jb += 32) {
+                    const int j = jb + lane;
+                    if (j < njobs) {
+                        const uint32_t job = sjob[wid][j];
+                        const int ow = (int)(job & 31u), slot = (int)(job >> 5);
+                        SRT_DCHECK(slot >= 0 && slot < s.n);
+                        const double *q = sray[wid][ow];
+                        ExactRay er;
+                        er.ox = q[0], er.oy = q[1], er.oz = q[2], er.dx = q[3], er.dy = q[4], er.dz = q[5];
+                        er.inv_dd = q[6];
+                        er.fdx = (float)er.dx, er.fdy = (float)er.dy, er.fdz = (float)er.dz;
+                        er.t_min = (float)src.t_min;
+                        er.t_max0 = src.t_max >= 3.0e38 ? INFINITY : (float)src.t_max;
+                        ScreenRay sr;
+                        sr.fox = (float)er.ox, sr.foy = (float)er.oy, sr.foz = (float)er.oz;
+                        sr.omag = fmaxf(fabsf(sr.fox), fmaxf(fabsf(sr.foy), fabsf(sr.foz)));
+                        sr.fdx = er.fdx, sr.fdy = er.fdy, sr.fdz = er.fdz;
+                        sr.inv_dd = er.inv_dd;
+                        sr.t_min = er.t_min, sr.t_max0 = er.t_max0;
+                        const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+                        const float4 gm = __ldg(g), ga = __ldg(g + 1), gb = __ldg(g + 2);
+                        const Screen sc = screen<MODE>(sr, gm, ga, gb, s2, sqrt_s2, er.t_max0);
+                        if (sc.maybe) {
+                            const Cand c = candidate<MODE>(er, gm, ga, gb, s2);
+                            if (c.valid) {
+                                const int pos = atomicAdd(&scnt[wid][ow], 1);
+                                if (pos < kExactCap) {
+                                    wkey[(size_t)ow * kExactCap + pos] = pack_hit(c.t, __float_as_int(gb.z));
+                                    walpha[(size_t)ow * kExactCap + pos] = c.alpha;
+                                }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                njobs = 0;
+            };
+            while (true) {
+                if (njobs >= BATCH || (node == kLeafEmpty && sp == 0 && njobs)) run_jobs();
+                if (node == kLeafEmpty) {
+                    if (sp == 0) break;
+                    node = sstk[wid][--sp];
+                }
+                SRT_DCHECK(node >= 0 && node < s.num_nodes4);
+                const float4 *np = reinterpret_cast<const float4 *>(tree + node);
+                const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
+                             az = __ldg(np + 4), bz = __ldg(np + 5);
+                const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+                const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
+                const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
+                const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
+                const float paz[4] = {az.x, az.y, az.z, az.w}, pbz[4] = {bz.x, bz.y, bz.z, bz.w};
+                unsigned hitm = 0;
+                float tn4[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float tn, tf;
+                    if (!mixed) {
+                        tn = fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
+                                   fmaf(paz[k], r.idz, -r.oidz));
+                        tf = fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
+                                   fminf(fmaf(pbz[k], r.idz, -r.oidz), far));
+                    } else {
+                        const float xa = fmaf(pax[k], r.idx, -r.oidx), xb = fmaf(pbx[k], r.idx, -r.oidx);
+                        const float ya = fmaf(pay[k], r.idy, -r.oidy), yb = fmaf(pby[k], r.idy, -r.oidy);
+                        const float za = fmaf(paz[k], r.idz, -r.oidz), zb = fmaf(pbz[k], r.idz, -r.oidz);
+                        tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fminf(za, zb));
+                        tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
+                    }
+                    // closed slab (kernels.py:279,308) clipped to [t_min, t_max]: the
+                    // walk is unclipped, so boxes wholly behind the origin are culled here
+                    hitm |= fmaxf(tn, r.t_min) <= tf ? (1u << k) : 0u;
+                    tn4[k] = tn;
+                }
+                const unsigned leafm = (hint >> 4) & 15u;
+                hitm &= hint & 15u;
+                node = kLeafEmpty;
+                const unsigned any = __reduce_or_sync(FULL, hitm);
+                const unsigned lh = hitm & leafm;
+                for (unsigned al = any & leafm; al; al &= al - 1) {
+                    const int k = __ffs(al) - 1;
+                    const bool h = (lh >> k) & 1u;
+                    const unsigned bm = __ballot_sync(FULL, h);
+                    if (h) {
+                        SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
+                        sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+                    }
+                    njobs += __popc(bm);
+                }
+                // inner children: nearest (warp-min entry) first, so lists
+                // arrive nearly in depth order; the rest pushed far-to-near
+                const unsigned ih = hitm & ~leafm;
+                const unsigned ai = any & ~leafm;
+                if (ai) {
+                    if (!(ai & (ai - 1))) {
+                        node = sel4(kids, __ffs(ai) - 1);
+                    } else {
+                        int wk[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? ordered_key(tn4[k], k)
+                                                                            : 0x7FFFFFFF);
+#define SRT_CX(a, b)                  \
+    {                                 \
+        int lo_ = min(wk[a], wk[b]);  \
+        int hi_ = max(wk[a], wk[b]);  \
+        wk[a] = lo_;                  \
+        wk[b] = hi_;                  \
+    }
+                        SRT_CX(0, 1) SRT_CX(2, 3) SRT_CX(0, 2) SRT_CX(1, 3) SRT_CX(1, 2)
+#undef SRT_CX
+                        const int nin = __popc(ai);
+                        if (sp + nin - 1 > PSTACK) {
+                            if (lane == 0) raise_flag(overflow);
+                            break;
+                        }
+#pragma unroll
+                        for (int j = 3; j >= 1; --j)
+                            if (lane == 0 && j < nin) sstk[wid][sp + nin - 1 - j] = sel4(kids, wk[j] & 3);
+                        sp += nin - 1;
+                        node = sel4(kids, wk[0] & 3);
+                    }
+                }
+                __syncwarp();
+            }
+            if (njobs) run_jobs();  // a stack overflow left the loop with jobs queued
+            __syncwarp();
+            // the warp sorts and composites each ray's list in turn
+            const int m = scnt[wid][lane];
+            double mine[4] = {0.0, 0.0, 0.0, 0.0};
+            for (unsigned todo = __ballot_sync(FULL, valid && m <= kExactCap); todo; todo &= todo - 1) {
+                const int ow = __ffs(todo) - 1;
+                const double *q = sray[wid][ow];
+                double out[4];
+                const int mo = scnt[wid][ow];
+                const bool sm = mo <= kExactSortSmem;
+                composite_ray_warp(s, wkey + (size_t)ow * kExactCap, walpha + (size_t)ow * kExactCap, mo,
+                                   (float)q[3], (float)q[4], (float)q[5], bg, sm ? ssk[wid] : gsk,
+                                   sm ? ssx[wid] : gsx, sscn[wid], out);
+                if (lane == ow)
+                    for (int c = 0; c < 4; ++c) mine[c] = out[c];
+            }
+            if (valid && m > kExactCap) exact_ray_long<MODE>(s, r, s2, bg, mine, overflow);
+            for (int c = 0; c < 4; ++c) acc[c] += mine[c];
+            __syncwarp();
+        }
+        if (any_valid) src.write(p, lane, acc);
+    }
+    release_counter(work);
+}
+
+// List scratch + work counter for one k_exact_packet launch (stream-ordered).
+template <int MODE, class Src>
+static srt_status launch_exact_packet(const SrtScene *s, const Src &src, float s2, const double *bg,
+                                      cudaStream_t st) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_packet<MODE, Src>, kExactThreads, 0);
+    per_sm = std::max(1, std::min(per_sm, kExactBlocksPerSM));
+    const int grid = num_sms * per_sm;
+    const size_t entries = (size_t)grid * kExactThreads * kExactCap;
+    unsigned long long *lkey = nullptr;
+    float *lalpha = nullptr;
+    unsigned *gsort = nullptr;
+    LaunchCounter work;
+    srt_status rc = work.init(s, st);
+    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lkey, entries * sizeof(unsigned long long), st), "exact list alloc");
+    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lalpha, entries * sizeof(float), st), "exact list alloc");
+    if (!rc)
+        rc = cuda_status(cudaMallocAsync((void **)&gsort, (size_t)grid * (kExactThreads / 32) * kExactCap * 2 * sizeof(unsigned), st),
+                         "exact sort scratch alloc");
+    if (!rc) {
+        k_exact_packet<MODE, Src><<<grid, kExactThreads, 0, st>>>(
+            s->view(), src, s2, make_float3((float)bg[0], (float)bg[1], (float)bg[2]), lkey, lalpha, gsort, work.p,
+            s->d_flag);
+        rc = cuda_status(cudaGetLastError(), "k_exact_packet launch");
+    }
+    if (lkey) cudaFreeAsync(lkey, st);
+    if (lalpha) cudaFreeAsync(lalpha, st);
+    if (gsort) cudaFreeAsync(gsort, st);
+    return rc;
+}
+
 srt_status launch_biased_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int kk,
                               const double *bg, const double *d_table, double *d_rgb, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
@@ -404,6 +850,24 @@ srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R,
                              double s2, const double *bg, double *d_rgb, double *d_op, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
     if (blocks == 0) return SRT_OK;
+    // one-hemisphere batches (camera-like) walk as packets, coherence-sorted
+    // unless they share one origin; incoherent ones per lane
+    bool one_origin = false, one_hemisphere = false;
+    if (R >= 4096 && (uint64_t)R < (1ull << 31)) {
+        srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
+        if (rc) return rc;
+    }
+    if (one_hemisphere) {
+        uint32_t *perm = nullptr;
+        void *sort_mem = nullptr;
+        srt_status rc = SRT_OK;
+        if (!one_origin) rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
+        ExactRaySrc src{d_rays, perm, (uint32_t)R, 1, d_rgb, d_op, t_min, t_max};
+        if (!rc) rc = mode == 0 ? launch_exact_packet<0>(s, src, (float)s2, bg, st)
+                                : launch_exact_packet<1>(s, src, (float)s2, bg, st);
+        if (sort_mem) cudaFreeAsync(sort_mem, st);
+        return rc;
+    }
     float3 b = make_float3((float)bg[0], (float)bg[1], (float)bg[2]);
     if (mode == 0)
         k_exact_rays<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, b, d_rgb, d_op,
@@ -416,14 +880,11 @@ srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R,
 
 srt_status launch_exact_frame(const SrtScene *s, const CamD &cam, const RenderArgs &a, double *d_rgb, double *d_op,
                               cudaStream_t st) {
-    int64_t n = (int64_t)a.width * a.height;
-    unsigned blocks = (unsigned)((n + 127) / 128);
-    if (blocks == 0) return SRT_OK;
-    if (a.mode == 0)
-        k_exact_frame<0><<<blocks, 128, 0, st>>>(s->view(), cam, a, d_rgb, d_op, s->d_flag);
-    else
-        k_exact_frame<1><<<blocks, 128, 0, st>>>(s->view(), cam, a, d_rgb, d_op, s->d_flag);
-    return cuda_status(cudaGetLastError(), "k_exact_frame launch");
+    if ((int64_t)a.width * a.height == 0) return SRT_OK;
+    ExactFrameSrc src{cam, a.width, a.height, a.passes, a.pass0, (a.width + 7) / 8, a.seed, d_rgb, d_op, 0.0,
+                      DBL_MAX};
+    const double bg[3] = {a.bg[0], a.bg[1], a.bg[2]};
+    return a.mode == 0 ? launch_exact_packet<0>(s, src, a.s2, bg, st) : launch_exact_packet<1>(s, src, a.s2, bg, st);
 }
 
 }  // namespace srt

@@ -83,6 +83,58 @@ struct SceneView {
     int64_t n;
 };
 
+// End of a persistent launch: the last block out zeroes the (work, done)
+// counter pair, so a counter reused by the next launch on the same stream
+// needs no memset (LaunchCounter).
+__device__ __forceinline__ void release_counter(uint32_t *work) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            work[0] = 0u;
+            work[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// Hit key (orderable fp32 depth << 32 | prim id): integer order = (t, id)
+// order, so a 64-bit atomicMin keeps the closest hit with ties to the
+// smaller id (kernels.py:353-357) and a sort of keys is the stable
+// (t, id) order of np.argsort(kind="mergesort") (kernels.py:463).
+__device__ __forceinline__ unsigned long long pack_hit(float t, int pid) {
+    unsigned u = __float_as_uint(t);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)u << 32) | (unsigned)pid;
+}
+__device__ __forceinline__ float unpack_t(unsigned long long v) {
+    unsigned u = (unsigned)(v >> 32);
+    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
+    return __uint_as_float(u);
+}
+
+// Child ordering keys: an fp32 entry distance as an orderable int with the
+// child index in the low 2 bits.
+__device__ __forceinline__ int ordered_key(float t, int k) {
+    int i = __float_as_int(t);
+    i = i >= 0 ? i : i ^ 0x7FFFFFFF;
+    return (i & ~3) | k;
+}
+__device__ __forceinline__ float key_t(int key) {
+    int ki = key & ~3;
+    return __int_as_float(ki >= 0 ? ki : ki ^ 0x7FFFFFFF);
+}
+
+__device__ __forceinline__ int pick(const int4 &v, int k) {
+    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
+}
+// pick() for a run-time k as three selects (no branches)
+__device__ __forceinline__ int sel4(const int4 &v, int k) {
+    const int a = (k & 1) ? v.y : v.x;
+    const int b = (k & 1) ? v.w : v.z;
+    return (k & 2) ? b : a;
+}
+
 // ---------------------------------------------------------------------------
 // counter RNG -- bitwise identical to oracle/srt_oracle.c
 // ---------------------------------------------------------------------------
@@ -284,6 +336,12 @@ __device__ __forceinline__ Cand candidate(const R &r, const float4 &m, const flo
     return c;
 }
 
+// The fields of a ray the exact candidate reads (a light RayState).
+struct ExactRay {
+    double ox, oy, oz, dx, dy, dz, inv_dd;
+    float fdx, fdy, fdz, t_min, t_max0;
+};
+
 // Stage-1 screen: the same quantities as `candidate` in plain fp32 (no
 // fp64), with a conservative bound on their rounding error.  A candidate the
 // screen rejects is certainly invalid or beyond `far`; `alpha_hi` bounds
@@ -396,6 +454,44 @@ __device__ __forceinline__ float3 sh_color(const float *__restrict__ sh, int K, 
             v += C3_0 * c0 * __ldg(q + 9) + C3_1 * c1 * __ldg(q + 10) + C3_2 * c2 * __ldg(q + 11) +
                  C3_3 * c3 * __ldg(q + 12) + C3_4 * c4 * __ldg(q + 13) + C3_5 * c5 * __ldg(q + 14) +
                  C3_6 * c6 * __ldg(q + 15);
+        out[ch] = fmaxf(v + 0.5f, 0.0f);
+    }
+    return make_float3(out[0], out[1], out[2]);
+}
+
+// sh_color for degree 3 with the 48 coefficients fetched as 12 128-bit loads
+// (a record is 192 B, 16-B aligned); the same expressions, so the same
+// result bit for bit.  Other degrees take sh_color.
+__device__ __forceinline__ float3 sh_color_v(const float *__restrict__ sh, int K, int deg, int pid, float x, float y,
+                                             float z) {
+    if (deg != 3) return sh_color(sh, K, deg, pid, x, y, z);
+    const float SH_C0 = 0.28209479177387814f, SH_C1 = 0.4886025119029199f;
+    const float C2_0 = 1.0925484305920792f, C2_1 = -1.0925484305920792f, C2_2 = 0.31539156525252005f,
+                C2_3 = -1.0925484305920792f, C2_4 = 0.5462742152960396f;
+    const float C3_0 = -0.5900435899266435f, C3_1 = 2.890611442640554f, C3_2 = -0.4570457994644658f,
+                C3_3 = 0.3731763325901154f, C3_4 = -0.4570457994644658f, C3_5 = 1.445305721320277f,
+                C3_6 = -0.5900435899266435f;
+    const float4 *s4 = reinterpret_cast<const float4 *>(sh + (int64_t)pid * 48);
+    float f[48];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+        const float4 v = __ldg(s4 + j);
+        f[4 * j] = v.x, f[4 * j + 1] = v.y, f[4 * j + 2] = v.z, f[4 * j + 3] = v.w;
+    }
+    float out[3];
+    float xx = x * x, yy = y * y, zz = z * z;
+    float b0 = x * y, b1 = y * z, b2 = 2.0f * zz - xx - yy, b3 = x * z, b4 = xx - yy;
+    float c0 = y * (3.0f * xx - yy), c1 = b0 * z, c2 = y * (4.0f * zz - xx - yy),
+          c3 = z * (2.0f * zz - 3.0f * xx - 3.0f * yy), c4 = x * (4.0f * zz - xx - yy), c5 = z * b4,
+          c6 = x * (xx - 3.0f * yy);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        const float *q = f + ch * 16;
+        float v = SH_C0 * q[0];
+        v = v - SH_C1 * y * q[1] + SH_C1 * z * q[2] - SH_C1 * x * q[3];
+        v += C2_0 * b0 * q[4] + C2_1 * b1 * q[5] + C2_2 * b2 * q[6] + C2_3 * b3 * q[7] + C2_4 * b4 * q[8];
+        v += C3_0 * c0 * q[9] + C3_1 * c1 * q[10] + C3_2 * c2 * q[11] + C3_3 * c3 * q[12] + C3_4 * c4 * q[13] +
+             C3_5 * c5 * q[14] + C3_6 * c6 * q[15];
         out[ch] = fmaxf(v + 0.5f, 0.0f);
     }
     return make_float3(out[0], out[1], out[2]);

@@ -143,6 +143,12 @@ srt_status launch_resolve_f64(const RenderArgs &a, const float4 *d_out, double *
                               cudaStream_t st);
 srt_status launch_unpack(const float4 *d_gathered, int width, int height, int shard_count, int64_t max_tiles,
                          float4 *d_frame, cudaStream_t st);
+// explicit-ray batches (trace.cu): a 64-ray probe for one origin / one
+// hemisphere, the smallest batch walked as packets, and a coherence sort
+// (Morton code of the origin + direction signs) returning a permutation
+srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin, bool &one_hemisphere, cudaStream_t st);
+int64_t packet_min(bool one_origin);
+srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out, cudaStream_t st);
 srt_status check_flag(const SrtScene *s, cudaStream_t st);
 srt_status clear_flag(const SrtScene *s, cudaStream_t st);
 

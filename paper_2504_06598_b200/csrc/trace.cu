@@ -29,20 +29,6 @@ namespace srt {
 
 constexpr int kDone = kLeafEmpty;  // "no item" code for the next node / postponed leaf
 
-// End of a persistent launch: the last block out zeroes the (work, done)
-// counter pair, so a counter reused by the next launch on the same stream
-// needs no memset (LaunchCounter).
-__device__ __forceinline__ void release_counter(uint32_t *work) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
-            work[0] = 0u;
-            work[1] = 0u;
-            __threadfence();
-        }
-    }
-}
 
 template <int NS>
 struct Slots {
@@ -161,25 +147,6 @@ __device__ __forceinline__ void visit_leaf(const SceneView &s, const RayState &r
     }
 }
 
-__device__ __forceinline__ int ordered_key(float t, int k) {
-    int i = __float_as_int(t);
-    i = i >= 0 ? i : i ^ 0x7FFFFFFF;
-    return (i & ~3) | k;
-}
-__device__ __forceinline__ float key_t(int key) {
-    int ki = key & ~3;
-    return __int_as_float(ki >= 0 ? ki : ki ^ 0x7FFFFFFF);
-}
-
-__device__ __forceinline__ int pick(const int4 &v, int k) {
-    return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
-}
-// pick() for a run-time k as three selects (no branches)
-__device__ __forceinline__ int sel4(const int4 &v, int k) {
-    const int a = (k & 1) ? v.y : v.x;
-    const int b = (k & 1) ? v.w : v.z;
-    return (k & 2) ? b : a;
-}
 
 // Per-lane traversal state (registers + a local-memory stack).
 struct Walk {
@@ -555,16 +522,6 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace(SceneView s, Src src, W
 // hit, ties to the smaller id -- exactly the order-free semantics of
 // kernels.py:353-357.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long pack_hit(float t, int pid) {
-    unsigned u = __float_as_uint(t);
-    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-    return ((unsigned long long)u << 32) | (unsigned)pid;
-}
-__device__ __forceinline__ float unpack_t(unsigned long long v) {
-    unsigned u = (unsigned)(v >> 32);
-    u = (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;
-    return __uint_as_float(u);
-}
 
 template <int NS, int MODE, int RNG, bool STATS>
 __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, const WalkCfg &w, int slot,
@@ -609,11 +566,6 @@ __device__ __forceinline__ void leaf_job(const SceneView &s, const RayState &r, 
         }
 }
 
-// The fields of a ray the exact candidate reads (a light RayState).
-struct ExactRay {
-    double ox, oy, oz, dx, dy, dz, inv_dd;
-    float fdx, fdy, fdz, t_min, t_max0;
-};
 
 // Leaf job of the packet kernel: screen on the owner's fp32 direction and
 // the shared camera origin; the exact fp64 stage rebuilds the owner's ray
@@ -872,6 +824,24 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
 // ---------------------------------------------------------------------------
 // BATCH: leaf jobs are run once at least BATCH are queued; MINB: minimum
 // resident blocks per SM requested from the register allocator.
+#ifdef SRT_PACKET_CLOCKS
+// Per-packet timing (experiments only, -DSRT_PACKET_CLOCKS via
+// tools/build_variant.sh): start (globaltimer ns) and duration | smid << 48
+// of work packet base/32 of the last k_trace_packet launch.
+constexpr uint32_t kClockSlots = 1u << 20;
+__device__ uint64_t g_packet_clk[2 * kClockSlots];
+__device__ uint32_t g_packet_cnt[4 * kClockSlots];  // node visits, leaf jobs, pops, mixed | lanes hit << 1
+}  // namespace srt
+extern "C" int srt_exp_packet_clocks(uint64_t *out, int n) {
+    if (n > (int)srt::kClockSlots) n = (int)srt::kClockSlots;
+    return (int)cudaMemcpyFromSymbol(out, srt::g_packet_clk, sizeof(uint64_t) * 2 * (size_t)n);
+}
+extern "C" int srt_exp_packet_counts(uint32_t *out, int n) {
+    if (n > (int)srt::kClockSlots) n = (int)srt::kClockSlots;
+    return (int)cudaMemcpyFromSymbol(out, srt::g_packet_cnt, sizeof(uint32_t) * 4 * (size_t)n);
+}
+namespace srt {
+#endif
 template <int NS, int MODE, int RNG, class Src, bool STATS, int BATCH = 32, int MINB = 1>
 __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView s, Src src, WalkCfg w, uint32_t *work,
                                                                        int *overflow, unsigned long long *stats) {
@@ -902,6 +872,11 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
         if (lane == 0) base = atomicAdd(work, 32u);
         base = __shfl_sync(FULL, base, 0);
         if (base >= total) break;
+#ifdef SRT_PACKET_CLOCKS
+        uint64_t clk_t0 = 0;
+        uint32_t pk_visits = 0, pk_jobs = 0, pk_pops = 0;
+        if (lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(clk_t0));
+#endif
         uint32_t idx = base + (uint32_t)lane;
         bool valid = idx < total && src.template init<NS>(idx, r, sl);
         float far;
@@ -991,6 +966,9 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 while (sp > 0) {
                     --sp;
                     if (lane == 0) ct.add(5, 1);
+#ifdef SRT_PACKET_CLOCKS
+                    ++pk_pops;
+#endif
                     if (sstk_key[wid][sp] <= maxfar) {
                         node = sstk_node[wid][sp];
                         SRT_DCHECK(node >= 0 && node < s.num_nodes4);
@@ -1001,6 +979,9 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 if (node == kDone) continue;  // all culled: flush what is queued, then finish
             }
             if (lane == 0) ct.add(0, 1);
+#ifdef SRT_PACKET_CLOCKS
+            ++pk_visits;
+#endif
             SRT_DCHECK(node >= 0 && node < s.num_nodes4);
             const float4 *np = reinterpret_cast<const float4 *>(tree + node);
             // near / far planes of the 4 children along the packet's octant
@@ -1067,6 +1048,9 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                     sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
                 }
                 njobs += __popc(bm);
+#ifdef SRT_PACKET_CLOCKS
+                pk_jobs += __popc(bm);
+#endif
             }
             // inner children any lane hits: descend into the nearest (warp-min
             // entry), push the others far-to-near with their warp-min entries
@@ -1117,6 +1101,25 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz);
         }
         __syncwarp();
+#ifdef SRT_PACKET_CLOCKS
+        if (lane == 0 && (base >> 5) < kClockSlots) {
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_packet_clk[(base >> 5) * 2] = clk_t0;
+            g_packet_clk[(base >> 5) * 2 + 1] = (t1 - clk_t0) | ((uint64_t)smid << 48);
+        }
+        {
+            const unsigned hitl = __ballot_sync(FULL, valid && far < r.t_max0);
+            if (lane == 0 && (base >> 5) < kClockSlots) {
+                g_packet_cnt[(base >> 5) * 4] = pk_visits;
+                g_packet_cnt[(base >> 5) * 4 + 1] = pk_jobs;
+                g_packet_cnt[(base >> 5) * 4 + 2] = pk_pops;
+                g_packet_cnt[(base >> 5) * 4 + 3] = (mixed ? 1u : 0u) | ((unsigned)__popc(hitl) << 1);
+            }
+        }
+#endif
     }
     src.done();
     ct.flush(stats);
@@ -1483,8 +1486,8 @@ __global__ void k_ray_keys(const double *__restrict__ rays, uint32_t R, const in
 // direction lies in the hemisphere of the first (a coherent batch: camera
 // rays, the reference's parallel jittered rays, validate.py:36-43).  Only the
 // kernel choice depends on it, never a result.
-static srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin, bool &one_hemisphere,
-                             cudaStream_t st) {
+srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin, bool &one_hemisphere,
+                      cudaStream_t st) {
     double probe[64][6];
     const size_t step = (size_t)(R / 64) * 6 * sizeof(double);
     srt_status rc = cuda_status(cudaMemcpy2DAsync(probe, sizeof(probe[0]), d_rays, step, sizeof(probe[0]), 64,
@@ -1505,10 +1508,10 @@ static srt_status probe_rays(const double *d_rays, uint32_t R, bool &one_origin,
 // packets 0.583 vs 0.523 ms per-lane at 60k rays, 2x faster at 2M;
 // tools/exp/prays3.sh, prays4.sh: 1.47x at 131k).
 constexpr int64_t PACKET_MIN_DISTINCT = 65536;
-static int64_t packet_min(bool one_origin) { return one_origin ? 4096 : PACKET_MIN_DISTINCT; }
+int64_t packet_min(bool one_origin) { return one_origin ? 4096 : PACKET_MIN_DISTINCT; }
 
-static srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out,
-                            cudaStream_t st) {
+srt_status sort_rays(const double *d_rays, uint32_t R, uint32_t **d_perm_out, void **d_mem_out,
+                     cudaStream_t st) {
     *d_perm_out = nullptr;
     *d_mem_out = nullptr;
     size_t temp = 0;
@@ -1631,6 +1634,7 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= R) return;
     if (perm) i = __ldg(perm + i);  // walked in sorted order, written in the caller's
+    const float sqrt_s2 = sqrtf(s2);
     const double *q = rays + i * 6;
     RayState r;
     init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
@@ -1652,6 +1656,8 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
                 SRT_DCHECK(~code < s.n);
                 const float4 *g = reinterpret_cast<const float4 *>(s.geom + ~code);
                 float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+                // fp32 screen first: certainly-invalid candidates skip the fp64 stage
+                if (!screen<MODE>(r, m, a, b, s2, sqrt_s2, r.t_max0).maybe) continue;
                 Cand cd = candidate<MODE>(r, m, a, b, s2);
                 if (cd.valid) result *= 1.0 - (double)cd.alpha;
             } else if (node == kDone) {
@@ -1688,6 +1694,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
     __shared__ int sstk[W][PSTACK];
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float sqrt_s2 = sqrtf(s2);
     const unsigned lt = (1u << lane) - 1u;
     while (true) {
         uint32_t base = 0;
@@ -1727,6 +1734,7 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
                         init_ray(ro, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
                         const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
                         float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
+                        if (!screen<MODE>(ro, m, a, b, s2, sqrt_s2, ro.t_max0).maybe) continue;
                         Cand cd = candidate<MODE>(ro, m, a, b, s2);
                         if (cd.valid) {
                             const double f = 1.0 - (double)cd.alpha;

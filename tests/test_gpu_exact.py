@@ -183,3 +183,68 @@ def test_exact_and_biased_peel_many_candidates(oracle):
     k = 600
     trunc = (trans[:k, None] * alphas[:k, None] * colors[:k]).sum(axis=0) + trans[k] * np.array([0.2, 0.3, 0.4])
     np.testing.assert_allclose(got[0], trunc, rtol=1e-4)
+
+
+def test_exact_frame_packets_vs_oracle(oracle):
+    """render(reference_mode=True) walks 8x4 pixel blocks as packets
+    (k_exact_packet, every pass of a block in one warp): a 20k SH-3
+    density-preserving cloud at 72x44 (partial blocks at the right and bottom
+    edges), 2 passes, against the brute-force oracle render_exact."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.scene import camera_tuple
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    a = density_cloud(20_000, seed=5)
+    pk = a.packed
+    st = RenderSettings(width=72, height=44, spp=2, seed=4, reference_mode=True, background=[0.1, 0.2, 0.05])
+    buf = render(a, front_camera(), st)
+    want_rgb, want_op = oracle.render_exact(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree,
+                                            np.array(camera_tuple(front_camera(), 72, 44)), 72, 44, frames=2,
+                                            s2=S2, seed=4, background=(0.1, 0.2, 0.05))
+    assert _close_fraction(buf.rgb.reshape(-1, 3), want_rgb.reshape(-1, 3)) >= 0.995
+    assert _close_fraction(buf.opacity.reshape(-1), want_op.reshape(-1)) >= 0.995
+    np.testing.assert_allclose(buf.rgb, want_rgb, atol=2e-3)
+
+
+@pytest.mark.parametrize("one_origin", [True, False])
+def test_exact_rays_packets_vs_oracle(oracle, one_origin):
+    """One-hemisphere exact_batch batches of >= 4096 rays take the packet
+    kernel (coherence-sorted when the origins differ)."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    a = density_cloud(10_000, seed=6)
+    pk = a.packed
+    rs = np.random.default_rng(7)
+    R = 5000
+    d = rs.normal(size=(R, 3)) * [0.2, 0.2, 0.0] + [0.0, 0.0, 1.0]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = np.tile([0.1, -0.2, -4.0], (R, 1)) if one_origin else rs.uniform(-1.0, 1.0, (R, 3)) * [1, 1, 0] + [0, 0, -4]
+    sc = DeviceScene.from_packed(pk)
+    sc.build_bvh(np.sqrt(S2))
+    rgb, op = sc.exact_rays(o, d, s2=S2, background=(0.3, 0.1, 0.2))
+    sc.close()
+    want_rgb, want_op = oracle.exact_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, o, d, s2=S2,
+                                           background=(0.3, 0.1, 0.2))
+    assert _close_fraction(rgb, want_rgb) >= 0.995
+    assert _close_fraction(op, want_op) >= 0.995
+
+
+@pytest.mark.parametrize("layers", [1000, 1100])
+def test_exact_frame_long_lists(layers):
+    """Camera rays through every layer of a 1000- / 1100-layer stack: 1000
+    fits a packet lane's candidate list (sorted there), 1100 exceeds it and
+    the lane composites by chunked peeling; both equal the closed form."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, render
+    from paper_2504_06598_b200.synthetic import pancake_stack
+
+    rs = np.random.default_rng(11)
+    alphas = rs.uniform(0.001, 0.004, layers)
+    colors = rs.uniform(0.0, 1.0, (layers, 3))
+    a = pancake_stack(alphas, colors, z0=1.0, spacing=0.004, thickness=0.0005)
+    buf = render(a, front_camera(), RenderSettings(width=16, height=8, spp=1, reference_mode=True,
+                                                   background=[0.2, 0.3, 0.4]))
+    trans = np.cumprod(np.concatenate([[1.0], 1.0 - alphas]))
+    closed = (trans[:layers, None] * alphas[:, None] * colors).sum(axis=0) + trans[layers] * np.array([0.2, 0.3, 0.4])
+    np.testing.assert_allclose(buf.rgb.reshape(-1, 3), np.broadcast_to(closed, (128, 3)), rtol=1e-4)
+    np.testing.assert_allclose(buf.opacity, 1.0 - trans[layers], rtol=1e-5)
