@@ -452,7 +452,7 @@ __device__ __noinline__ void exact_ray_long(const SceneView &s, const RayState &
 //     prefix product of (1 - alpha); sum of T_i alpha_i c_i over the warp.
 // Same fp64 terms as exact_ray, products and sums associated differently
 // (relative 1e-15).
-constexpr int kExactBuckets = 512;
+constexpr int kExactBuckets = 256;
 constexpr int kExactSortSmem = 512;  // lists up to this long sort in shared memory, longer ones in global scratch
 __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsigned long long *key,
                                                 const float *alpha, int m, float fdx, float fdy, float fdz,

@@ -1043,10 +1043,20 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 const int k = __ffs(al) - 1;
                 const bool h = (lh >> k) & 1u;
                 const unsigned bm = __ballot_sync(FULL, h);
+#ifdef SRT_PRED_STORE
+                {
+                    // predicated shared store: no divergent branch to reconverge
+                    const uint32_t code = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+                    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&sjob[wid][njobs + __popc(bm & lt)]);
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}"
+                                 :: "r"(addr), "r"(code), "r"((uint32_t)h) : "memory");
+                }
+#else
                 if (h) {
                     SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
                     sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
                 }
+#endif
                 njobs += __popc(bm);
 #ifdef SRT_PACKET_CLOCKS
                 pk_jobs += __popc(bm);
@@ -1792,6 +1802,163 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
     release_counter(work);
 }
 
+
+// Incoherent transmittance batches (rays from distinct origins in all
+// directions): per-lane walks with warp-compacted leaf work.  Each step
+// every active lane visits one node of its own ray (min/max slab, per-lane
+// stack); the leaf children the lanes hit go to a warp job queue (prefix-sum
+// compaction) and, once 32 are queued or a lane's walk ends, the whole warp
+// screens and evaluates them together, multiplying (1 - alpha) into the
+// owner's product in shared memory.  Idle lanes take new rays as soon as 8
+// are free, so the warp stays full while long rays finish.  Same candidates
+// and factors as the per-lane walk; only the product order differs.
+template <int MODE>
+__global__ void __launch_bounds__(kTraceThreads) k_transmittance_coop(SceneView s, const double *__restrict__ rays,
+                                                                      const uint32_t *__restrict__ perm, uint32_t R,
+                                                                      double t_min, double t_max, float s2,
+                                                                      double *out, uint32_t *work, int *overflow) {
+    constexpr int W = kTraceThreads / 32, QCAP = 32 + 128;
+    __shared__ double sray[W][32][7];  // fp64 origin, direction, 1/|d|^2
+    __shared__ unsigned long long sprod[W][32];
+    __shared__ uint32_t sjob[W][QCAP];  // (slot << 5) | owner lane
+    const unsigned FULL = 0xffffffffu;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const float sqrt_s2 = sqrtf(s2);
+    const float ft_min = (float)t_min, ft_max = t_max >= 3.0e38 ? INFINITY : (float)t_max;
+    RayState r;
+    init_ray(r, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
+    int stk[kStackSize];
+    int sp = 0, node = kLeafEmpty, njobs = 0;
+    bool active = false, exhausted = false;
+    uint32_t ri = 0;
+    while (true) {
+        const unsigned idle = __ballot_sync(FULL, !active);
+        if (!exhausted && __popc(idle) >= 8) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(work, (uint32_t)__popc(idle));
+            base = __shfl_sync(FULL, base, 0);
+            if (base + (uint32_t)__popc(idle) >= R) exhausted = true;
+            if (!active) {
+                const uint32_t my = base + (uint32_t)__popc(idle & lt);
+                if (my < R) {
+                    ri = perm ? __ldg(perm + my) : my;
+                    const double *q = rays + (int64_t)ri * 6;
+                    init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+                    double *sq = sray[wid][lane];
+                    sq[0] = r.ox, sq[1] = r.oy, sq[2] = r.oz, sq[3] = r.dx, sq[4] = r.dy, sq[5] = r.dz;
+                    sq[6] = r.inv_dd;
+                    sprod[wid][lane] = __double_as_longlong(1.0);
+                    sp = 0;
+                    node = s.num_nodes4 > 0 ? 0 : kLeafEmpty;
+                    active = true;
+                }
+            }
+        } else if (exhausted && idle == FULL) {
+            break;
+        }
+        // one node visit per walking lane
+        unsigned lm = 0;
+        int4 kids = make_int4(kLeafEmpty, kLeafEmpty, kLeafEmpty, kLeafEmpty);
+        if (active && node != kLeafEmpty) {
+            SRT_DCHECK(node >= 0 && node < s.num_nodes4);
+            const float4 *np = reinterpret_cast<const float4 *>(s.nodes4 + node);
+            const float4 lox = __ldg(np), hix = __ldg(np + 1), loy = __ldg(np + 2), hiy = __ldg(np + 3),
+                         loz = __ldg(np + 4), hiz = __ldg(np + 5);
+            kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+            const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
+            const float lx[4] = {lox.x, lox.y, lox.z, lox.w}, hx[4] = {hix.x, hix.y, hix.z, hix.w};
+            const float ly[4] = {loy.x, loy.y, loy.z, loy.w}, hy[4] = {hiy.x, hiy.y, hiy.z, hiy.w};
+            const float lz[4] = {loz.x, loz.y, loz.z, loz.w}, hz[4] = {hiz.x, hiz.y, hiz.z, hiz.w};
+            unsigned hitm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float xa = fmaf(lx[k], r.idx, -r.oidx), xb = fmaf(hx[k], r.idx, -r.oidx);
+                const float ya = fmaf(ly[k], r.idy, -r.oidy), yb = fmaf(hy[k], r.idy, -r.oidy);
+                const float za = fmaf(lz[k], r.idz, -r.oidz), zb = fmaf(hz[k], r.idz, -r.oidz);
+                const float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
+                const float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), r.t_max0));
+                hitm |= tn <= tf ? (1u << k) : 0u;
+            }
+            hitm &= hint & 15u;
+            const unsigned leafm = (hint >> 4) & 15u;
+            lm = hitm & leafm;
+            // unclipped: every hit inner child is walked, in any order
+            node = kLeafEmpty;
+            for (unsigned im = hitm & ~leafm; im; im &= im - 1) {
+                const int c = sel4(kids, __ffs(im) - 1);
+                if (node == kLeafEmpty) {
+                    node = c;
+                } else if (sp < kStackSize) {
+                    stk[sp++] = c;
+                } else {
+                    raise_flag(overflow);
+                }
+            }
+            if (node == kLeafEmpty && sp > 0) node = stk[--sp];
+        }
+        // queue the hit leaf children of every lane
+        const int cnt = __popc(lm);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += v;
+        }
+        int off = njobs + incl - cnt;
+        for (unsigned m = lm; m; m &= m - 1) {
+            SRT_DCHECK(off < QCAP);
+            sjob[wid][off++] = ((uint32_t)~sel4(kids, __ffs(m) - 1) << 5) | (uint32_t)lane;
+        }
+        njobs += __shfl_sync(FULL, incl, 31);
+        const bool ending = active && node == kLeafEmpty;
+        if (njobs >= 32 || (njobs > 0 && __any_sync(FULL, ending))) {
+            __syncwarp();
+            for (int jb = 0; jb < njobs; jb += 32) {
+                const int j = jb + lane;
+                if (j < njobs) {
+                    const uint32_t job = sjob[wid][j];
+                    const int ow = (int)(job & 31u), slot = (int)(job >> 5);
+                    SRT_DCHECK(slot >= 0 && slot < s.n);
+                    const double *q = sray[wid][ow];
+                    ExactRay er;
+                    er.ox = q[0], er.oy = q[1], er.oz = q[2], er.dx = q[3], er.dy = q[4], er.dz = q[5];
+                    er.inv_dd = q[6];
+                    er.fdx = (float)er.dx, er.fdy = (float)er.dy, er.fdz = (float)er.dz;
+                    er.t_min = ft_min, er.t_max0 = ft_max;
+                    ScreenRay sr;
+                    sr.fox = (float)er.ox, sr.foy = (float)er.oy, sr.foz = (float)er.oz;
+                    sr.omag = fmaxf(fabsf(sr.fox), fmaxf(fabsf(sr.foy), fabsf(sr.foz)));
+                    sr.fdx = er.fdx, sr.fdy = er.fdy, sr.fdz = er.fdz;
+                    sr.inv_dd = er.inv_dd;
+                    sr.t_min = ft_min, sr.t_max0 = ft_max;
+                    const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
+                    const float4 gm = __ldg(g), ga = __ldg(g + 1), gb = __ldg(g + 2);
+                    if (screen<MODE>(sr, gm, ga, gb, s2, sqrt_s2, ft_max).maybe) {
+                        const Cand cd = candidate<MODE>(er, gm, ga, gb, s2);
+                        if (cd.valid) {
+                            const double f = 1.0 - (double)cd.alpha;
+                            unsigned long long *pp = &sprod[wid][ow];
+                            unsigned long long old = *pp, assumed;
+                            do {
+                                assumed = old;
+                                old = atomicCAS(pp, assumed, __double_as_longlong(__longlong_as_double(assumed) * f));
+                            } while (assumed != old);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            njobs = 0;
+        }
+        if (ending && njobs == 0) {
+            out[ri] = __longlong_as_double(sprod[wid][lane]);
+            active = false;
+        }
+    }
+    release_counter(work);
+}
+
 srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t R, double t_min, double t_max,
                                 int mode, double s2, double *d_out, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
@@ -1843,13 +2010,41 @@ srt_status launch_transmittance(const SrtScene *s, const double *d_rays, int64_t
         if (sort_mem) cudaFreeAsync(sort_mem, st);
         return rc;
     }
-    if (mode == 0)
-        k_transmittance<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
-                                                   perm);
-    else
-        k_transmittance<1><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
-                                                   perm);
-    srt_status rc = cuda_status(cudaGetLastError(), "k_transmittance launch");
+    if (!fits) {
+        // more rays than one work counter covers: per-lane walks
+        if (mode == 0)
+            k_transmittance<0><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
+                                                       perm);
+        else
+            k_transmittance<1><<<blocks, 128, 0, st>>>(s->view(), d_rays, R, t_min, t_max, (float)s2, d_out, s->d_flag,
+                                                       perm);
+        srt_status rc = cuda_status(cudaGetLastError(), "k_transmittance launch");
+        if (sort_mem) cudaFreeAsync(sort_mem, st);
+        return rc;
+    }
+    // incoherent batches: per-lane walks, warp-compacted leaf work
+    static int coop_per_sm = 0;
+    if (!coop_per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per_sm, k_transmittance_coop<0>, kTraceThreads, 0);
+        if (coop_per_sm < 1) coop_per_sm = 1;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    LaunchCounter work;
+    srt_status rc = work.init(s, st);
+    const int64_t grid = std::min<int64_t>((int64_t)g_num_sms * coop_per_sm, (R + kTraceThreads - 1) / kTraceThreads);
+    if (!rc) {
+        if (mode == 0)
+            k_transmittance_coop<0><<<(unsigned)grid, kTraceThreads, 0, st>>>(
+                s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work.p, s->d_flag);
+        else
+            k_transmittance_coop<1><<<(unsigned)grid, kTraceThreads, 0, st>>>(
+                s->view(), d_rays, perm, (uint32_t)R, t_min, t_max, (float)s2, d_out, work.p, s->d_flag);
+        rc = cuda_status(cudaGetLastError(), "k_transmittance_coop launch");
+    }
     if (sort_mem) cudaFreeAsync(sort_mem, st);
     return rc;
 }
