@@ -19,7 +19,7 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2504_06598_b200 import RenderSettings, _lib, front_camera  # noqa: E402
+from paper_2504_06598_b200 import CameraConfig, RenderSettings, _lib, front_camera  # noqa: E402
 from paper_2504_06598_b200.render import prepare  # noqa: E402
 from paper_2504_06598_b200.scene import camera_tuple, make_camera, make_render_params, shard_tiles  # noqa: E402
 from paper_2504_06598_b200.synthetic import density_cloud  # noqa: E402
@@ -28,7 +28,12 @@ seed = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 out_npz = sys.argv[2] if len(sys.argv) > 2 else None
 W, H = 1920, 1080
 st = RenderSettings(width=W, height=H, spp=1)
-cam = make_camera(camera_tuple(front_camera(), W, H))
+camera = front_camera()
+if os.environ.get("SRT_CAM_SHIFT"):  # translate the camera (and its target) by (dx, dy)
+    dx, dy = (float(v) for v in os.environ["SRT_CAM_SHIFT"].split(","))
+    camera = CameraConfig(position=camera.position + [dx, dy, 0.0], look_at=camera.look_at + [dx, dy, 0.0],
+                          fov_deg=camera.fov_deg)
+cam = make_camera(camera_tuple(camera, W, H))
 prm = make_render_params(W, H, 1, 1, 0, st.cutoff_s ** 2)
 acc = torch.empty(shard_tiles(W, H) * 256 * 4, device="cuda")
 out = torch.empty(W * H * 4, device="cuda")
@@ -105,5 +110,9 @@ top = np.argsort(-dur)[:12]
 for i in top:
     print(f"  packet {i}: {dur[i] / 1e3:6.1f} us visits {visits[i]} jobs {jobs[i]} pops {pops[i]} "
           f"mixed {mixed[i]} lanes hit {lanes_hit[i]} at block ({px[i] // 8}, {py[i] // 4})")
+col = np.bincount(px // 8, weights=visits, minlength=W // 8) / np.maximum(np.bincount(px // 8, minlength=W // 8), 1)
+row = np.bincount(py // 4, weights=visits, minlength=H // 4) / np.maximum(np.bincount(py // 4, minlength=H // 4), 1)
+print("visits per packet by block column (every 4th):", " ".join(f"{v:.0f}" for v in col[::4]))
+print("visits per packet by block row (every 4th):", " ".join(f"{v:.0f}" for v in row[::4]))
 if out_npz:
     np.savez_compressed(out_npz, start=start, dur=dur, smid=smid, visits=visits, jobs=jobs, pops=pops, flags=flags)
