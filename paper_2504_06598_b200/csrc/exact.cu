@@ -359,31 +359,43 @@ static BiasedArgs biased_args(double t_min, double t_max, double s2, int mode, i
 
 
 // ---------------------------------------------------------------------------
-// Exact compositing as warp packets (render(reference_mode=True) frames and
-// one-hemisphere exact_batch rays).  The 32 rays of a packet (an 8x4 pixel
-// block, or 32 consecutive rays of a coherence-sorted batch) walk the
-// octant tree together WITHOUT clipping (kernels.py:441-475 composites
-// every valid candidate); leaf children any lane hits are compacted into a
-// warp job queue as in k_trace_packet.  A job screens the owner's ray in
-// fp32 (Screen: certainly-invalid candidates never reach fp64), evaluates
-// the exact candidate exactly as exact_ray does, and appends a valid one as
-// (hit key, alpha) to the owner's list in global scratch (lanes
-// interleaved).  Once the walk ends, each lane sorts its list by key --
-// (t, prim id), the stable mergesort order -- and composites front to back
-// in fp64 with the same arithmetic as exact_ray.  A ray with more than
-// kExactCap valid candidates composites through exact_ray's chunked peeling
-// instead (kept out of line).
+// Exact and biased compositing as warp packets: render(reference_mode=True)
+// frames, the --compare-biased frame (cli.py:164-203) and one-hemisphere
+// exact_batch / biased_batch rays.  The 32 rays of a packet (an 8x4 pixel
+// block, or 32 consecutive rays of a coherence-sorted batch) walk the octant
+// tree together; leaf children any lane hits are compacted into a warp job
+// queue as in k_trace_packet.  A job screens the owner's ray in fp32
+// (certainly-invalid candidates never reach fp64; in biased counter mode a
+// draw above the screen's alpha bound is a certain rejection), evaluates
+// the exact candidate exactly as the per-lane paths do, and appends a valid
+// (biased: accepted) one as (hit key, alpha) to the owner's list in global
+// scratch.
+//  - exact (kernels.py:441-475): unclipped; every valid candidate counts.
+//  - biased (kernels.py:479-518): one draw per candidate (slot 0 of the
+//    ray's stream); only the kk nearest accepted are composited, so each
+//    owner keeps the kk smallest depths it has accepted (kk <= kBiasedClip)
+//    and clips its walk beyond the kk-th (widened, conservative): nodes and
+//    candidates past it cannot be among the kk nearest.
+// Once the walk ends, the warp sorts each ray's list by (t, prim id) -- the
+// stable mergesort order of the reference -- and composites front to back
+// in fp64 (composite_ray_warp).  A ray with more than kExactCap list
+// entries composites through the per-lane chunked peeling (out of line).
 // ---------------------------------------------------------------------------
 constexpr int kExactCap = 1024;      // list entries per ray (C3-target: mean 261, max ~720 valid candidates)
 constexpr int kExactThreads = 128;
 constexpr int kExactBlocksPerSM = 6;  // bounds the list scratch: 148 x 6 x 128 lanes x 12 KB = 1.4 GB
+constexpr int kBiasedClip = 8;        // biased walks with kk <= this clip at the kk-th accepted depth
+
+enum { kPacketExact = 0, kPacketBiasedCounter = 1, kPacketBiasedTable = 2 };
 
 // Rays of a packet: camera frames (all passes of an 8x4 pixel block, summed
-// in the warp in pass order, mean written once: deterministic).
+// in the warp in pass order, mean written once: deterministic).  The
+// biased frame's draw of pixel (px, py), pass f is keyed (seed, py*W+px, f)
+// (k_biased_frame).
 struct ExactFrameSrc {
     CamD cam;
     int width, height, passes, pass0, bw;
-    uint32_t seed;
+    uint32_t seed, fkey;
     double *rgb, *op;
     double t_min, t_max;
     __device__ uint32_t packets() const { return (uint32_t)bw * (uint32_t)((height + 3) / 4); }
@@ -394,6 +406,10 @@ struct ExactFrameSrc {
         o[0] = cam.e[0], o[1] = cam.e[1], o[2] = cam.e[2];
         return true;
     }
+    __device__ uint32_t key(uint32_t p, int lane, int f) const {
+        const int px = (int)(p % (uint32_t)bw) * 8 + (lane & 7), py = (int)(p / (uint32_t)bw) * 4 + (lane >> 3);
+        return walk_key(fkey, (uint32_t)py * (uint32_t)width + (uint32_t)px, (uint32_t)(pass0 + f));
+    }
     __device__ void write(uint32_t p, int lane, const double acc[4]) const {
         const int px = (int)(p % (uint32_t)bw) * 8 + (lane & 7), py = (int)(p / (uint32_t)bw) * 4 + (lane >> 3);
         const int64_t i = (int64_t)py * width + px;
@@ -401,12 +417,13 @@ struct ExactFrameSrc {
         rgb[i * 3] = acc[0] * inv;
         rgb[i * 3 + 1] = acc[1] * inv;
         rgb[i * 3 + 2] = acc[2] * inv;
-        op[i] = acc[3] * inv;
+        if (op) op[i] = acc[3] * inv;
     }
 };
 
-// Explicit rays (exact_batch, kernels.py:584-604), walked in the order of
-// an optional coherence permutation and written in the caller's.
+// Explicit rays (exact_batch kernels.py:584-604, biased_batch 561-580),
+// walked in the order of an optional coherence permutation and written in
+// the caller's; ray i draws with (seed, ray_id0 + i, sample0).
 struct ExactRaySrc {
     const double *rays;
     const uint32_t *perm;
@@ -414,6 +431,7 @@ struct ExactRaySrc {
     int passes;
     double *rgb, *op;
     double t_min, t_max;
+    uint32_t fkey, ray_id0, sample0;
     __device__ uint32_t packets() const { return (R + 31u) / 32u; }
     __device__ uint32_t index(uint32_t p, int lane) const {
         const uint32_t k = p * 32u + (uint32_t)lane;
@@ -425,19 +443,38 @@ struct ExactRaySrc {
         o[0] = q[0], o[1] = q[1], o[2] = q[2], d[0] = q[3], d[1] = q[4], d[2] = q[5];
         return true;
     }
+    __device__ uint32_t key(uint32_t p, int lane, int) const {
+        return walk_key(fkey, ray_id0 + index(p, lane), sample0);
+    }
     __device__ void write(uint32_t p, int lane, const double acc[4]) const {
         const int64_t i = index(p, lane);
         rgb[i * 3] = acc[0];
         rgb[i * 3 + 1] = acc[1];
         rgb[i * 3 + 2] = acc[2];
-        op[i] = acc[3];
+        if (op) op[i] = acc[3];
     }
+};
+
+// Per-packet arguments beyond the source.
+struct PacketCompositeArgs {
+    float s2;
+    float3 bg;
+    int kk;                 // biased: accepted candidates composited
+    const double *table;    // biased table mode: u = table[pid * tstride]
+    int64_t tstride;
+    BiasedArgs ba;          // biased: the per-lane fallback's arguments
 };
 
 template <int MODE>
 __device__ __noinline__ void exact_ray_long(const SceneView &s, const RayState &r, float s2, const float *bg,
                                             double out[4], int *overflow) {
     exact_ray<MODE>(s, r, s2, bg, out, overflow);
+}
+template <int MODE, int RNG>
+__device__ __noinline__ void biased_ray_long(const SceneView &s, const double *q, uint32_t key, const BiasedArgs &a,
+                                             double out[4], int *overflow) {
+    biased_ray<MODE, RNG>(s, q, key, a, out, overflow);
+    out[3] = 0.0;
 }
 
 // Sort ray o's list (m <= kExactCap entries, key[0..m), alpha[0..m)) and
@@ -447,7 +484,7 @@ __device__ __noinline__ void exact_ray_long(const SceneView &s, const RayState &
 //     (bucket index monotone in t, so bucket order is depth order), keys
 //     and list positions scattered into sk / sx;
 //  3. insertion sort inside each bucket (a few entries; exact (t, id) order);
-//  4. compositing in chunks of 32: lane i of a chunk takes entry c + i, the
+//  4. compositing of the first `take` in chunks of 32: lane i of a chunk takes entry c + i, the
 //     transmittance before it is the chunk's base times an exclusive warp
 //     prefix product of (1 - alpha); sum of T_i alpha_i c_i over the warp.
 // Same fp64 terms as exact_ray, products and sums associated differently
@@ -455,8 +492,8 @@ __device__ __noinline__ void exact_ray_long(const SceneView &s, const RayState &
 constexpr int kExactBuckets = 256;
 constexpr int kExactSortSmem = 512;  // lists up to this long sort in shared memory, longer ones in global scratch
 __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsigned long long *key,
-                                                const float *alpha, int m, float fdx, float fdy, float fdz,
-                                                const float *bg, unsigned *sk, uint16_t *sx, int *scn,
+                                                const float *alpha, int m, int take, float fdx, float fdy,
+                                                float fdz, const float *bg, unsigned *sk, uint16_t *sx, int *scn,
                                                 double out[4]) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -532,11 +569,11 @@ __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsign
     __syncwarp();
     // 4. front-to-back compositing, 32 entries per step
     double T = 1.0, rr = 0.0, gg = 0.0, bb = 0.0;
-    for (int c0 = 0; c0 < m; c0 += 32) {
+    for (int c0 = 0; c0 < take; c0 += 32) {
         const int i = c0 + lane;
         double a = 0.0;
         float3 col = make_float3(0.0f, 0.0f, 0.0f);
-        if (i < m) {
+        if (i < take) {
             const int x = sx[i];
             const int id = (int)(unsigned)key[x];
             SRT_DCHECK(id >= 0 && id < s.n);
@@ -569,15 +606,21 @@ __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsign
     out[3] = 1.0 - T;
 }
 
-template <int MODE, class Src>
-__global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_packet(SceneView s, Src src, float s2, float3 bgc,
-                                                                 unsigned long long *lkey, float *lalpha,
-                                                                 unsigned *gsort, uint32_t *work, int *overflow) {
+template <int MODE, int KIND, class Src>
+__global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
+    k_composite_packet(SceneView s, Src src, PacketCompositeArgs pa, unsigned long long *lkey, float *lalpha,
+                       unsigned *gsort, uint32_t *work, int *overflow) {
     constexpr int W = kExactThreads / 32, PSTACK = 128, BATCH = 32;
+    constexpr bool BIASED = KIND != kPacketExact;
+    constexpr int KC = BIASED ? kBiasedClip : 1;
     __shared__ double sray[W][32][7];  // fp64 origin, direction, 1/|d|^2 of each lane's ray
-    __shared__ int scnt[W][32];        // valid candidates found per ray
+    __shared__ int scnt[W][32];        // list entries per ray
+    __shared__ uint32_t skey[W][32];   // biased counter mode: walk key of each ray
     __shared__ uint32_t sjob[W][BATCH + 128];
-    __shared__ int sstk[W][PSTACK];
+    __shared__ int2 sstk[W][PSTACK];   // (node, warp-min entry key)
+    __shared__ unsigned long long stopk[W][KC][32];  // biased: the kk nearest accepted (hit key, alpha) per ray,
+    __shared__ float stopa[W][KC][32];               // ascending -- the composite itself when clipping
+    __shared__ float sfar[W][32];      // far bound of each ray during a job round
     // one ray's list at a time, bucket-sorted: in shared memory up to
     // kExactSortSmem entries, else in the warp's global sort scratch
     __shared__ unsigned ssk[W][kExactSortSmem];
@@ -586,8 +629,9 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    const float sqrt_s2 = sqrtf(s2);
-    const float bg[3] = {bgc.x, bgc.y, bgc.z};
+    const float s2 = pa.s2, sqrt_s2 = sqrtf(s2);
+    const float bg[3] = {pa.bg.x, pa.bg.y, pa.bg.z};
+    const bool clip = BIASED && pa.kk <= kBiasedClip;
     const size_t lbase = ((size_t)blockIdx.x * W + wid) * 32u * (size_t)kExactCap;
     unsigned long long *wkey = lkey + lbase;
     float *walpha = lalpha + lbase;
@@ -612,11 +656,13 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
             any_valid |= valid;
             RayState r = r0;
             float far = -INFINITY;  // idle lanes hit nothing
+            int seen = 0, nbest = 0;  // biased clip: list entries ingested, depths kept
             if (valid) {
                 init_ray(r, o[0], o[1], o[2], d[0], d[1], d[2], src.t_min, src.t_max);
                 far = r.t_max0;
                 double *q = sray[wid][lane];
                 q[0] = o[0], q[1] = o[1], q[2] = o[2], q[3] = d[0], q[4] = d[1], q[5] = d[2], q[6] = r.inv_dd;
+                if (KIND == kPacketBiasedCounter) skey[wid][lane] = src.key(p, lane, f);
             }
             scnt[wid][lane] = 0;
             const unsigned vm = __ballot_sync(FULL, valid);
@@ -629,6 +675,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
             int sp = 0, njobs = 0;
             int node = (s.num_nodes4 > 0 && vm) ? 0 : kLeafEmpty;
             auto run_jobs = [&]() {
+                if (BIASED) sfar[wid][lane] = far;
                 __syncwarp();
                 for (int jb = 0; jb < njobs; jb += 32) {
                     const int j = jb + lane;
@@ -651,13 +698,25 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                         sr.t_min = er.t_min, sr.t_max0 = er.t_max0;
                         const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
                         const float4 gm = __ldg(g), ga = __ldg(g + 1), gb = __ldg(g + 2);
-                        const Screen sc = screen<MODE>(sr, gm, ga, gb, s2, sqrt_s2, er.t_max0);
-                        if (sc.maybe) {
+                        const float ofar = BIASED ? sfar[wid][ow] : er.t_max0;
+                        const Screen sc = screen<MODE>(sr, gm, ga, gb, s2, sqrt_s2, ofar);
+                        const int pid = __float_as_int(gb.z);
+                        float u = 0.0f;
+                        bool go = sc.maybe;
+                        if (KIND == kPacketBiasedCounter) {
+                            u = counter_u(skey[wid][ow], (uint32_t)pid);
+                            go = go && u < sc.alpha_hi;  // u >= alpha_hi: certainly rejected
+                        }
+                        if (go) {
                             const Cand c = candidate<MODE>(er, gm, ga, gb, s2);
-                            if (c.valid) {
+                            bool take = c.valid;
+                            if (KIND == kPacketBiasedCounter) take = take && u < c.alpha;
+                            if (KIND == kPacketBiasedTable)
+                                take = take && __ldg(pa.table + (int64_t)pid * pa.tstride) < (double)c.alpha;
+                            if (take) {
                                 const int pos = atomicAdd(&scnt[wid][ow], 1);
                                 if (pos < kExactCap) {
-                                    wkey[(size_t)ow * kExactCap + pos] = pack_hit(c.t, __float_as_int(gb.z));
+                                    wkey[(size_t)ow * kExactCap + pos] = pack_hit(c.t, pid);
                                     walpha[(size_t)ow * kExactCap + pos] = c.alpha;
                                 }
                             }
@@ -666,12 +725,40 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                 }
                 __syncwarp();
                 njobs = 0;
+                if (clip && valid) {
+                    // ingest this batch's accepted candidates into the kk nearest
+                    // (by (t, prim id)); clip beyond the kk-th
+                    const int m = min(scnt[wid][lane], kExactCap);
+                    for (; seen < m; ++seen) {
+                        const unsigned long long kk_key = wkey[(size_t)lane * kExactCap + seen];
+                        if (nbest == pa.kk && !(kk_key < stopk[wid][nbest - 1][lane])) continue;
+                        const float ka = walpha[(size_t)lane * kExactCap + seen];
+                        int q = nbest < pa.kk ? nbest++ : nbest - 1;
+                        while (q > 0 && stopk[wid][q - 1][lane] > kk_key) {
+                            stopk[wid][q][lane] = stopk[wid][q - 1][lane];
+                            stopa[wid][q][lane] = stopa[wid][q - 1][lane];
+                            --q;
+                        }
+                        stopk[wid][q][lane] = kk_key;
+                        stopa[wid][q][lane] = ka;
+                    }
+                    if (nbest == pa.kk) far = fminf(far, window_hi((double)unpack_t(stopk[wid][pa.kk - 1][lane])));
+                }
             };
             while (true) {
                 if (njobs >= BATCH || (node == kLeafEmpty && sp == 0 && njobs)) run_jobs();
                 if (node == kLeafEmpty) {
                     if (sp == 0) break;
-                    node = sstk[wid][--sp];
+                    // pop, culling entries beyond every lane's far bound
+                    const int maxfar = __reduce_max_sync(FULL, ordered_key(far, 3));
+                    while (sp > 0) {
+                        const int2 en = sstk[wid][--sp];
+                        if (en.y <= maxfar) {
+                            node = en.x;
+                            break;
+                        }
+                    }
+                    if (node == kLeafEmpty) continue;  // all culled: flush what is queued, then finish
                 }
                 SRT_DCHECK(node >= 0 && node < s.num_nodes4);
                 const float4 *np = reinterpret_cast<const float4 *>(tree + node);
@@ -699,8 +786,8 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                         tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fminf(za, zb));
                         tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
                     }
-                    // closed slab (kernels.py:279,308) clipped to [t_min, t_max]: the
-                    // walk is unclipped, so boxes wholly behind the origin are culled here
+                    // closed slab (kernels.py:279,308) clipped to [t_min, far]: boxes
+                    // wholly behind the origin are culled here
                     hitm |= fmaxf(tn, r.t_min) <= tf ? (1u << k) : 0u;
                     tn4[k] = tn;
                 }
@@ -719,8 +806,9 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                     }
                     njobs += __popc(bm);
                 }
-                // inner children: nearest (warp-min entry) first, so lists
-                // arrive nearly in depth order; the rest pushed far-to-near
+                // inner children: nearest (warp-min entry) first -- lists arrive
+                // roughly in depth order and the biased clip tightens early; the
+                // rest pushed far-to-near with their warp-min entries
                 const unsigned ih = hitm & ~leafm;
                 const unsigned ai = any & ~leafm;
                 if (ai) {
@@ -730,8 +818,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                         int wk[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? ordered_key(tn4[k], k)
-                                                                            : 0x7FFFFFFF);
+                            wk[k] = __reduce_min_sync(FULL, ((ih >> k) & 1u) ? ordered_key(tn4[k], k) : 0x7FFFFFFF);
 #define SRT_CX(a, b)                  \
     {                                 \
         int lo_ = min(wk[a], wk[b]);  \
@@ -748,7 +835,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
                         }
 #pragma unroll
                         for (int j = 3; j >= 1; --j)
-                            if (lane == 0 && j < nin) sstk[wid][sp + nin - 1 - j] = sel4(kids, wk[j] & 3);
+                            if (j < nin) sstk[wid][sp + nin - 1 - j] = make_int2(sel4(kids, wk[j] & 3), wk[j] & ~3);
                         sp += nin - 1;
                         node = sel4(kids, wk[0] & 3);
                     }
@@ -757,22 +844,49 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
             }
             if (njobs) run_jobs();  // a stack overflow left the loop with jobs queued
             __syncwarp();
-            // the warp sorts and composites each ray's list in turn
+            // the warp sorts and composites each ray's list in turn; a clipped
+            // biased ray composites its kept kk nearest itself
             const int m = scnt[wid][lane];
             double mine[4] = {0.0, 0.0, 0.0, 0.0};
-            for (unsigned todo = __ballot_sync(FULL, valid && m <= kExactCap); todo; todo &= todo - 1) {
+            if (clip && valid && m <= kExactCap) {
+                double rr = 0.0, gg = 0.0, bb = 0.0, trans = 1.0;
+                for (int i = 0; i < nbest; ++i) {
+                    const int id = (int)(unsigned)stopk[wid][i][lane];
+                    SRT_DCHECK(id >= 0 && id < s.n);
+                    const double a = (double)stopa[wid][i][lane];
+                    const float3 col = sh_color_v(s.sh, s.sh_k, s.sh_deg, id, r.fdx, r.fdy, r.fdz);
+                    const double w = trans * a;
+                    rr += w * col.x;
+                    gg += w * col.y;
+                    bb += w * col.z;
+                    trans *= 1.0 - a;
+                }
+                mine[0] = rr + trans * bg[0];
+                mine[1] = gg + trans * bg[1];
+                mine[2] = bb + trans * bg[2];
+                mine[3] = 1.0 - trans;
+            }
+            for (unsigned todo = __ballot_sync(FULL, valid && m <= kExactCap && !clip); todo; todo &= todo - 1) {
                 const int ow = __ffs(todo) - 1;
                 const double *q = sray[wid][ow];
                 double out[4];
                 const int mo = scnt[wid][ow];
                 const bool sm = mo <= kExactSortSmem;
                 composite_ray_warp(s, wkey + (size_t)ow * kExactCap, walpha + (size_t)ow * kExactCap, mo,
-                                   (float)q[3], (float)q[4], (float)q[5], bg, sm ? ssk[wid] : gsk,
-                                   sm ? ssx[wid] : gsx, sscn[wid], out);
+                                   BIASED ? min(mo, pa.kk) : mo, (float)q[3], (float)q[4], (float)q[5], bg,
+                                   sm ? ssk[wid] : gsk, sm ? ssx[wid] : gsx, sscn[wid], out);
                 if (lane == ow)
                     for (int c = 0; c < 4; ++c) mine[c] = out[c];
             }
-            if (valid && m > kExactCap) exact_ray_long<MODE>(s, r, s2, bg, mine, overflow);
+            if (valid && m > kExactCap) {
+                if constexpr (BIASED) {
+                    const double qq[6] = {o[0], o[1], o[2], d[0], d[1], d[2]};
+                    biased_ray_long<MODE, KIND == kPacketBiasedTable ? SRT_RNG_TABLE : SRT_RNG_COUNTER>(
+                        s, qq, src.key(p, lane, f), pa.ba, mine, overflow);
+                } else {
+                    exact_ray_long<MODE>(s, r, s2, bg, mine, overflow);
+                }
+            }
             for (int c = 0; c < 4; ++c) acc[c] += mine[c];
             __syncwarp();
         }
@@ -781,10 +895,10 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM) k_exact_pack
     release_counter(work);
 }
 
-// List scratch + work counter for one k_exact_packet launch (stream-ordered).
-template <int MODE, class Src>
-static srt_status launch_exact_packet(const SrtScene *s, const Src &src, float s2, const double *bg,
-                                      cudaStream_t st) {
+// List scratch + work counter for one k_composite_packet launch (stream-ordered).
+template <int MODE, int KIND, class Src>
+static srt_status launch_composite_packet(const SrtScene *s, const Src &src, const PacketCompositeArgs &pa,
+                                          cudaStream_t st) {
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
@@ -792,7 +906,7 @@ static srt_status launch_exact_packet(const SrtScene *s, const Src &src, float s
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_exact_packet<MODE, Src>, kExactThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_composite_packet<MODE, KIND, Src>, kExactThreads, 0);
     per_sm = std::max(1, std::min(per_sm, kExactBlocksPerSM));
     const int grid = num_sms * per_sm;
     const size_t entries = (size_t)grid * kExactThreads * kExactCap;
@@ -801,21 +915,27 @@ static srt_status launch_exact_packet(const SrtScene *s, const Src &src, float s
     unsigned *gsort = nullptr;
     LaunchCounter work;
     srt_status rc = work.init(s, st);
-    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lkey, entries * sizeof(unsigned long long), st), "exact list alloc");
-    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lalpha, entries * sizeof(float), st), "exact list alloc");
+    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lkey, entries * sizeof(unsigned long long), st), "list alloc");
+    if (!rc) rc = cuda_status(cudaMallocAsync((void **)&lalpha, entries * sizeof(float), st), "list alloc");
     if (!rc)
-        rc = cuda_status(cudaMallocAsync((void **)&gsort, (size_t)grid * (kExactThreads / 32) * kExactCap * 2 * sizeof(unsigned), st),
-                         "exact sort scratch alloc");
+        rc = cuda_status(
+            cudaMallocAsync((void **)&gsort, (size_t)grid * (kExactThreads / 32) * kExactCap * 2 * sizeof(unsigned), st),
+            "sort scratch alloc");
     if (!rc) {
-        k_exact_packet<MODE, Src><<<grid, kExactThreads, 0, st>>>(
-            s->view(), src, s2, make_float3((float)bg[0], (float)bg[1], (float)bg[2]), lkey, lalpha, gsort, work.p,
-            s->d_flag);
-        rc = cuda_status(cudaGetLastError(), "k_exact_packet launch");
+        k_composite_packet<MODE, KIND, Src><<<grid, kExactThreads, 0, st>>>(s->view(), src, pa, lkey, lalpha, gsort,
+                                                                            work.p, s->d_flag);
+        rc = cuda_status(cudaGetLastError(), "k_composite_packet launch");
     }
     if (lkey) cudaFreeAsync(lkey, st);
     if (lalpha) cudaFreeAsync(lalpha, st);
     if (gsort) cudaFreeAsync(gsort, st);
     return rc;
+}
+
+template <int KIND, class Src>
+static srt_status launch_composite_packet(const SrtScene *s, const Src &src, int mode, const PacketCompositeArgs &pa,
+                                          cudaStream_t st) {
+    return mode == 0 ? launch_composite_packet<0, KIND>(s, src, pa, st) : launch_composite_packet<1, KIND>(s, src, pa, st);
 }
 
 srt_status launch_biased_rays(const SrtScene *s, const SrtTraceParams *p, const double *d_rays, int64_t R, int kk,
@@ -824,6 +944,32 @@ srt_status launch_biased_rays(const SrtScene *s, const SrtTraceParams *p, const 
     if (blocks == 0) return SRT_OK;
     BiasedArgs a = biased_args(p->t_min, p->t_max, p->s2, p->mode, kk, bg, p->seed, p->ray_id0, p->sample0, d_table,
                                p->table_slots);
+    // counter / table draws: one-hemisphere batches walk as packets
+    // (coherence-sorted unless one origin), clipped at the kk-th accepted depth
+    bool one_origin = false, one_hemisphere = false;
+    if (p->rng != SRT_RNG_TRIG64 && R >= 4096 && (uint64_t)R < (1ull << 31)) {
+        srt_status rc = probe_rays(d_rays, (uint32_t)R, one_origin, one_hemisphere, st);
+        if (rc) return rc;
+    }
+    if (one_hemisphere) {
+        uint32_t *perm = nullptr;
+        void *sort_mem = nullptr;
+        srt_status rc = SRT_OK;
+        if (!one_origin) rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
+        ExactRaySrc src{d_rays, perm, (uint32_t)R, 1, d_rgb, nullptr, p->t_min, p->t_max, a.fkey, a.ray_id0, a.sample0};
+        PacketCompositeArgs pa{};
+        pa.s2 = (float)p->s2;
+        pa.bg = a.bg;
+        pa.kk = std::max(1, kk);
+        pa.table = d_table;
+        pa.tstride = p->table_slots;
+        pa.ba = a;
+        if (!rc)
+            rc = p->rng == SRT_RNG_TABLE ? launch_composite_packet<kPacketBiasedTable>(s, src, p->mode, pa, st)
+                                         : launch_composite_packet<kPacketBiasedCounter>(s, src, p->mode, pa, st);
+        if (sort_mem) cudaFreeAsync(sort_mem, st);
+        return rc;
+    }
     SceneView v = s->view();
 #define SRT_B(M, G) k_biased_rays<M, G><<<blocks, 128, 0, st>>>(v, d_rays, R, a, d_rgb, s->d_flag)
     SRT_BIASED_DISPATCH(p->rng, p->mode, SRT_B)
@@ -837,6 +983,17 @@ srt_status launch_biased_frame(const SrtScene *s, const CamD &cam, const SrtRend
     unsigned blocks = (unsigned)((n + 127) / 128);
     if (blocks == 0) return SRT_OK;
     BiasedArgs a = biased_args(0.0, DBL_MAX, p->s2, p->mode, kk, p->background, p->seed, 0, 0, nullptr, 0);
+    if (p->rng != SRT_RNG_TRIG64) {
+        // counter draws: 8x4 pixel blocks as packets
+        ExactFrameSrc src{cam, p->width, p->height, p->passes, p->pass0, (p->width + 7) / 8, p->seed, a.fkey, d_rgb,
+                          nullptr, 0.0, DBL_MAX};
+        PacketCompositeArgs pa{};
+        pa.s2 = (float)p->s2;
+        pa.bg = a.bg;
+        pa.kk = std::max(1, kk);
+        pa.ba = a;
+        return launch_composite_packet<kPacketBiasedCounter>(s, src, p->mode, pa, st);
+    }
     SceneView v = s->view();
 #define SRT_B(M, G)                                                                                          \
     k_biased_frame<M, G><<<blocks, 128, 0, st>>>(v, cam, a, p->width, p->height, p->passes, p->pass0, p->seed, \
@@ -862,9 +1019,11 @@ srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R,
         void *sort_mem = nullptr;
         srt_status rc = SRT_OK;
         if (!one_origin) rc = sort_rays(d_rays, (uint32_t)R, &perm, &sort_mem, st);
-        ExactRaySrc src{d_rays, perm, (uint32_t)R, 1, d_rgb, d_op, t_min, t_max};
-        if (!rc) rc = mode == 0 ? launch_exact_packet<0>(s, src, (float)s2, bg, st)
-                                : launch_exact_packet<1>(s, src, (float)s2, bg, st);
+        ExactRaySrc src{d_rays, perm, (uint32_t)R, 1, d_rgb, d_op, t_min, t_max, 0u, 0u, 0u};
+        PacketCompositeArgs pa{};
+        pa.s2 = (float)s2;
+        pa.bg = make_float3((float)bg[0], (float)bg[1], (float)bg[2]);
+        if (!rc) rc = launch_composite_packet<kPacketExact>(s, src, mode, pa, st);
         if (sort_mem) cudaFreeAsync(sort_mem, st);
         return rc;
     }
@@ -881,10 +1040,12 @@ srt_status launch_exact_rays(const SrtScene *s, const double *d_rays, int64_t R,
 srt_status launch_exact_frame(const SrtScene *s, const CamD &cam, const RenderArgs &a, double *d_rgb, double *d_op,
                               cudaStream_t st) {
     if ((int64_t)a.width * a.height == 0) return SRT_OK;
-    ExactFrameSrc src{cam, a.width, a.height, a.passes, a.pass0, (a.width + 7) / 8, a.seed, d_rgb, d_op, 0.0,
+    ExactFrameSrc src{cam, a.width, a.height, a.passes, a.pass0, (a.width + 7) / 8, a.seed, 0u, d_rgb, d_op, 0.0,
                       DBL_MAX};
-    const double bg[3] = {a.bg[0], a.bg[1], a.bg[2]};
-    return a.mode == 0 ? launch_exact_packet<0>(s, src, a.s2, bg, st) : launch_exact_packet<1>(s, src, a.s2, bg, st);
+    PacketCompositeArgs pa{};
+    pa.s2 = a.s2;
+    pa.bg = make_float3(a.bg[0], a.bg[1], a.bg[2]);
+    return launch_composite_packet<kPacketExact>(s, src, a.mode, pa, st);
 }
 
 }  // namespace srt

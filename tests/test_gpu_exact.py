@@ -248,3 +248,55 @@ def test_exact_frame_long_lists(layers):
     closed = (trans[:layers, None] * alphas[:, None] * colors).sum(axis=0) + trans[layers] * np.array([0.2, 0.3, 0.4])
     np.testing.assert_allclose(buf.rgb.reshape(-1, 3), np.broadcast_to(closed, (128, 3)), rtol=1e-4)
     np.testing.assert_allclose(buf.opacity, 1.0 - trans[layers], rtol=1e-5)
+
+
+@pytest.mark.parametrize("kk", [1, 4, 12])
+def test_biased_frame_packets_vs_oracle(oracle, kk):
+    """render_biased walks 8x4 pixel blocks as packets (k <= 8: clipped at
+    the k-th accepted depth; 12: unclipped) -- 2 passes of a 20k SH-3
+    cloud at 56x40 against the oracle's biased_batch over the same camera
+    rays, draw (seed, py*W+px, pass)."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, generate_camera_ray, render_biased
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    a = density_cloud(20_000, seed=9)
+    pk = a.packed
+    cam = front_camera()
+    W, H = 56, 40
+    st = RenderSettings(width=W, height=H, spp=2, seed=5, background=[0.2, 0.1, 0.0])
+    frame = render_biased(a, cam, st, kk)
+    want = np.zeros((H * W, 3))
+    for f in range(2):
+        rays = [generate_camera_ray(cam, st, (x, y), f) for y in range(H) for x in range(W)]
+        o = np.array([r[0] for r in rays])
+        d = np.array([r[1] for r in rays])
+        want += oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 3, o, d, kk, s2=S2,
+                                    background=(0.2, 0.1, 0.0), rng="counter", seed=5, ray_id0=0, sample0=f)
+    want /= 2
+    assert _close_fraction(frame.reshape(-1, 3), want) >= 0.995
+
+
+@pytest.mark.parametrize("rng,kk", [("counter", 1), ("counter", 6), ("counter", 20), ("table", 3)])
+def test_biased_rays_packets_vs_oracle(oracle, rng, kk):
+    """One-hemisphere biased_batch batches of >= 4096 rays from distinct
+    origins walk as coherence-sorted packets; draws keyed by the caller's ray
+    index (counter) or read from the table."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    a = density_cloud(10_000, seed=12)
+    pk = a.packed
+    rs = np.random.default_rng(13)
+    R = 5000
+    d = rs.normal(size=(R, 3)) * [0.2, 0.2, 0.0] + [0.0, 0.0, 1.0]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = rs.uniform(-1.0, 1.0, (R, 3)) * [1, 1, 0] + [0, 0, -4]
+    table = rs.uniform(0.0, 1.0, pk.means.shape[0]) if rng == "table" else None
+    sc = DeviceScene.from_packed(pk)
+    sc.build_bvh(np.sqrt(S2))
+    kw = dict(table=table) if table is not None else dict(seed=21, ray_id0=7, sample0=3)
+    rgb = sc.biased_rays(o, d, kk, s2=S2, background=(0.1, 0.3, 0.2), rng=rng, **kw)
+    sc.close()
+    want = oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 3, o, d, kk, s2=S2,
+                               background=(0.1, 0.3, 0.2), rng=rng, **kw)
+    assert _close_fraction(rgb, want) >= 0.995
