@@ -855,8 +855,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     __shared__ unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
     __shared__ uint32_t sjob[W][BATCH + 128];  // leaf job: (slot << 5) | owner lane
-    __shared__ int sstk_node[W][PSTACK];
-    __shared__ int sstk_key[W][PSTACK];
+    __shared__ int2 sstk[W][PSTACK];  // (node, warp-min entry key): one 64-bit word per entry
     // explicit-ray packets (Src::kRayOrigin): each lane's own origin
     constexpr bool RO = Src::kRayOrigin;
     __shared__ float4 sorg[RO ? W : 1][32];    // fp32 origin + max |o_i|
@@ -972,8 +971,9 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
 #ifdef SRT_PACKET_CLOCKS
                     ++pk_pops;
 #endif
-                    if (sstk_key[wid][sp] <= maxfar) {
-                        node = sstk_node[wid][sp];
+                    const int2 e = sstk[wid][sp];
+                    if (e.y <= maxfar) {
+                        node = e.x;
                         SRT_DCHECK(node >= 0 && node < s.num_nodes4);
                         break;
                     }
@@ -1092,8 +1092,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
 #pragma unroll
                     for (int j = 3; j >= 1; --j)
                         if (j < nin) {
-                            sstk_node[wid][sp + nin - 1 - j] = sel4(kids, wk[j] & 3);
-                            sstk_key[wid][sp + nin - 1 - j] = wk[j] & ~3;
+                            sstk[wid][sp + nin - 1 - j] = make_int2(sel4(kids, wk[j] & 3), wk[j] & ~3);
                         }
                     sp += nin - 1;
                     node = sel4(kids, wk[0] & 3);
