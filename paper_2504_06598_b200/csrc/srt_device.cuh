@@ -342,6 +342,24 @@ struct ExactRay {
     float fdx, fdy, fdz, t_min, t_max0;
 };
 
+// The screen's transcendentals without denormal handling (MUFU directly):
+// exp2 flushes results below 2^-126 to 0 and rsqrt treats a denormal input
+// as 0.  Both keep the screen's bounds conservative -- alpha_hi >= 1e-7 bounds
+// any flushed alpha from above, a flushed alpha_lo only loosens the lower
+// bound -- and a denormal d.A.d (an eigenvalue of A below 1e-38 along the ray,
+// i.e. a primitive scale above 1e18) is the only input they change.
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float exp_ftz(float x) { return ex2_ftz(x * 1.4426950408889634f); }
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Stage-1 screen: the same quantities as `candidate` in plain fp32 (no
 // fp64), with a conservative bound on their rounding error.  A candidate the
 // screen rejects is certainly invalid or beyond `far`; `alpha_hi` bounds
@@ -361,7 +379,7 @@ struct Screen {
     __device__ __forceinline__ bool sure(float s2, float t_min, float t_max0) const {
         return (dad > 0.0f) && isfinite(dad) && (mah + mr <= s2) && (t - mt > t_min) && (t + mt < t_max0);
     }
-    __device__ __forceinline__ float alpha_lo() const { return alpha_base * __expf(-mr) * 0.9999f - 1e-7f; }
+    __device__ __forceinline__ float alpha_lo() const { return alpha_base * exp_ftz(-mr) * 0.9999f - 1e-7f; }
 };
 
 // Minimal fp32 ray for the screen (camera rays share one origin).
@@ -390,7 +408,7 @@ __device__ __forceinline__ Screen screen(const R &r, const float4 &m, const floa
     float awz = a02 * wx + a12 * wy + a22 * wz;
     float daw = r.fdx * awx + r.fdy * awy + r.fdz * awz;
     float waw = wx * awx + wy * awy + wz * awz;
-    float rs = rsqrtf(dad);
+    float rs = rsqrt_ftz(dad);
     float inv_dad = rs * rs;
     float resid = waw - daw * daw * inv_dad;
     float mah, t;
@@ -414,7 +432,7 @@ __device__ __forceinline__ Screen screen(const R &r, const float4 &m, const floa
     float mt = e + es * rs + 2.0e-6f * (fabsf(t) + 1.0f);
     sc.t_lo = t - mt;
     sc.maybe = (dad > 0.0f) && (mah - mr <= s2) && (t - mt <= far) && (t + mt > r.t_min) && (t - mt < r.t_max0);
-    sc.alpha_base = m.w * __expf(-0.5f * fmaxf(resid - mr, 0.0f));
+    sc.alpha_base = m.w * exp_ftz(-0.5f * fmaxf(resid - mr, 0.0f));
     sc.alpha_hi = sc.alpha_base * 1.0001f + 1e-7f;
     // alpha_lo(): the same error terms the other way (exp(-mr) widens the
     // band by the residual's bound; the opacity is fp32-rounded)
