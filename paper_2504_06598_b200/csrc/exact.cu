@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
             const unsigned nz_m = __ballot_sync(FULL, valid && signbit(r.idz));
             const int oct = (nx_m ? 1 : 0) | (ny_m ? 2 : 0) | (nz_m ? 4 : 0);
             const bool mixed = (nx_m && nx_m != vm) || (ny_m && ny_m != vm) || (nz_m && nz_m != vm);
-            const Node4 *tree = s.nodes8 + (size_t)oct * (size_t)s.num_nodes4;
+            const uint32_t obase = (uint32_t)oct * (uint32_t)s.num_nodes4;
             int sp = 0, njobs = 0;
             int node = (s.num_nodes4 > 0 && vm) ? 0 : kLeafEmpty;
             auto run_jobs = [&]() {
@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                     if (node == kLeafEmpty) continue;  // all culled: flush what is queued, then finish
                 }
                 SRT_DCHECK(node >= 0 && node < s.num_nodes4);
-                const float4 *np = reinterpret_cast<const float4 *>(tree + node);
+                const float4 *np = reinterpret_cast<const float4 *>(s.nodes8 + (obase + (uint32_t)node));
                 const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
                              az = __ldg(np + 4), bz = __ldg(np + 5);
                 const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
@@ -802,7 +802,11 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                     const unsigned bm = __ballot_sync(FULL, h);
                     if (h) {
                         SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
+#ifdef SRT_OCT_LEAF_SHIFT
+                        sjob[wid][njobs + __popc(bm & lt)] = (uint32_t)~sel4(kids, k) | (uint32_t)lane;
+#else
                         sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+#endif
                     }
                     njobs += __popc(bm);
                 }

@@ -659,6 +659,12 @@ __global__ void k_octant_nodes(const Node4 *__restrict__ n4, int m, Node4 *out) 
     if (oct & 1) { o.lox = a.hix; o.hix = a.lox; }
     if (oct & 2) { o.loy = a.hiy; o.hiy = a.loy; }
     if (oct & 4) { o.loz = a.hiz; o.hiz = a.loz; }
+#ifdef SRT_OCT_LEAF_SHIFT
+    // leaf children as ~(slot << 5): a packet's job word is ~code | lane
+    int *kc = &o.kids.x;
+    for (int k = 0; k < 4; ++k)
+        if (kc[k] < 0 && kc[k] != kLeafEmpty) kc[k] = ~(int)((uint32_t)~kc[k] << 5);
+#endif
     out[i] = o;
 }
 
@@ -671,6 +677,10 @@ srt_status collapse4(SrtScene *s) {
     s->d_nodes8 = nullptr;
     const int m = s->num_nodes4;
     if (m == 0) return SRT_OK;
+    if ((uint64_t)m * 8 >= (1ull << 32)) {  // packet kernels index the octant copies with 32 bits
+        set_error("BVH too large for the octant node copies");
+        return SRT_ERR_INVALID_ARG;
+    }
     rc = cuda_status(cudaMalloc(&s->d_nodes8, sizeof(Node4) * 8 * (size_t)m), "octant node alloc");
     if (rc) return rc;
     const int64_t total = (int64_t)m * 8;
