@@ -802,11 +802,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                     const unsigned bm = __ballot_sync(FULL, h);
                     if (h) {
                         SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
-#ifdef SRT_OCT_LEAF_SHIFT
-                        sjob[wid][njobs + __popc(bm & lt)] = (uint32_t)~sel4(kids, k) | (uint32_t)lane;
-#else
                         sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
-#endif
                     }
                     njobs += __popc(bm);
                 }

@@ -659,12 +659,6 @@ __global__ void k_octant_nodes(const Node4 *__restrict__ n4, int m, Node4 *out) 
     if (oct & 1) { o.lox = a.hix; o.hix = a.lox; }
     if (oct & 2) { o.loy = a.hiy; o.hiy = a.loy; }
     if (oct & 4) { o.loz = a.hiz; o.hiz = a.loz; }
-#ifdef SRT_OCT_LEAF_SHIFT
-    // leaf children as ~(slot << 5): a packet's job word is ~code | lane
-    int *kc = &o.kids.x;
-    for (int k = 0; k < 4; ++k)
-        if (kc[k] < 0 && kc[k] != kLeafEmpty) kc[k] = ~(int)((uint32_t)~kc[k] << 5);
-#endif
     out[i] = o;
 }
 

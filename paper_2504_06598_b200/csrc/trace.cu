@@ -1052,11 +1052,7 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 {
                     // predicated shared store (no divergent branch to reconverge):
                     // 1.787 -> 1.762 ms seed mean
-#ifdef SRT_OCT_LEAF_SHIFT
-                    const uint32_t code = (uint32_t)~sel4(kids, k) | (uint32_t)lane;
-#else
                     const uint32_t code = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
-#endif
                     SRT_DCHECK(!h || njobs + __popc(bm & lt) < BATCH + 128);
                     const uint32_t addr = (uint32_t)__cvta_generic_to_shared(&sjob[wid][njobs + __popc(bm & lt)]);
                     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}"
