@@ -347,9 +347,12 @@ struct CameraSource {
     // Walk result -> either the hit buffer (split trace/shade) or, fused, the
     // SH colour of every slot's hit on this ray's direction plus background
     // for misses, accumulated exactly as k_shade_pass does (kernels.py:657-673).
+    // f64v / f64pix (packet kernel): a pixel bound for the f64 frame is
+    // returned there instead of stored (store_f64_packet writes the warp's)
     template <int NS>
     __device__ __forceinline__ void finish_shaded(uint32_t idx, const Slots<NS> &sl, const SceneView &s, float fx,
-                                                  float fy, float fz) const {
+                                                  float fy, float fz, double *f64v = nullptr,
+                                                  int64_t *f64pix = nullptr) const {
         if (hits) {
             finish<NS>(idx, sl);
             return;
@@ -392,6 +395,14 @@ struct CameraSource {
                 // layout -- over PCIe when it is mapped host memory, so the
                 // device->host transfer overlaps the rest of the walk
                 int64_t pix = (int64_t)py * a.width + px;
+                if (f64v) {  // the packet kernel stores the warp's pixels together
+                    f64v[0] = (double)(acc.x * inv);
+                    f64v[1] = (double)(acc.y * inv);
+                    f64v[2] = (double)(acc.z * inv);
+                    f64v[3] = (double)(acc.w * inv);
+                    *f64pix = pix;
+                    return;
+                }
                 rgb64[pix * 3 + 0] = (double)(acc.x * inv);
                 rgb64[pix * 3 + 1] = (double)(acc.y * inv);
                 rgb64[pix * 3 + 2] = (double)(acc.z * inv);
@@ -441,7 +452,7 @@ struct ArraySource {
     }
     template <int NS>
     __device__ __forceinline__ void finish_shaded(uint32_t idx, const Slots<NS> &sl, const SceneView &, float, float,
-                                                  float) const {
+                                                  float, double * = nullptr, int64_t * = nullptr) const {
         finish<NS>(idx, sl);
     }
     __device__ __forceinline__ void done() const {}
@@ -827,6 +838,50 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace_coop(SceneView s, Src s
 // ---------------------------------------------------------------------------
 // BATCH: leaf jobs are run once at least BATCH are queued; MINB: minimum
 // resident blocks per SM requested from the register allocator.
+// The f64 frame pixels of a packet (an 8x4 block when the packet is whole):
+// staged in shared memory and written as 16-byte words, each row's 8 pixels
+// one contiguous 192 B (rgb) + 64 B (opacity) run -- full PCIe write
+// payloads into mapped host memory instead of 8-byte stores at a 24-byte
+// stride.  Partial or unaligned packets store per lane.
+template <class Src>
+__device__ __forceinline__ void store_f64_packet(const Src &src, bool f64, const double v[4], int64_t pix,
+                                                 double *stage_rgb, double *stage_op) {
+    if constexpr (!Src::kRayOrigin) {
+        const unsigned FULL = 0xffffffffu;
+        const int lane = threadIdx.x & 31;
+        const unsigned m = __ballot_sync(FULL, f64);
+        if (!m) return;
+        double *rgb = src.rgb64, *op = src.op64;
+        const int64_t W = src.a.width;
+        const int64_t pix0 = __shfl_sync(FULL, pix, 0);
+        const bool block = m == FULL && pix == pix0 + (int64_t)(lane >> 3) * W + (lane & 7);
+        const bool aligned = ((((uintptr_t)rgb | (uintptr_t)op) & 15u) == 0) && !((pix0 | W) & 1);
+        if (__all_sync(FULL, block) && aligned) {
+            stage_rgb[lane * 3] = v[0];
+            stage_rgb[lane * 3 + 1] = v[1];
+            stage_rgb[lane * 3 + 2] = v[2];
+            stage_op[lane] = v[3];
+            __syncwarp();
+            for (int g = lane; g < 48; g += 32) {  // 4 rows x 12 double2 of rgb
+                const int r = g / 12, q = g - r * 12;
+                const double2 w = *reinterpret_cast<const double2 *>(stage_rgb + r * 24 + 2 * q);
+                *reinterpret_cast<double2 *>(rgb + (pix0 + r * W) * 3 + 2 * q) = w;
+            }
+            if (lane < 16) {  // 4 rows x 4 double2 of opacity
+                const int r = lane >> 2, q = lane & 3;
+                const double2 w = *reinterpret_cast<const double2 *>(stage_op + r * 8 + 2 * q);
+                *reinterpret_cast<double2 *>(op + pix0 + r * W + 2 * q) = w;
+            }
+            __syncwarp();
+        } else if (f64) {
+            rgb[pix * 3] = v[0];
+            rgb[pix * 3 + 1] = v[1];
+            rgb[pix * 3 + 2] = v[2];
+            op[pix] = v[3];
+        }
+    }
+}
+
 #ifdef SRT_PACKET_CLOCKS
 // Per-packet timing (experiments only, -DSRT_PACKET_CLOCKS via
 // tools/build_variant.sh): start (globaltimer ns) and duration | smid << 48
@@ -851,8 +906,8 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
     constexpr int W = kTraceThreads / 32;
     constexpr int PSTACK = 128;
     __shared__ float4 sdir[W][32];      // fp32 direction + far bound of each lane's ray
-    __shared__ double sdd[W][32][3];    // fp64 direction (exact stage)
-    __shared__ unsigned long long sbest[W][32][NS];
+    __shared__ __align__(16) double sdd[W][32][3];  // fp64 direction (exact stage); f64 pixel staging
+    __shared__ __align__(16) unsigned long long sbest[W][32][NS];
     __shared__ uint32_t skey[W][32][NS];
     __shared__ uint32_t sjob[W][BATCH + 128];  // leaf job: (slot << 5) | owner lane
     __shared__ int2 sstk[W][PSTACK];  // (node, warp-min entry key): one 64-bit word per entry
@@ -1103,6 +1158,8 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
             }
             __syncwarp();
         }
+        double f64v[4] = {-1.0, 0.0, 0.0, 0.0};
+        int64_t f64pix = -1;
         if (valid) {
 #pragma unroll
             for (int k = 0; k < NS; ++k) {
@@ -1110,8 +1167,12 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 sl.id[k] = (int)(unsigned)v;
                 sl.t[k] = unpack_t(v);
             }
-            src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz);
+            src.template finish_shaded<NS>(idx, sl, s, r.fdx, r.fdy, r.fdz, f64v, &f64pix);
         }
+        __syncwarp();
+        // the packet's f64 frame pixels (fused last pass into rgb64/op64);
+        // staged in sdd / sbest, which the next packet rewrites after this
+        store_f64_packet(src, f64pix >= 0, f64v, f64pix, &sdd[wid][0][0], reinterpret_cast<double *>(&sbest[wid][0][0]));
         __syncwarp();
 #ifdef SRT_PACKET_CLOCKS
         if (lane == 0 && (base >> 5) < kClockSlots) {
