@@ -61,12 +61,10 @@ static srt_status launch_pack_rays(const double *d_o, const double *d_d, int64_t
 // The caller's (R,3) origin and direction arrays -> (R,6) ray records on the
 // device: two contiguous uploads into `stage` (48 R bytes), interleaved there
 // (no host packing pass).
-static srt_status upload_rays(const double *o, const double *d, int64_t R, double *stage, double *d_rays,
-                              cudaStream_t st) {
-    srt_status rc = cuda_status(cudaMemcpyAsync(stage, o, sizeof(double) * 3 * R, cudaMemcpyHostToDevice, st),
-                                "origins upload");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(stage + 3 * R, d, sizeof(double) * 3 * R, cudaMemcpyHostToDevice, st),
-                              "dirs upload");
+static srt_status upload_rays(SrtScene *s, const double *o, const double *d, int64_t R, double *stage,
+                              double *d_rays, cudaStream_t st) {
+    srt_status rc = copy_h2d(s, stage, o, sizeof(double) * 3 * R, st);
+    if (!rc) rc = copy_h2d(s, stage + 3 * R, d, sizeof(double) * 3 * R, st);
     if (!rc) rc = launch_pack_rays(stage, stage + 3 * R, R, d_rays, st);
     return rc;
 }
@@ -286,9 +284,9 @@ srt_status srt_scene_create(const SrtSceneDesc *desc, int32_t device, SrtScene *
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_cov6, sizeof(double) * n * 6), "cov alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_opac, sizeof(double) * n), "opacity alloc");
         if (!rc) rc = cuda_status(cudaMalloc(&s->d_sh, sizeof(float) * n * 3 * s->sh_k), "sh alloc");
-        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_means, desc->means, sizeof(double) * n * 3, cudaMemcpyHostToDevice, st), "means upload");
-        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_cov6, desc->cov_inv6, sizeof(double) * n * 6, cudaMemcpyHostToDevice, st), "cov upload");
-        if (!rc) rc = cuda_status(cudaMemcpyAsync(s->d_opac, desc->opacities, sizeof(double) * n, cudaMemcpyHostToDevice, st), "opacity upload");
+        if (!rc) rc = copy_h2d(s, s->d_means, desc->means, sizeof(double) * n * 3, st);
+        if (!rc) rc = copy_h2d(s, s->d_cov6, desc->cov_inv6, sizeof(double) * n * 6, st);
+        if (!rc) rc = copy_h2d(s, s->d_opac, desc->opacities, sizeof(double) * n, st);
         if (!rc) {
             shf.assign((size_t)n * 3 * s->sh_k, 0.0f);
             if (desc->sh)
@@ -350,6 +348,7 @@ srt_status srt_scene_destroy(SrtScene *s) {
     if (s->h_flag) cudaFreeHost(s->h_flag);
     cudaFree(s->d_counter);
     cudaFree(s->d_scratch);
+    stage_release(s);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
     return SRT_OK;
@@ -692,9 +691,9 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     double *d_stage = (double *)(base + stage_off);
     // contiguous uploads straight from the caller's arrays, interleaved into
     // the (R,6) ray records on the device (no host packing pass)
-    rc = upload_rays(origins, dirs, R, d_stage, d_rays, st);
+    rc = upload_rays(s, origins, dirs, R, d_stage, d_rays, st);
     if (!rc && d_table)
-        rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
+        rc = copy_h2d(s, d_table, p->table, table_bytes, st);
     double *d_t64 = (double *)(base + ray_bytes);
     if (p->rng == SRT_RNG_TRIG64) d_id = (int32_t *)(base + ray_bytes + sizeof(double) * R * nslots);
     if (!rc) {
@@ -710,8 +709,8 @@ srt_status srt_trace_rays(const SrtScene *sc, const SrtTraceParams *p, const dou
     int64_t *w_id = (int64_t *)(d_stage + m);
     if (!rc) rc = launch_widen_hits(p->rng == SRT_RNG_TRIG64 ? nullptr : d_t, p->rng == SRT_RNG_TRIG64 ? d_t64 : nullptr,
                                     d_id, m, w_t, w_id, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_t, w_t, sizeof(double) * m, cudaMemcpyDeviceToHost, st), "t download");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_id, w_id, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, st), "id download");
+    if (!rc) rc = copy_d2h(s, out_t, w_t, sizeof(double) * m, st);
+    if (!rc) rc = copy_d2h(s, out_id, w_id, sizeof(int64_t) * m, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -737,9 +736,9 @@ srt_status srt_transmittance_rays(const SrtScene *sc, const double *origins, con
     if (rc) return rc;
     double *d_rays = (double *)s->d_scratch;
     double *d_out = d_rays + R * 6;
-    rc = upload_rays(origins, dirs, R, d_out + R, d_rays, st);
+    rc = upload_rays(s, origins, dirs, R, d_out + R, d_rays, st);
     if (!rc) rc = launch_transmittance(s, d_rays, R, t_min, t_max, mode, s2, d_out, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out, d_out, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "download");
+    if (!rc) rc = copy_d2h(s, out, d_out, sizeof(double) * R, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -767,10 +766,10 @@ srt_status srt_exact_rays(const SrtScene *sc, const double *origins, const doubl
     double *d_rays = (double *)s->d_scratch;
     double *d_rgb = d_rays + R * 6;
     double *d_op = d_rgb + R * 3;
-    rc = upload_rays(origins, dirs, R, d_op + R, d_rays, st);
+    rc = upload_rays(s, origins, dirs, R, d_op + R, d_rays, st);
     if (!rc) rc = launch_exact_rays(s, d_rays, R, t_min, t_max, mode, s2, background, d_rgb, d_op, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * R * 3, cudaMemcpyDeviceToHost, st), "rgb");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * R, cudaMemcpyDeviceToHost, st), "op");
+    if (!rc) rc = copy_d2h(s, out_rgb, d_rgb, sizeof(double) * R * 3, st);
+    if (!rc) rc = copy_d2h(s, out_op, d_op, sizeof(double) * R, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -797,11 +796,11 @@ srt_status srt_biased_rays(const SrtScene *sc, const SrtTraceParams *p, const do
     double *d_rays = (double *)s->d_scratch;
     double *d_rgb = d_rays + R * 6;
     double *d_table = table_bytes ? d_rgb + R * 3 : nullptr;
-    rc = upload_rays(origins, dirs, R, (double *)((char *)(d_rgb + R * 3) + table_bytes), d_rays, st);
+    rc = upload_rays(s, origins, dirs, R, (double *)((char *)(d_rgb + R * 3) + table_bytes), d_rays, st);
     if (!rc && d_table)
-        rc = cuda_status(cudaMemcpyAsync(d_table, p->table, table_bytes, cudaMemcpyHostToDevice, st), "table upload");
+        rc = copy_h2d(s, d_table, p->table, table_bytes, st);
     if (!rc) rc = launch_biased_rays(s, p, d_rays, R, kk, background, d_table, d_rgb, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, rgb_bytes, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = copy_d2h(s, out_rgb, d_rgb, rgb_bytes, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -824,7 +823,7 @@ srt_status srt_render_biased(const SrtScene *sc, const SrtCamera *camera, const 
     if (rc) return rc;
     double *d_rgb = (double *)s->d_scratch;
     rc = launch_biased_frame(s, make_cam(camera), p, kk, d_rgb, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb");
+    if (!rc) rc = copy_d2h(s, out_rgb, d_rgb, sizeof(double) * npix * 3, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -848,8 +847,8 @@ srt_status srt_render_exact(const SrtScene *sc, const SrtCamera *camera, const S
     double *d_rgb = (double *)s->d_scratch;
     double *d_op = d_rgb + npix * 3;
     rc = launch_exact_frame(s, make_cam(camera), make_render_args(p), d_rgb, d_op, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "op");
+    if (!rc) rc = copy_d2h(s, out_rgb, d_rgb, sizeof(double) * npix * 3, st);
+    if (!rc) rc = copy_d2h(s, out_op, d_op, sizeof(double) * npix, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }
@@ -1083,11 +1082,9 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
             rc = launch_resolve_fixed(a, d_acc64, p->passes, nullptr, direct ? m_rgb : f_rgb, direct ? m_op : f_op,
                                       st);
         if (!rc && !direct) {
-            rc = cuda_status(cudaMemcpyAsync(out_rgb, f_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st),
-                             "rgb download");
+            rc = copy_d2h(s, out_rgb, f_rgb, sizeof(double) * npix * 3, st);
             if (!rc)
-                rc = cuda_status(cudaMemcpyAsync(out_op, f_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st),
-                                 "opacity download");
+                rc = copy_d2h(s, out_op, f_op, sizeof(double) * npix, st);
         }
         if (!rc) rc = check_flag(s, st);
         return rc;
@@ -1132,8 +1129,8 @@ srt_status srt_render(const SrtScene *sc, const SrtCamera *camera, const SrtRend
         return rc;
     }
     if (!rc) rc = launch_resolve_f64(a, d_out, d_rgb, d_op, st);
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_rgb, d_rgb, sizeof(double) * npix * 3, cudaMemcpyDeviceToHost, st), "rgb download");
-    if (!rc) rc = cuda_status(cudaMemcpyAsync(out_op, d_op, sizeof(double) * npix, cudaMemcpyDeviceToHost, st), "opacity download");
+    if (!rc) rc = copy_d2h(s, out_rgb, d_rgb, sizeof(double) * npix * 3, st);
+    if (!rc) rc = copy_d2h(s, out_op, d_op, sizeof(double) * npix, st);
     if (!rc) rc = check_flag(s, st);
     return rc;
 }

@@ -38,6 +38,9 @@ struct SrtScene {
     // cached scratch for the host-pointer entry points
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
+    // page-locked staging ring for pageable caller arrays (hostcopy.cu)
+    void *h_stage[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     cudaStream_t stream = nullptr;
     // Host entry points that use the scene's stream and scratch serialise on
     // `mu` (calls on one handle serialise).  Every persistent
@@ -180,5 +183,12 @@ struct LaunchCounter {
 };
 
 int64_t shard_tiles(int width, int height, int shard_index, int shard_count);
+
+// Caller-array transfers (hostcopy.cu): pageable memory through the scene's
+// page-locked ring with parallel host copies, pinned memory directly.  Both
+// return with the host side complete (d2h: the data is in dst).
+srt_status copy_h2d(SrtScene *s, void *dst, const void *src, size_t bytes, cudaStream_t st);
+srt_status copy_d2h(SrtScene *s, void *dst, const void *src, size_t bytes, cudaStream_t st);
+void stage_release(SrtScene *s);
 
 }  // namespace srt
