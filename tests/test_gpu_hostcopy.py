@@ -24,7 +24,7 @@ def scene():
 
 
 def _batched(f, o, d, step=40_000):
-    outs = [f(o[i:i + step], d[i:i + step]) for i in range(0, o.shape[0], step)]
+    outs = [f(o[i:i + step], d[i:i + step], i) for i in range(0, o.shape[0], step)]
     if isinstance(outs[0], tuple):
         return tuple(np.concatenate([x[k] for x in outs]) for k in range(len(outs[0])))
     return np.concatenate(outs)
@@ -33,7 +33,8 @@ def _batched(f, o, d, step=40_000):
 def test_trace_rays_staged_equals_direct(scene):
     o, d = random_rays(np.random.default_rng(21), 700_001, box=2.0)  # 16.8 MB per array: 3 chunks
     t, ids = scene.trace_rays(o, d, s2=S2, nslots=2, seed=5)
-    t2, ids2 = _batched(lambda a, b: scene.trace_rays(a, b, s2=S2, nslots=2, seed=5), o, d)
+    # the counter draw is keyed on the ray's index: batches start at ray_id0 = offset
+    t2, ids2 = _batched(lambda a, b, i: scene.trace_rays(a, b, s2=S2, nslots=2, seed=5, ray_id0=i), o, d)
     assert np.array_equal(ids, ids2)
     assert np.array_equal(t, t2)
 
@@ -41,13 +42,13 @@ def test_trace_rays_staged_equals_direct(scene):
 def test_transmittance_staged_equals_direct(scene):
     o, d = random_rays(np.random.default_rng(22), 450_003, box=2.0)
     tr = scene.transmittance(o, d, s2=S2)
-    tr2 = _batched(lambda a, b: scene.transmittance(a, b, s2=S2), o, d)
+    tr2 = _batched(lambda a, b, i: scene.transmittance(a, b, s2=S2), o, d)
     np.testing.assert_allclose(tr, tr2, rtol=1e-12, atol=1e-300)
 
 
 def test_exact_rays_staged_equals_direct(scene):
     o, d = random_rays(np.random.default_rng(23), 120_001, box=2.0)  # rgb out 2.9 MB
     rgb, op = scene.exact_rays(o, d, s2=S2, background=(0.1, 0.2, 0.3))
-    rgb2, op2 = _batched(lambda a, b: scene.exact_rays(a, b, s2=S2, background=(0.1, 0.2, 0.3)), o, d)
+    rgb2, op2 = _batched(lambda a, b, i: scene.exact_rays(a, b, s2=S2, background=(0.1, 0.2, 0.3)), o, d)
     np.testing.assert_allclose(rgb, rgb2, rtol=1e-12, atol=1e-15)
     np.testing.assert_allclose(op, op2, rtol=1e-12, atol=1e-15)
