@@ -1752,12 +1752,15 @@ __global__ void __launch_bounds__(128) k_transmittance(SceneView s, const double
 }
 
 // Coherent transmittance batches (one hemisphere, e.g. shadow rays towards a
-// light): the warp walks its 32 rays as a packet -- one node fetch and slab
-// test per lane, leaf hits compacted by ballot into a job queue -- and every
-// job evaluates the owner's fp64 candidate exactly as k_transmittance does,
-// multiplying (1 - alpha) into the owner's product in shared memory.  The
-// walk is unclipped (kernels.py:392-432), so nothing is culled; only the
-// product order differs from the per-lane walk (roundoff).
+// light): the warp walks its 32 rays as a packet over the octant node copies
+// (near planes first: 6 FMAs and two 3-way min/max per child, as in
+// k_trace_packet), leaf hits compacted by ballot into a job queue; each job
+// screens the owner's ray in fp32 and evaluates the owner's fp64 candidate
+// exactly as the per-lane walk does, multiplying (1 - alpha) into the owner's
+// product in shared memory.  The owner's fp64 origin, direction and 1/|d|^2
+// sit in shared memory, so a job builds no RayState.  The walk is unclipped
+// (kernels.py:392-432): nothing is culled, any visit order gives the same
+// factors; only the product order differs from the per-lane walk (roundoff).
 template <int MODE>
 __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneView s, const double *__restrict__ rays,
                                                                         const uint32_t *__restrict__ perm, uint32_t R,
@@ -1765,15 +1768,15 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
                                                                         double *out, uint32_t *work, int *overflow) {
     constexpr int W = kTraceThreads / 32;
     constexpr int PSTACK = 128, BATCH = 32;
-    __shared__ double sray[W][32][6];
+    __shared__ double sray[W][32][7];  // fp64 origin, direction, 1/|d|^2
     __shared__ unsigned long long sprod[W][32];
-    __shared__ int sjob[W][BATCH + 128];
-    __shared__ unsigned char sown[W][BATCH + 128];
+    __shared__ uint32_t sjob[W][BATCH + 128];  // (slot << 5) | owner lane
     __shared__ int sstk[W][PSTACK];
     const unsigned FULL = 0xffffffffu;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const float sqrt_s2 = sqrtf(s2);
     const unsigned lt = (1u << lane) - 1u;
+    const float ft_min = (float)t_min, ft_max = t_max >= 3.0e38 ? INFINITY : (float)t_max;
     while (true) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(work, 32u);
@@ -1786,42 +1789,59 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
         float far;
         if (valid) {
             const double *q = rays + (int64_t)ri * 6;
-#pragma unroll
-            for (int c = 0; c < 6; ++c) sray[wid][lane][c] = q[c];
             init_ray(r, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+            double *sq = sray[wid][lane];
+            sq[0] = r.ox, sq[1] = r.oy, sq[2] = r.oz, sq[3] = r.dx, sq[4] = r.dy, sq[5] = r.dz, sq[6] = r.inv_dd;
             sprod[wid][lane] = __double_as_longlong(1.0);
             far = r.t_max0;
         } else {
             init_ray(r, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, 0.0, 1.0);
             far = -INFINITY;  // hits nothing
         }
+        const unsigned vm = __ballot_sync(FULL, valid);
+        const unsigned nx_m = __ballot_sync(FULL, valid && signbit(r.idx));
+        const unsigned ny_m = __ballot_sync(FULL, valid && signbit(r.idy));
+        const unsigned nz_m = __ballot_sync(FULL, valid && signbit(r.idz));
+        const int oct = (nx_m ? 1 : 0) | (ny_m ? 2 : 0) | (nz_m ? 4 : 0);
+        const bool mixed = (nx_m && nx_m != vm) || (ny_m && ny_m != vm) || (nz_m && nz_m != vm);
+        const uint32_t obase = (uint32_t)oct * (uint32_t)s.num_nodes4;
         int sp = 0, njobs = 0;
-        int node = (s.num_nodes4 > 0 && __any_sync(FULL, valid)) ? 0 : kDone;
+        int node = (s.num_nodes4 > 0 && vm) ? 0 : kDone;
         bool ovf = false;
         while (true) {
-            if (njobs >= BATCH || (node == kDone && sp == 0 && njobs)) {
+            if (njobs >= BATCH || (node == kDone && (sp == 0 || ovf) && njobs)) {
                 __syncwarp();
                 for (int jb = 0; jb < njobs; jb += 32) {
                     const int j = jb + lane;
                     if (j < njobs) {
-                        const int o = sown[wid][j];
-                        const int slot = sjob[wid][j];
+                        const uint32_t job = sjob[wid][j];
+                        const int ow = (int)(job & 31u), slot = (int)(job >> 5);
                         SRT_DCHECK(slot >= 0 && slot < s.n);
-                        const double *q = sray[wid][o];
-                        RayState ro;
-                        init_ray(ro, q[0], q[1], q[2], q[3], q[4], q[5], t_min, t_max);
+                        const double *q = sray[wid][ow];
+                        ExactRay er;
+                        er.ox = q[0], er.oy = q[1], er.oz = q[2], er.dx = q[3], er.dy = q[4], er.dz = q[5];
+                        er.inv_dd = q[6];
+                        er.fdx = (float)er.dx, er.fdy = (float)er.dy, er.fdz = (float)er.dz;
+                        er.t_min = ft_min, er.t_max0 = ft_max;
+                        ScreenRay sr;
+                        sr.fox = (float)er.ox, sr.foy = (float)er.oy, sr.foz = (float)er.oz;
+                        sr.omag = fmaxf(fabsf(sr.fox), fmaxf(fabsf(sr.foy), fabsf(sr.foz)));
+                        sr.fdx = er.fdx, sr.fdy = er.fdy, sr.fdz = er.fdz;
+                        sr.inv_dd = er.inv_dd;
+                        sr.t_min = ft_min, sr.t_max0 = ft_max;
                         const float4 *g = reinterpret_cast<const float4 *>(s.geom + slot);
-                        float4 m = __ldg(g), a = __ldg(g + 1), b = __ldg(g + 2);
-                        if (!screen<MODE>(ro, m, a, b, s2, sqrt_s2, ro.t_max0).maybe) continue;
-                        Cand cd = candidate<MODE>(ro, m, a, b, s2);
-                        if (cd.valid) {
-                            const double f = 1.0 - (double)cd.alpha;
-                            unsigned long long *p = &sprod[wid][o];
-                            unsigned long long old = *p, assumed;
-                            do {
-                                assumed = old;
-                                old = atomicCAS(p, assumed, __double_as_longlong(__longlong_as_double(assumed) * f));
-                            } while (assumed != old);
+                        const float4 gm = __ldg(g), ga = __ldg(g + 1), gb = __ldg(g + 2);
+                        if (screen<MODE>(sr, gm, ga, gb, s2, sqrt_s2, ft_max).maybe) {
+                            const Cand cd = candidate<MODE>(er, gm, ga, gb, s2);
+                            if (cd.valid) {
+                                const double f = 1.0 - (double)cd.alpha;
+                                unsigned long long *p = &sprod[wid][ow];
+                                unsigned long long old = *p, assumed;
+                                do {
+                                    assumed = old;
+                                    old = atomicCAS(p, assumed, __double_as_longlong(__longlong_as_double(assumed) * f));
+                                } while (assumed != old);
+                            }
                         }
                     }
                 }
@@ -1832,30 +1852,56 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
                 if (sp == 0 || ovf) break;
                 node = sstk[wid][--sp];
             }
-            int4 kids;
-            int key[4];
             SRT_DCHECK(node >= 0 && node < s.num_nodes4);
-            const unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), far, kids, key);
-            const unsigned anyhit = __reduce_or_sync(FULL, hitm);
+            const float4 *np = reinterpret_cast<const float4 *>(s.nodes8 + (obase + (uint32_t)node));
+            const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
+                         az = __ldg(np + 4), bz = __ldg(np + 5);
+            const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+            const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
+            const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
+            const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
+            const float paz[4] = {az.x, az.y, az.z, az.w}, pbz[4] = {bz.x, bz.y, bz.z, bz.w};
+            unsigned hitm = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float tn, tf;
+                if (!mixed) {
+                    tn = fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
+                               fmaf(paz[k], r.idz, -r.oidz));
+                    tf = fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
+                               fminf(fmaf(pbz[k], r.idz, -r.oidz), far));
+                } else {
+                    const float xa = fmaf(pax[k], r.idx, -r.oidx), xb = fmaf(pbx[k], r.idx, -r.oidx);
+                    const float ya = fmaf(pay[k], r.idy, -r.oidy), yb = fmaf(pby[k], r.idy, -r.oidy);
+                    const float za = fmaf(paz[k], r.idz, -r.oidz), zb = fmaf(pbz[k], r.idz, -r.oidz);
+                    tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fminf(za, zb));
+                    tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
+                }
+                // closed slab (kernels.py:279,308) clipped to [t_min, t_max]
+                hitm |= fmaxf(tn, r.t_min) <= tf ? (1u << k) : 0u;
+            }
+            hitm &= hint & 15u;
+            const unsigned leafm = (hint >> 4) & 15u;
+            const unsigned any = __reduce_or_sync(FULL, hitm);
+            const unsigned lh = hitm & leafm;
             node = kDone;
-            for (unsigned m = anyhit; m; m &= m - 1) {
-                const int k = __ffs(m) - 1;
-                const int code = pick(kids, k);  // warp-uniform
-                if (code < 0) {
-                    const bool h = (hitm >> k) & 1u;
-                    const unsigned bm = __ballot_sync(FULL, h);
-                    if (h) {
-                        const int o = njobs + __popc(bm & lt);
-                        SRT_DCHECK(o < BATCH + 128);
-                        sjob[wid][o] = ~code;
-                        sown[wid][o] = (unsigned char)lane;
-                    }
-                    njobs += __popc(bm);
-                } else if (node == kDone) {
+            for (unsigned al = any & leafm; al; al &= al - 1) {
+                const int k = __ffs(al) - 1;
+                const bool h = (lh >> k) & 1u;
+                const unsigned bm = __ballot_sync(FULL, h);
+                if (h) {
+                    SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
+                    sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+                }
+                njobs += __popc(bm);
+            }
+            // unclipped: every inner child any lane hits is walked, in any order
+            for (unsigned ai = any & ~leafm; ai; ai &= ai - 1) {
+                const int code = sel4(kids, __ffs(ai) - 1);
+                if (node == kDone) {
                     node = code;
                 } else if (sp < PSTACK) {
-                    if (lane == 0) sstk[wid][sp] = code;
-                    ++sp;
+                    sstk[wid][sp++] = code;  // warp-uniform: every lane stores the same word
                 } else {
                     if (lane == 0) raise_flag(overflow);
                     ovf = true;
@@ -1869,7 +1915,6 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
     }
     release_counter(work);
 }
-
 
 // Incoherent transmittance batches (rays from distinct origins in all
 // directions): per-lane walks with warp-compacted leaf work.  Each step
