@@ -383,7 +383,9 @@ static BiasedArgs biased_args(double t_min, double t_max, double s2, int mode, i
 // ---------------------------------------------------------------------------
 constexpr int kExactCap = 1024;      // list entries per ray (C3-target: mean 261, max ~720 valid candidates)
 constexpr int kExactThreads = 128;
-constexpr int kExactBlocksPerSM = 6;  // bounds the list scratch: 148 x 6 x 128 lanes x 12 KB = 1.4 GB
+// 6 blocks (80 registers) per SM bound the list scratch: 148 x 6 x 128 lanes x
+// 12 KB = 1.4 GB; 7 / 8 blocks were slower (1080p frame 52.6 -> 60.6 / 65.3 ms)
+constexpr int kExactBlocksPerSM = 6;
 constexpr int kBiasedClip = 8;        // biased walks with kk <= this clip at the kk-th accepted depth
 
 enum { kPacketExact = 0, kPacketBiasedCounter = 1, kPacketBiasedTable = 2 };
