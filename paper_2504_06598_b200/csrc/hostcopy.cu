@@ -10,7 +10,6 @@
 // chunk c through the other.  Pinned caller memory (srt_host_alloc,
 // registered) and small copies take one cudaMemcpyAsync.
 #include <algorithm>
-#include <atomic>
 #include <condition_variable>
 #include <cstring>
 #include <deque>
@@ -44,7 +43,10 @@ class CopyPool {
             return;
         }
         const size_t piece = ((n + parts - 1) / parts + 63) & ~(size_t)63;
-        std::atomic<int> left(parts - 1);
+        // completion count, guarded by dm: a worker touches dm / dcv only while
+        // holding dm, so once the caller sees zero (under dm) no worker will
+        // touch them again and they may go out of scope
+        int left = parts - 1;
         std::mutex dm;
         std::condition_variable dcv;
         {
@@ -53,17 +55,15 @@ class CopyPool {
                 const size_t off = std::min(n, piece * p), len = std::min(n - off, piece);
                 tasks_.push_back([=, &left, &dm, &dcv] {
                     std::memcpy((char *)dst + off, (const char *)src + off, len);
-                    if (left.fetch_sub(1) == 1) {
-                        std::lock_guard<std::mutex> g(dm);
-                        dcv.notify_one();
-                    }
+                    std::lock_guard<std::mutex> g(dm);
+                    if (--left == 0) dcv.notify_one();
                 });
             }
         }
         cv_.notify_all();
         std::memcpy(dst, src, std::min(n, piece));
         std::unique_lock<std::mutex> lk(dm);
-        dcv.wait(lk, [&] { return left.load() == 0; });
+        dcv.wait(lk, [&] { return left == 0; });
     }
 
   private:
