@@ -16,7 +16,7 @@
 
 namespace srt {
 
-constexpr int kPlocRadius = 16;  // neighbourhood half-width (SRT_PLOC_RADIUS overrides, experiments)
+constexpr int kPlocRadius = 16;  // neighbourhood half-width (SRT_PLOC_RADIUS overrides in the experiments build)
 
 __device__ __forceinline__ float half_area(float4 lo, float4 hi) {
     float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
@@ -113,8 +113,12 @@ srt_status ploc_build(SrtScene *s, int64_t n, const uint32_t *slot_prim, const f
     size_t temp_bytes = 0;
     int nc = (int)n;
     const int B = 256;
-    const char *env = getenv("SRT_PLOC_RADIUS");
+#ifdef SRT_EXPERIMENTS
+    const char *env = getenv("SRT_PLOC_RADIUS");  // radius sweeps (tools/tree_probe.py), experiments build only
     const int radius = env ? max(1, atoi(env)) : kPlocRadius;
+#else
+    const int radius = kPlocRadius;
+#endif
     rc = cuda_status(cudaMalloc(&code, sizeof(int) * n), "ploc alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&code2, sizeof(int) * n), "ploc alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&nn, sizeof(int) * n), "ploc alloc");

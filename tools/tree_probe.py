@@ -1,7 +1,9 @@
 """Tree-quality probe: front-camera C3-target frame time and a view-independent
 probe (14 views -- 6 axis + 8 diagonal cameras around the scene, 480x270,
-1 spp) for the current build (SRT_PLOC_RADIUS selects the PLOC radius):
-    SRT_PLOC_RADIUS=r python tools/tree_probe.py seed"""
+1 spp) for the current build (SRT_PLOC_RADIUS selects the PLOC radius in
+the experiments build):
+    make -C paper_2504_06598_b200/csrc experiments
+    SRT_LIBSRT_PATH=paper_2504_06598_b200/libsrt_exp.so SRT_PLOC_RADIUS=r python tools/tree_probe.py seed"""
 import os
 import statistics
 import sys
