@@ -153,7 +153,6 @@ struct Walk {
     int next;  // next inner node, or kDone
     int sp;
     float far;
-    uint32_t obase;  // the ray's direction-octant copy of the tree (SceneView::nodes8), node index base
     int stk_code[kStackSize];
     float stk_t[kStackSize];
 
@@ -212,35 +211,10 @@ __device__ __forceinline__ int visit_node(const SceneView &s, const RayState &r,
     int4 kids;
     int key[4];
     SRT_DCHECK(node >= 0 && node < s.num_nodes4);
-#ifdef SRT_LANE_OCT
-    // the ray's octant copy of the node: near planes first, so 6 FMAs and two
-    // 3-way min/max per child; valid / leaf masks from the node's hint word
-    const float4 *np = reinterpret_cast<const float4 *>(s.nodes8 + (wk.obase + (uint32_t)node));
-    const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3), az = __ldg(np + 4),
-                 bz = __ldg(np + 5);
-    kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
-    const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
-    const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
-    const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
-    const float paz[4] = {az.x, az.y, az.z, az.w}, pbz[4] = {bz.x, bz.y, bz.z, bz.w};
-    unsigned hitm = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float tn = fmaxf(fmaxf(fmaf(pax[k], r.idx, -r.oidx), fmaf(pay[k], r.idy, -r.oidy)),
-                               fmaxf(fmaf(paz[k], r.idz, -r.oidz), r.t_min));
-        const float tf = fminf(fminf(fmaf(pbx[k], r.idx, -r.oidx), fmaf(pby[k], r.idy, -r.oidy)),
-                               fminf(fmaf(pbz[k], r.idz, -r.oidz), wk.far));
-        hitm |= tn <= tf ? (1u << k) : 0u;
-        key[k] = ordered_key(tn, k);
-    }
-    hitm &= hint & 15u;
-    const unsigned leafm = (hint >> 4) & 15u;
-#else
     unsigned hitm = slab4(r, reinterpret_cast<const float4 *>(s.nodes4 + node), wk.far, kids, key);
     unsigned leafm = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) leafm |= pick(kids, k) < 0 ? (1u << k) : 0u;
-#endif
     unsigned lm = hitm & leafm;
     while (lm) {
         int k = __ffs(lm) - 1;
@@ -529,8 +503,6 @@ __global__ void __launch_bounds__(kTraceThreads) k_trace(SceneView s, Src src, W
                     wk.sp = 0;
                     wk.far = r.t_max0;
                     wk.next = s.num_nodes4 > 0 ? 0 : kDone;
-                    wk.obase = (uint32_t)((signbit(r.idx) ? 1 : 0) | (signbit(r.idy) ? 2 : 0) | (signbit(r.idz) ? 4 : 0)) *
-                               (uint32_t)s.num_nodes4;
                 }
             }
         } else if (exhausted && idle == FULL) {
