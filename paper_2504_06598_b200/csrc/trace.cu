@@ -193,7 +193,9 @@ __device__ __forceinline__ unsigned slab4(const RayState &r, const float4 *np, f
         float tn = fmaxf(fmaxf(fminf(xa, xb), fminf(ya, yb)), fmaxf(fminf(za, zb), r.t_min));
         float tf = fminf(fminf(fmaxf(xa, xb), fmaxf(ya, yb)), fminf(fmaxf(za, zb), far));
         // empty slots carry inverted boxes, which min/max slab tests would see
-        // as infinite: mask them by code
+        // as infinite: mask them by code (deriving the masks from the already
+        // loaded codes beats loading the node's hint word here: 161 vs 156
+        // Mrays/s on random rays)
         bool hit = tn <= tf && pick(kids, k) != kLeafEmpty;
         key[k] = NONNEG ? ((__float_as_int(tn) & ~3) | k) : ordered_key(tn, k);
         hitm |= hit ? (1u << k) : 0u;
@@ -977,10 +979,18 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
         auto run_jobs = [&]() {
             sdir[wid][lane] = make_float4(r.fdx, r.fdy, r.fdz, far);
             __syncwarp();
-            for (int jb = 0; jb < njobs; jb += 32) {
+            // N <= 2: mid-walk flushes run whole rounds of 32 jobs only; the
+            // rest stay queued (moved to the front) for the next flush or the
+            // walk's end (rounds 84% -> ~100% full; N=1 seed mean 1.678 ->
+            // 1.648 ms at 32-job batches, N=2 +1.7%; N=4 / N=8 lose 1.4 / 1.7%:
+            // their clip waits on more slots, so they flush everything)
+            constexpr bool kFullRounds = NS <= 2;
+            const bool walk_end = node == kDone && sp == 0;
+            const int nrun = (walk_end || !kFullRounds) ? njobs : (njobs & ~31);
+            for (int jb = 0; jb < nrun; jb += 32) {
                 if (lane == 0) ct.add(13, 1);
                 int j = jb + lane;
-                if (j < njobs) {
+                if (j < nrun) {
                     const uint32_t job = sjob[wid][j];
                     const int o = (int)(job & 31u), slot = (int)(job >> 5);
                     float4 dv = sdir[wid][o];
@@ -1005,7 +1015,14 @@ __global__ void __launch_bounds__(kTraceThreads, MINB) k_trace_packet(SceneView 
                 }
             }
             __syncwarp();
-            njobs = 0;
+            {
+                const int left = njobs - nrun;  // < 32
+                const uint32_t v = lane < left ? sjob[wid][nrun + lane] : 0u;
+                __syncwarp();
+                if (lane < left) sjob[wid][lane] = v;
+                __syncwarp();
+                njobs = left;
+            }
             if (valid && w.clip) {
                 // clip to the farthest slot once every slot holds a hit (kernels.py:358-364)
                 float worst = unpack_t(sbest[wid][lane][0]);
@@ -1318,13 +1335,14 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
 #define SRT_N1_MINB 8
 #endif
 #ifndef SRT_N1_BATCH
-#define SRT_N1_BATCH 48
+#define SRT_N1_BATCH 32
 #endif
     constexpr int kMinB = NS == 1 ? SRT_N1_MINB
                           : ((NS == 2 && MODE == 0) ? 8
                              : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5)));
-    // leaf jobs per batch: 48 for N=1 (1.964 vs 1.976 ms at 32) and N=4
-    // (2.957 vs 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
+    // leaf jobs per flush threshold (flushes run whole 32-job rounds): 32 for
+    // N=1 (round 2: 1.648 vs 1.662 ms at 48), 48 for N=4 (round 1: 2.957 vs
+    // 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
     constexpr int kBatch = NS == 1 ? SRT_N1_BATCH : ((NS == 4 && MODE == 0) ? 48 : 32);
     return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB>(s, src, w, st);
 }
