@@ -345,11 +345,12 @@ def test_c5_scale_6m_vs_oracle(oracle):
     _check_colours(rgb[sub], ref["rgb"][sub], np.all(agree, axis=2))
 
 
-@pytest.mark.parametrize("passes,nslots", [(1, 1), (3, 2)])
-def test_mapped_host_output_equals_copy_path(passes, nslots):
+@pytest.mark.parametrize("passes,nslots,W,H", [(1, 1, 72, 40), (3, 2, 72, 40), (1, 1, 37, 23), (1, 2, 70, 41)])
+def test_mapped_host_output_equals_copy_path(passes, nslots, W, H):
     """srt_render into mapped page-locked outputs (the last fused pass stores
-    the f64 frame over PCIe) equals the resolve-and-copy path into pageable
-    memory, bit for bit."""
+    the f64 frame over PCIe: whole 8x4 packets as staged 16-byte rows, partial
+    or unaligned ones -- odd widths, edge blocks -- per lane) equals the
+    resolve-and-copy path into pageable memory, bit for bit."""
     from paper_2504_06598_b200 import front_camera
     from paper_2504_06598_b200.render import PinnedPool
     from paper_2504_06598_b200.scene import DeviceScene, camera_tuple
@@ -358,7 +359,6 @@ def test_mapped_host_output_equals_copy_path(passes, nslots):
     a = random_cloud(5_000, seed=12, sh_degree=2)
     sc = DeviceScene.from_packed(a.packed)
     sc.build_bvh(np.sqrt(S2))
-    W, H = 72, 40
     cam = camera_tuple(front_camera(), W, H)
     pool = PinnedPool()
     prgb, pop = pool.array((H, W, 3)), pool.array((H, W))
