@@ -5,8 +5,10 @@
     compute-sanitizer --tool synccheck python tools/sanitize_workload.py
 
 Builds (PLOC, LBVH, upload), splat packing, fused and split frames (mapped
-and pageable outputs, N = 1/2/4, both depth modes), explicit rays (counter,
-table, trig64), transmittance, exact and biased composites.
+and pageable outputs, N = 1/2/4, both depth modes, odd widths), explicit rays
+(counter, table, trig64; per lane and as packets), transmittance, exact and
+biased composites (per lane and as packets), host arrays through the staging
+ring.
 """
 import sys
 
@@ -51,7 +53,31 @@ def main() -> None:
             sc.biased_rays(o, d, 3, s2=S2, rng=rng_name)
             sc.render_biased(cam, W, H, 2, 2, 0, S2, rng=rng_name)
         sc.biased_rays(o, d, 2, s2=S2, rng="table", table=np.zeros(2_000))
+        # one-hemisphere batches of >= 4096 rays: the packet routes (trace,
+        # transmittance, exact and biased composites; distinct origins sorted)
+        hd = rng.normal(size=(5000, 3)) * [0.2, 0.2, 0.0] + [0.0, 0.0, 1.0]
+        hd /= np.linalg.norm(hd, axis=1, keepdims=True)
+        ho = rng.uniform(-1, 1, (5000, 3)) * [1, 1, 0] + [0, 0, -4]
+        sc.trace_rays(ho, hd, 0.0, TMAX, 0, S2, True, 1)
+        sc.transmittance(ho, hd, 0.0, TMAX, 0, S2)
+        sc.exact_rays(ho, hd, s2=S2)
+        for kk in (1, 4, 12):
+            sc.biased_rays(ho, hd, kk, s2=S2)
+        sc.biased_rays(ho, hd, 3, s2=S2, rng="table", table=rng.uniform(size=2_000))
+        sc.render_biased(cam, W, H, 12, 2, 0, S2)
+        # odd width: partial packets store the f64 frame per lane
+        cam_odd = camera_tuple(front_camera(), 37, 23)
+        sc.render(cam_odd, 37, 23, 1, 1, 0, S2, True, 1, (0.1, 0.2, 0.3), out_rgb=pool.array((23, 37, 3)),
+                  out_op=pool.array((23, 37)))
         sc.close()
+    # host arrays above 2 MB: the page-locked staging ring
+    big = DeviceScene.from_packed(a.packed)
+    big.build_bvh(np.sqrt(S2))
+    bo = np.random.default_rng(2).uniform(-3, 3, (120_000, 3))
+    bd = np.random.default_rng(3).normal(size=(120_000, 3))
+    bd /= np.linalg.norm(bd, axis=1, keepdims=True)
+    big.trace_rays(bo, bd, 0.0, TMAX, 0, S2, True, 1)
+    big.close()
     # raw splats packed on the GPU, and a scene from the reference's own BVH layout
     sp = DeviceScene.from_splats(a)
     sp.build_bvh(np.sqrt(S2))
