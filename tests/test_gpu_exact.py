@@ -300,3 +300,28 @@ def test_biased_rays_packets_vs_oracle(oracle, rng, kk):
     want = oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, 3, o, d, kk, s2=S2,
                                background=(0.1, 0.3, 0.2), rng=rng, **kw)
     assert _close_fraction(rgb, want) >= 0.995
+
+
+def test_biased_frame_long_accepted_lists_fall_back(oracle):
+    """k = 12 walks unclipped and keeps every accepted candidate in the ray's
+    list: through 1,100 near-opaque layers a list overflows its 1,024
+    entries and the ray composites through the per-lane peeling path --
+    same result as the oracle's brute-force biased composite."""
+    from paper_2504_06598_b200 import RenderSettings, front_camera, generate_camera_ray, render_biased
+    from paper_2504_06598_b200.synthetic import pancake_stack
+
+    layers = 1100
+    rs = np.random.default_rng(17)
+    alphas = rs.uniform(0.97, 0.99, layers)
+    colors = rs.uniform(0.0, 1.0, (layers, 3))
+    a = pancake_stack(alphas, colors, z0=1.0, spacing=0.004, thickness=0.0005)
+    pk = a.packed
+    cam = front_camera()
+    st = RenderSettings(width=16, height=8, spp=1, seed=3, background=[0.2, 0.3, 0.4])
+    frame = render_biased(a, cam, st, 12)
+    rays = [generate_camera_ray(cam, st, (x, y), 0) for y in range(8) for x in range(16)]
+    o = np.array([r[0] for r in rays])
+    d = np.array([r[1] for r in rays])
+    want = oracle.biased_batch(pk.means, pk.cov_inv6, pk.opacities, pk.sh, pk.sh_degree, o, d, 12, s2=S2,
+                               background=(0.2, 0.3, 0.4), rng="counter", seed=3, ray_id0=0, sample0=0)
+    np.testing.assert_allclose(frame.reshape(-1, 3), want, rtol=1e-4, atol=1e-6)
