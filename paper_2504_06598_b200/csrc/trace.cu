@@ -153,8 +153,7 @@ struct Walk {
     int next;  // next inner node, or kDone
     int sp;
     float far;
-    int stk_code[kStackSize];
-    float stk_t[kStackSize];
+    int2 stk[kStackSize];  // (code, entry distance bits): one 64-bit local-memory word per entry
 
     float popped_t;  // entry distance of the last popped node
 
@@ -163,9 +162,10 @@ struct Walk {
         while (sp > 0) {
             --sp;
             ct.add(5, 1);
-            if (stk_t[sp] <= far) {  // cull beyond the (clipped) far bound
-                popped_t = stk_t[sp];
-                return stk_code[sp];
+            const int2 e = stk[sp];
+            if (__int_as_float(e.y) <= far) {  // cull beyond the (clipped) far bound
+                popped_t = __int_as_float(e.y);
+                return e.x;
             }
             ct.add(6, 1);
         }
@@ -250,8 +250,7 @@ __device__ __forceinline__ int visit_node(const SceneView &s, const RayState &r,
             if (j < ni) {
                 float te = key_t(key[j]);
                 if (te <= wk.far) {
-                    wk.stk_code[wk.sp] = pick(kids, key[j] & 3);
-                    wk.stk_t[wk.sp] = te;
+                    wk.stk[wk.sp] = make_int2(pick(kids, key[j] & 3), __float_as_int(te));
                     ++wk.sp;
                 }
             }
@@ -690,8 +689,7 @@ __device__ __forceinline__ int descend(Walk &wk, const int4 &kids, int key[4], u
 #pragma unroll
         for (int j = 3; j >= 1; --j) {
             if (j < ni) {
-                wk.stk_code[wk.sp] = pick(kids, key[j] & 3);
-                wk.stk_t[wk.sp] = key_t(key[j]);
+                wk.stk[wk.sp] = make_int2(pick(kids, key[j] & 3), __float_as_int(key_t(key[j])));
                 ++wk.sp;
             }
         }
