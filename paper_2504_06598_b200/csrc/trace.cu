@@ -1335,13 +1335,25 @@ static srt_status launch_trace_packet(const SrtScene *s, const Src &src, const W
 #ifndef SRT_N1_BATCH
 #define SRT_N1_BATCH 32
 #endif
+    // N=4 at 8 blocks/SM and N=8 at 7 (end of round 2: 2.647 -> 2.612 ms and
+    // 4.149 -> 3.975 ms for the 1080p frame; 8 blocks for N=8 and 32-job
+    // batches for N=4 measured no better)
+#ifndef SRT_N4_MINB
+#define SRT_N4_MINB 8
+#endif
+#ifndef SRT_N4_BATCH
+#define SRT_N4_BATCH 48
+#endif
+#ifndef SRT_N8_MINB
+#define SRT_N8_MINB 7
+#endif
     constexpr int kMinB = NS == 1 ? SRT_N1_MINB
                           : ((NS == 2 && MODE == 0) ? 8
-                             : ((NS == 2 || (NS == 4 && MODE == 0)) ? 7 : (NS <= 8 ? 6 : 5)));
+                             : (NS == 2 ? 7 : ((NS == 4 && MODE == 0) ? SRT_N4_MINB : (NS <= 8 ? SRT_N8_MINB : 5))));
     // leaf jobs per flush threshold (flushes run whole 32-job rounds): 32 for
     // N=1 (round 2: 1.648 vs 1.662 ms at 48), 48 for N=4 (round 1: 2.957 vs
     // 2.993 ms); N=2 at 8 blocks/SM: 2.376 vs 2.419 ms
-    constexpr int kBatch = NS == 1 ? SRT_N1_BATCH : ((NS == 4 && MODE == 0) ? 48 : 32);
+    constexpr int kBatch = NS == 1 ? SRT_N1_BATCH : ((NS == 4 && MODE == 0) ? SRT_N4_BATCH : 32);
     return launch_trace_packet_v<NS, MODE, RNG, Src, STATS, kBatch, kMinB>(s, src, w, st);
 }
 
