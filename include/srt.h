@@ -185,7 +185,10 @@ srt_status srt_transmittance_rays(const SrtScene *scene, const double *origins,
 /* ---- exact compositing (kernels.exact_batch / render_exact) -------------- */
 /* Every valid candidate along the ray, sorted by (t, prim id), composited
  * front to back over `background` (kernels.py:441-475, 584-604).  out_rgb
- * (R,3) f64, out_op (R,) f64. */
+ * (R,3) f64, out_op (R,) f64.  Any number of candidates per ray (packets keep
+ * up to 1,024 per ray in a list; longer ones, and incoherent batches, peel
+ * them 256 at a time).  Host arrays may be pageable (staged through the
+ * scene's page-locked ring) or page-locked. */
 srt_status srt_exact_rays(const SrtScene *scene, const double *origins, const double *dirs,
                           int64_t num_rays, double t_min, double t_max, int32_t mode, double s2,
                           const double *background, double *out_rgb, double *out_op);
@@ -201,8 +204,10 @@ srt_status srt_render_exact(const SrtScene *scene, const SrtCamera *camera,
  * SRT_RNG_TRIG64); the kk nearest accepted candidates, sorted by (t, prim id),
  * are composited front to back with their own alphas over `background`
  * (kernels.py:479-518, 561-580).  kk >= 1; params->nslots/clip are ignored.
- * out_rgb (R,3) f64.  Any kk and any number of accepted candidates (peeled
- * 128 at a time). */
+ * out_rgb (R,3) f64.  Any kk and any number of accepted candidates
+ * (one-hemisphere batches of >= 4096 rays with counter / table draws walk as
+ * packets keeping the kk nearest per ray; the rest, and rays with more than
+ * 1,024 accepted, peel them 128 at a time). */
 srt_status srt_biased_rays(const SrtScene *scene, const SrtTraceParams *params, const double *origins,
                            const double *dirs, int64_t num_rays, int32_t kk, const double *background,
                            double *out_rgb);
