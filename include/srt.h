@@ -155,6 +155,11 @@ srt_status srt_bvh_upload(SrtScene *scene, int64_t num_nodes, const double *node
 /* Introspection: node count, tree depth, primitive count, device bytes. */
 srt_status srt_bvh_info(const SrtScene *scene, int64_t *num_nodes, int32_t *depth,
                         int64_t *num_prims, int64_t *device_bytes);
+/* The packet walk's spatially split tree (PLOC builds of >= 16,384
+ * primitives): leaf references (>= num_prims when built, 0 when the packet
+ * walk uses the unsplit tree), its 4-wide node count and grid cells per axis. */
+srt_status srt_bvh_split_info(const SrtScene *scene, int64_t *num_refs, int32_t *num_nodes4,
+                              int32_t *cells);
 /* Copy the built BVH back in the reference layout (for invariant tests).
  * Arrays sized by srt_bvh_info: nodes M = 2n-1 (or 0), prims n. */
 srt_status srt_bvh_download(const SrtScene *scene, float *node_lo, float *node_hi,

@@ -81,6 +81,7 @@ SYMBOLS = [
     ("srt_bvh_build", _i32, [_vp, _f64]),
     ("srt_bvh_build_ex", _i32, [_vp, _f64, _i32]),
     ("srt_bvh_upload", _i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("srt_bvh_split_info", _i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     ("srt_bvh_info", _i32, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i64),
                             ctypes.POINTER(_i64)]),
     ("srt_bvh_download", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

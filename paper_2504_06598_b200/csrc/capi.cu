@@ -344,6 +344,7 @@ srt_status srt_scene_destroy(SrtScene *s) {
     cudaFree(s->d_nodes);
     cudaFree(s->d_nodes4);
     cudaFree(s->d_nodes8);
+    free_split(s);
     cudaFree(s->d_stats);
     if (s->h_flag) cudaFreeHost(s->h_flag);
     cudaFree(s->d_counter);
@@ -477,6 +478,7 @@ srt_status srt_bvh_upload(SrtScene *s, int64_t M, const double *node_lo, const d
         return SRT_ERR_INVALID_ARG;
     }
     // slot-ordered geometry from prim_order
+    free_split(s);
     if (s->d_nodes) cudaFree(s->d_nodes);
     if (s->d_geom) cudaFree(s->d_geom);
     s->d_nodes = nullptr;
@@ -545,7 +547,19 @@ srt_status srt_bvh_info(const SrtScene *s, int64_t *num_nodes, int32_t *depth, i
     if (num_prims) *num_prims = s->n;
     if (device_bytes)
         *device_bytes = (int64_t)sizeof(Node2) * s->num_nodes + (int64_t)sizeof(Node4) * 9 * s->num_nodes4 +
-                        (int64_t)sizeof(Geom) * s->n + (int64_t)sizeof(float) * s->n * 3 * s->sh_k;
+                        (int64_t)sizeof(Geom) * s->n + (int64_t)sizeof(float) * s->n * 3 * s->sh_k +
+                        (int64_t)sizeof(Node4) * 9 * s->num_nodes4_split + (int64_t)sizeof(Geom) * s->n_refs;
+    return SRT_OK;
+}
+
+srt_status srt_bvh_split_info(const SrtScene *s, int64_t *num_refs, int32_t *num_nodes4, int32_t *cells) {
+    if (!s) {
+        set_error("null scene");
+        return SRT_ERR_INVALID_ARG;
+    }
+    if (num_refs) *num_refs = s->n_refs;
+    if (num_nodes4) *num_nodes4 = s->num_nodes4_split;
+    if (cells) *cells = s->split_cells;
     return SRT_OK;
 }
 

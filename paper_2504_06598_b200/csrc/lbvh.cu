@@ -251,6 +251,12 @@ __global__ void k_single(const float *plo, const float *phi, Node2 *nodes) {
     nodes[0] = nd;
 }
 
+srt_status launch_geom(int64_t n, const uint32_t *slot_prim, const SrtScene *s, Geom *out, cudaStream_t st) {
+    if (n <= 0) return SRT_OK;
+    k_geom<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, slot_prim, s->d_means, s->d_cov6, s->d_opac, out);
+    return cuda_status(cudaGetLastError(), "k_geom");
+}
+
 template <typename T>
 static srt_status dalloc(T **p, size_t count, const char *what) {
     cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (count ? count : 1));
@@ -264,6 +270,7 @@ static srt_status dalloc(T **p, size_t count, const char *what) {
 srt_status lbvh_build(SrtScene *s, double cutoff_s, int method) {
     const int64_t n = s->n;
     cudaStream_t st = s->stream;
+    free_split(s);
     if (s->d_nodes) cudaFree(s->d_nodes);
     if (s->d_geom) cudaFree(s->d_geom);
     s->d_nodes = nullptr;
@@ -339,7 +346,7 @@ srt_status lbvh_build(SrtScene *s, double cutoff_s, int method) {
         SRT_TRY(cuda_status(cudaMemsetAsync(ddepth, 0, sizeof(int), st), "depth"));
         SRT_TRY(cuda_status(cudaMemsetAsync(parent_int, 0xFF, sizeof(int) * m, st), "parents"));
         if (method == SRT_BVH_PLOC) {
-            SRT_TRY(ploc_build(s, n, vals2, plo, phi, parent_int, parent_leaf, st));
+            SRT_TRY(ploc_build(s, n, vals2, plo, phi, parent_int, parent_leaf, st, s->d_nodes));
         } else {
             k_karras<<<(unsigned)((m + B - 1) / B), B, 0, st>>>(n, keys2, children, parent_int, parent_leaf);
             SRT_TRY(cuda_status(cudaGetLastError(), "k_karras"));
@@ -355,6 +362,9 @@ srt_status lbvh_build(SrtScene *s, double cutoff_s, int method) {
     }
     SRT_TRY(cuda_status(cudaStreamSynchronize(st), "lbvh build"));
     SRT_TRY(collapse4(s));
+    // the packet walk's spatially split copy (PLOC builds of large scenes)
+    free_split(s);
+    if (method == SRT_BVH_PLOC) SRT_TRY(split_build(s, plo, phi, cb, st));
     s->has_bvh = true;
 done:
 #undef SRT_TRY
@@ -664,24 +674,28 @@ __global__ void k_octant_nodes(const Node4 *__restrict__ n4, int m, Node4 *out) 
 
 static srt_status collapse4_tree(SrtScene *s);
 
-srt_status collapse4(SrtScene *s) {
-    srt_status rc = collapse4_tree(s);
-    if (rc) return rc;
-    if (s->d_nodes8) cudaFree(s->d_nodes8);
-    s->d_nodes8 = nullptr;
-    const int m = s->num_nodes4;
+srt_status octant_copies(const Node4 *n4, int32_t m, Node4 **out8, cudaStream_t st) {
+    *out8 = nullptr;
     if (m == 0) return SRT_OK;
     if ((uint64_t)m * 8 >= (1ull << 32)) {  // packet kernels index the octant copies with 32 bits
         set_error("BVH too large for the octant node copies");
         return SRT_ERR_INVALID_ARG;
     }
-    rc = cuda_status(cudaMalloc(&s->d_nodes8, sizeof(Node4) * 8 * (size_t)m), "octant node alloc");
+    srt_status rc = cuda_status(cudaMalloc(out8, sizeof(Node4) * 8 * (size_t)m), "octant node alloc");
     if (rc) return rc;
     const int64_t total = (int64_t)m * 8;
-    k_octant_nodes<<<(unsigned)((total + 255) / 256), 256, 0, s->stream>>>(s->d_nodes4, m, s->d_nodes8);
+    k_octant_nodes<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n4, m, *out8);
     rc = cuda_status(cudaGetLastError(), "k_octant_nodes");
-    if (!rc) rc = cuda_status(cudaStreamSynchronize(s->stream), "octant nodes");
+    if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "octant nodes");
     return rc;
+}
+
+srt_status collapse4(SrtScene *s) {
+    srt_status rc = collapse4_tree(s);
+    if (rc) return rc;
+    if (s->d_nodes8) cudaFree(s->d_nodes8);
+    s->d_nodes8 = nullptr;
+    return octant_copies(s->d_nodes4, s->num_nodes4, &s->d_nodes8, s->stream);
 }
 
 static srt_status collapse4_tree(SrtScene *s) {
@@ -697,12 +711,16 @@ static srt_status collapse4_tree(SrtScene *s) {
         }
     }
 #endif
-    cudaStream_t st = s->stream;
     if (s->d_nodes4) cudaFree(s->d_nodes4);
     s->d_nodes4 = nullptr;
     s->num_nodes4 = 0;
-    if (s->num_nodes == 0) return SRT_OK;
-    const int m2 = s->num_nodes;
+    return collapse_tree(s->d_nodes, s->num_nodes, &s->d_nodes4, &s->num_nodes4, s->stream);
+}
+
+srt_status collapse_tree(const Node2 *n2, int32_t m2, Node4 **out4, int32_t *m4, cudaStream_t st) {
+    *out4 = nullptr;
+    *m4 = 0;
+    if (m2 == 0) return SRT_OK;
     srt_status rc = SRT_OK;
     int2 *wa = nullptr, *wb = nullptr;
     int *counters = nullptr;  // [0] n4 count, [1] work_out count
@@ -710,7 +728,7 @@ static srt_status collapse4_tree(SrtScene *s) {
     int n_in = 1;
     int2 root = make_int2(0, 0);
     // a 4-wide tree over m2 binary inner nodes has at most m2 nodes
-    rc = cuda_status(cudaMalloc(&s->d_nodes4, sizeof(Node4) * m2), "node4 alloc");
+    rc = cuda_status(cudaMalloc(out4, sizeof(Node4) * m2), "node4 alloc");
     if (!rc) rc = cuda_status(cudaMalloc(&wa, sizeof(int2) * m2), "worklist");
     if (!rc) rc = cuda_status(cudaMalloc(&wb, sizeof(int2) * m2), "worklist");
     if (!rc) rc = cuda_status(cudaMalloc(&counters, sizeof(int) * 2), "counters");
@@ -719,8 +737,7 @@ static srt_status collapse4_tree(SrtScene *s) {
     while (!rc && n_in > 0) {
         rc = cuda_status(cudaMemsetAsync(counters + 1, 0, sizeof(int), st), "counter reset");
         if (rc) break;
-        k_collapse4<<<(n_in + 127) / 128, 128, 0, st>>>(s->d_nodes, wa, n_in, wb, counters + 1, counters,
-                                                       s->d_nodes4);
+        k_collapse4<<<(n_in + 127) / 128, 128, 0, st>>>(n2, wa, n_in, wb, counters + 1, counters, *out4);
         rc = cuda_status(cudaGetLastError(), "k_collapse4");
         if (!rc) rc = cuda_status(cudaMemcpyAsync(h, counters, sizeof(h), cudaMemcpyDeviceToHost, st), "counters");
         if (!rc) rc = cuda_status(cudaStreamSynchronize(st), "collapse");
@@ -729,7 +746,7 @@ static srt_status collapse4_tree(SrtScene *s) {
         wa = wb;
         wb = t;
     }
-    if (!rc) s->num_nodes4 = h[0];
+    if (!rc) *m4 = h[0];
     cudaFree(wa);
     cudaFree(wb);
     cudaFree(counters);

@@ -27,6 +27,17 @@ struct SrtScene {
     srt::Node4 *d_nodes4 = nullptr; // (num_nodes4,) 4-wide tree traced by the kernels
     srt::Node4 *d_nodes8 = nullptr; // (8, num_nodes4) the same tree per direction octant (packet kernel)
     int32_t num_nodes4 = 0;
+    // Spatially split copy of the tree for the closest-hit walks (split.cu):
+    // leaf references to primitives clipped at the planes of a uniform cell
+    // grid, so the top of the tree has no overlap.  Only the 4-wide tree, its
+    // octant copies and the reference-ordered records are kept.  Null: the
+    // walks use the tree above (small scenes, uploaded reference BVHs).
+    srt::Geom *d_geom_split = nullptr;    // (n_refs,) reference (slot) order
+    srt::Node4 *d_nodes4_split = nullptr; // (num_nodes4_split,)
+    srt::Node4 *d_nodes8_split = nullptr; // (8, num_nodes4_split)
+    int32_t num_nodes4_split = 0;
+    int64_t n_refs = 0;
+    int32_t split_cells = 0;  // cells per axis of the split grid (0: no split tree)
     unsigned long long *d_stats = nullptr;  // traversal counters (srt_trace_stats)
     int32_t depth = 0;
     bool has_bvh = false;
@@ -65,6 +76,23 @@ struct SrtScene {
         v.n = n;
         return v;
     }
+    // The view the closest-hit walks (k_trace_packet, k_trace, k_trace_coop)
+    // traverse: the split tree when one exists.  Leaf codes index
+    // d_geom_split; duplicate references of a primitive give the same (t, id)
+    // key and draw, so the order-free closest-accepted slots are unchanged
+    // (split.cu).  Compositing walks keep view().
+    srt::SceneView walk_view() const {
+        srt::SceneView v = view();
+        if (d_nodes8_split) {
+            v.nodes = nullptr;
+            v.nodes4 = d_nodes4_split;
+            v.nodes8 = d_nodes8_split;
+            v.num_nodes4 = num_nodes4_split;
+            v.geom = d_geom_split;
+            v.n = n_refs;
+        }
+        return v;
+    }
 };
 
 namespace srt {
@@ -93,8 +121,16 @@ float box_hi_f32(double x);
 // build / launch helpers (lbvh.cu, trace.cu, shade.cu)
 srt_status lbvh_build(SrtScene *s, double cutoff_s, int method);
 srt_status ploc_build(SrtScene *s, int64_t n, const uint32_t *slot_prim, const float *plo, const float *phi,
-                      int *parent_int, int *parent_leaf, cudaStream_t st);
+                      int *parent_int, int *parent_leaf, cudaStream_t st, Node2 *nodes,
+                      const int *cell = nullptr);
 srt_status collapse4(SrtScene *s);
+// binary tree (m2 Node2, root 0) -> greedy 4-wide tree and its octant copies
+srt_status collapse_tree(const Node2 *n2, int32_t m2, Node4 **out4, int32_t *m4, cudaStream_t st);
+srt_status octant_copies(const Node4 *n4, int32_t m, Node4 **out8, cudaStream_t st);
+srt_status launch_geom(int64_t n, const uint32_t *slot_prim, const SrtScene *s, Geom *out, cudaStream_t st);
+// the packet walk's split tree (split.cu); free_split drops it
+srt_status split_build(SrtScene *s, const float *plo, const float *phi, const int *cbounds, cudaStream_t st);
+void free_split(SrtScene *s);
 srt_status scratch_reserve(SrtScene *s, size_t bytes);
 srt_status launch_pack_splats(int64_t n, const double *d_q, const double *d_scales, double *d_cov6, cudaStream_t st);
 

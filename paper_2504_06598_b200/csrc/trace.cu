@@ -1247,7 +1247,7 @@ static srt_status launch_trace_v(const SrtScene *s, const Src &src, const WalkCf
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace<NS, MODE, RNG, Src, REFILL, STATS>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->walk_view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace launch");
 }
 
@@ -1271,7 +1271,7 @@ static srt_status launch_trace_coop(const SrtScene *s, const Src &src, const Wal
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_coop<NS, MODE, RNG, Src, STATS, REFILL>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->walk_view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_coop launch");
 }
 
@@ -1301,7 +1301,7 @@ static srt_status launch_trace_packet_v(const SrtScene *s, const Src &src, const
     int64_t grid = (int64_t)g_num_sms * blocks_per_sm;
     if (grid > need) grid = need;
     k_trace_packet<NS, MODE, RNG, Src, STATS, BATCH, MINB>
-        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->view(), src, w, work.p, s->d_flag, s->d_stats);
+        <<<(unsigned)grid, kTraceThreads, 0, st>>>(s->walk_view(), src, w, work.p, s->d_flag, s->d_stats);
     return cuda_status(cudaGetLastError(), "k_trace_packet launch");
 }
 

@@ -193,6 +193,13 @@ class DeviceScene:
                                        ctypes.byref(nb)))
         return {"num_nodes": nn.value, "depth": d.value, "num_prims": npr.value, "device_bytes": nb.value}
 
+    def split_info(self) -> dict:
+        """The packet walk's spatially split tree (srt_bvh_split_info): leaf
+        references, 4-wide nodes, grid cells per axis (all 0 without one)."""
+        nr, n4, c = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        check(_lib.load().srt_bvh_split_info(self.handle, ctypes.byref(nr), ctypes.byref(n4), ctypes.byref(c)))
+        return {"num_refs": nr.value, "num_nodes4": n4.value, "cells": c.value}
+
     def download_bvh(self) -> dict:
         """Device BVH in the reference layout: inner nodes 0..M-1, then one
         single-primitive leaf node per slot (fp32 boxes)."""

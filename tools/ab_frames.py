@@ -35,6 +35,8 @@ lib = os.environ.get("SRT_LIBSRT_PATH", "libsrt.so").split("/")[-1]
 means = []
 for seed in seeds:
     sc = prepare(density_cloud(n, seed=seed), st)
+    if hasattr(sc, "split_info"):
+        print(f"seed {seed}: split tree {sc.split_info()}", flush=True)
     for _ in range(3):
         sc.render_pass_device(cam, prm, 0, acc.data_ptr(), True, True, out.data_ptr(), s)
     if os.environ.get("SRT_TRACE_STATS") == "1":
