@@ -30,9 +30,13 @@
 // 64-bit (t, id) atomicMin of each slot is idempotent, so the closest accepted
 // hit per slot is exactly the unsplit tree's (the per-lane walks' slot update
 // is idempotent too: strict t, ties to the smaller id).  Only the closest-hit
-// walks (k_trace_packet, k_trace, k_trace_coop) use this tree; compositing
-// walks (transmittance, exact, biased) sum over candidates and keep the
-// unsplit tree.
+// walks (k_trace_packet, k_trace, k_trace_coop and the trig64 bridge walks)
+// use this tree.  The compositing walks (transmittance, exact, biased) keep
+// the unsplit tree: they walk every candidate along the ray, so duplicated
+// references only add work -- measured with an ownership rule that counts
+// each candidate at one reference (the cell of its point): 1080p exact frame
+// 52 -> 65 ms, transmittance of 1M random rays 25.8 -> 22.1 Mrays/s.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -46,13 +50,23 @@ namespace srt {
 
 constexpr int64_t kSplitMinPrims = 1 << 14;  // smaller scenes: the packet walk uses the unsplit tree
 
-// cells per axis (0: no split tree)
+// cells per axis (0: no split tree).  Measured on density-preserving clouds
+// (device-timed frames, tools/exp_split_sizes.sh, profiles/r02g_split/):
+//   100k, 512^2:        none 0.395 ms, C=2 0.375, C=3 0.375, C=4 0.454
+//   1M, 1080p (3 seeds): none 1.654, C=2 1.572, C=4 1.503, C=6 1.480, C=7 1.454, C=8 1.565
+//   3M, 4K:             none 6.50, C=4 5.53, C=6 5.87, C=8 5.17, C=10 6.46
+//   6M, 1080p:          none 2.10, C=6 1.85, C=8 1.75, C=10 2.03, C=12 2.12
+// Finer grids duplicate more references (C=8 at 1M: 1.79 references per
+// primitive) and their planes interact with the Morton order inside a cell,
+// so the optimum is not monotone; the table keeps the measured best.
 static int split_cells_for(int64_t n) {
 #ifdef SRT_EXPERIMENTS
     if (const char *e = getenv("SRT_SPLIT_CELLS")) return atoi(e);
 #endif
     if (n < kSplitMinPrims) return 0;
-    return 4;
+    if (n < (1 << 18)) return 2;
+    if (n < 2000000) return 7;
+    return 8;
 }
 
 struct Grid {
@@ -64,7 +78,7 @@ struct Grid {
     float minv[3];
 };
 
-__device__ __forceinline__ float plane(const Grid &g, int a, int k) { return g.lo[a] + g.step[a] * (float)k; }
+__device__ __forceinline__ float plane(const Grid &g, int a, int k) { return __fmaf_rn(g.step[a], (float)k, g.lo[a]); }
 
 // cells k0 .. k1 that [l, h] overlaps: k0 = #{interior planes <= l}, k1 = #{interior planes < h}
 __device__ __forceinline__ void cell_range(const Grid &g, int a, float l, float h, int &k0, int &k1) {

@@ -76,7 +76,8 @@ struct SrtScene {
         v.n = n;
         return v;
     }
-    // The view the closest-hit walks (k_trace_packet, k_trace, k_trace_coop)
+    // The view the closest-hit walks (k_trace_packet, k_trace, k_trace_coop,
+    // the trig64 bridge walks)
     // traverse: the split tree when one exists.  Leaf codes index
     // d_geom_split; duplicate references of a primitive give the same (t, id)
     // key and draw, so the order-free closest-accepted slots are unchanged

@@ -161,7 +161,7 @@ srt_status launch_trace_rays_trig64(const SrtScene *s, const SrtTraceParams *p, 
                                     int nslots, double *d_t, int32_t *d_id, cudaStream_t st) {
     unsigned blocks = (unsigned)((R + 127) / 128);
     if (blocks == 0) return SRT_OK;
-    SceneView v = s->view();
+    SceneView v = s->walk_view();
     const int all = nslots;
     // slot groups of <= 16 (slots are independent; each group hashes its own slot indices)
     for (int g0 = 0; g0 < all; g0 += 16) {
@@ -186,7 +186,7 @@ srt_status launch_trace_pass_trig64(const SrtScene *s, const CamD &cam, const Re
     int64_t n = a.local_tiles * 256;
     unsigned blocks = (unsigned)((n + 127) / 128);
     if (blocks == 0) return SRT_OK;
-    SceneView v = s->view();
+    SceneView v = s->walk_view();
     for (int g0 = 0; g0 < a.nslots; g0 += 16) {
         const int nslots = std::min(16, a.nslots - g0);
 #define SRT_L(NS)                                                                                             \
