@@ -202,6 +202,7 @@ srt_status split_build(SrtScene *s, const float *plo, const float *phi, const in
         g.mlo[a] = lo;
         g.minv[a] = flat ? 0.f : 1.0f / ext;
     }
+    if (g.c[0] == 1 && g.c[1] == 1 && g.c[2] == 1) return SRT_OK;  // all centres coincide: nothing to split
     uint32_t *cnt = nullptr, *off = nullptr, *vals = nullptr, *vals2 = nullptr, *rprim = nullptr, *slot_prim = nullptr;
     uint64_t *keys = nullptr, *keys2 = nullptr;
     float *rlo = nullptr, *rhi = nullptr;
