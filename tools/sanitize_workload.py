@@ -83,6 +83,25 @@ def main() -> None:
     sp.build_bvh(np.sqrt(S2))
     sp.render(cam, W, H, 1, 1, 0, S2, True, 0, (0.0, 0.0, 0.0))
     sp.close()
+    # the closest-hit walks' split tree (>= 16,384 primitives), with a few
+    # degenerate primitives whose unbounded boxes land in every cell
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    pk = density_cloud(20_000, seed=2).packed
+    cov = pk.cov_inv6.copy()
+    cov[::4001] = 0.0
+    sp2 = DeviceScene(pk.means, cov, pk.opacities, pk.sh, pk.sh_degree)
+    sp2.build_bvh(np.sqrt(S2))
+    assert sp2.split_info()["num_refs"] >= 20_000
+    for nslots in (1, 4):
+        sp2.render(cam, W, H, 1, nslots, 0, S2, True, 0, (0.0, 0.0, 0.0), out_rgb=pool.array((H, W, 3)),
+                   out_op=pool.array((H, W)))
+        sp2.render(cam, W, H, 3, nslots, 1, S2, True, 0, (0.0, 0.0, 0.0), want_ids=True)
+    sp2.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 1)
+    sp2.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 4)
+    sp2.trace_rays(ho, hd, 0.0, TMAX, 0, S2, True, 2)
+    sp2.trace_rays(o, d, 0.0, TMAX, 0, S2, True, 2, rng="trig64")
+    sp2.close()
     t = two_layer_scene()
     render(t, front_camera(), RenderSettings(width=16, height=16, spp=2))
     render(t, front_camera(), RenderSettings(width=16, height=16, spp=2, reference_mode=True))
