@@ -530,7 +530,7 @@ def run_ours(args) -> None:
             "parallelism": f"tile-shard x{world}" + ("" if world == 1 else (
                 " + fused peer stores into rank 0's frame (CUDA IPC over NVLink) + one all-reduce per frame"
                 if peer is not None else " + NCCL gather to rank 0 + unpack")),
-            "setup": {"scene_setup_s": setup_s, "bvh_build_s": build_s, "bvh": sc.bvh_info(), "build_id": build_id,
+            "setup": {"scene_setup_s": setup_s, "bvh_build_s": build_s, "bvh": sc.bvh_info(), "split_tree": sc.split_info(), "build_id": build_id,
                       "wall_s_timed_region": wall},
             "ranks": [{"rank": i, "step_ms": r[0], "walk_ms": r[1], "gather_ms": r[2], "unpack_ms": r[3],
                        "tiles": int(r[4])} for i, r in enumerate(per_rank)],
