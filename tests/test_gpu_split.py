@@ -127,3 +127,48 @@ def test_split_tree_explicit_rays_equal_unsplit(kind, nslots):
     assert np.isinf(ta[~hit]).all() and np.isinf(tb[~hit]).all()
     a.close()
     b.close()
+
+
+def test_split_tree_follows_the_bvh_lifecycle(oracle):
+    """A rebuild with LBVH or an uploaded reference BVH drops the split tree
+    (the walks then use the tree they were given); a PLOC rebuild restores it."""
+    from paper_2504_06598_b200.scene import DeviceScene
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    asset = density_cloud(20_000, seed=8)
+    sc = DeviceScene.from_packed(asset.packed)
+    sc.build_bvh(CUTOFF)
+    assert sc.split_info()["num_refs"] >= 20_000
+    ref_ids = _frame(sc, 64, 48)[2]
+    sc.build_bvh(CUTOFF, method="lbvh")
+    assert sc.split_info()["num_refs"] == 0
+    np.testing.assert_array_equal(_frame(sc, 64, 48)[2], ref_ids)
+    lo, hi = asset.aabb_arrays(CUTOFF)
+    sc.upload_bvh(oracle.sah_build(lo, hi))
+    assert sc.split_info()["num_refs"] == 0
+    np.testing.assert_array_equal(_frame(sc, 64, 48)[2], ref_ids)
+    sc.build_bvh(CUTOFF)
+    assert sc.split_info()["num_refs"] >= 20_000
+    sc.close()
+
+
+@pytest.mark.parametrize("w,h", [(37, 23), (161, 90)])
+def test_split_tree_odd_frames_equal_unsplit(w, h):
+    """Partial edge packets (per-lane f64 stores) on the split tree."""
+    from paper_2504_06598_b200.render import PinnedPool
+    from paper_2504_06598_b200.synthetic import density_cloud
+
+    a, b = _scenes(density_cloud(40_000, seed=5))
+    pool = PinnedPool()
+    from paper_2504_06598_b200 import front_camera
+    from paper_2504_06598_b200.scene import camera_tuple
+
+    ct = camera_tuple(front_camera(), w, h)
+    ra = a.render(ct, w, h, 1, 1, 0, S2, True, 3, (0.2, 0.1, 0.0), out_rgb=pool.array((h, w, 3)),
+                  out_op=pool.array((h, w)))
+    rb = b.render(ct, w, h, 1, 1, 0, S2, True, 3, (0.2, 0.1, 0.0), out_rgb=pool.array((h, w, 3)),
+                  out_op=pool.array((h, w)))
+    np.testing.assert_array_equal(ra[0], rb[0])
+    np.testing.assert_array_equal(ra[1], rb[1])
+    a.close()
+    b.close()
