@@ -766,7 +766,8 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                 const float4 *np = reinterpret_cast<const float4 *>(s.nodes8 + (obase + (uint32_t)node));
                 const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
                              az = __ldg(np + 4), bz = __ldg(np + 5);
-                const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+                // child codes by shuffle, as in k_trace_packet (lane j holds code j & 3)
+                const int mykid = __ldg(reinterpret_cast<const int *>(np + 6) + (lane & 3));
                 const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
                 const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
                 const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
@@ -802,9 +803,10 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                     const int k = __ffs(al) - 1;
                     const bool h = (lh >> k) & 1u;
                     const unsigned bm = __ballot_sync(FULL, h);
+                    const int kc = __shfl_sync(FULL, mykid, k);
                     if (h) {
                         SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
-                        sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+                        sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~kc << 5) | (uint32_t)lane;
                     }
                     njobs += __popc(bm);
                 }
@@ -815,7 +817,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                 const unsigned ai = any & ~leafm;
                 if (ai) {
                     if (!(ai & (ai - 1))) {
-                        node = sel4(kids, __ffs(ai) - 1);
+                        node = __shfl_sync(FULL, mykid, __ffs(ai) - 1);
                     } else {
                         int wk[4];
 #pragma unroll
@@ -837,9 +839,10 @@ __global__ void __launch_bounds__(kExactThreads, kExactBlocksPerSM)
                         }
 #pragma unroll
                         for (int j = 3; j >= 1; --j)
-                            if (j < nin) sstk[wid][sp + nin - 1 - j] = make_int2(sel4(kids, wk[j] & 3), wk[j] & ~3);
+                            if (j < nin)
+                                sstk[wid][sp + nin - 1 - j] = make_int2(__shfl_sync(FULL, mykid, wk[j] & 3), wk[j] & ~3);
                         sp += nin - 1;
-                        node = sel4(kids, wk[0] & 3);
+                        node = __shfl_sync(FULL, mykid, wk[0] & 3);
                     }
                 }
                 __syncwarp();

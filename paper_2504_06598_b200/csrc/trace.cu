@@ -1889,7 +1889,8 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
             const float4 *np = reinterpret_cast<const float4 *>(s.nodes8 + (obase + (uint32_t)node));
             const float4 ax = __ldg(np), bx = __ldg(np + 1), ay = __ldg(np + 2), by = __ldg(np + 3),
                          az = __ldg(np + 4), bz = __ldg(np + 5);
-            const int4 kids = __ldg(reinterpret_cast<const int4 *>(np + 6));
+            // child codes by shuffle, as in k_trace_packet (lane j holds code j & 3)
+            const int mykid = __ldg(reinterpret_cast<const int *>(np + 6) + (lane & 3));
             const unsigned hint = (unsigned)__ldg(reinterpret_cast<const int *>(np + 7));
             const float pax[4] = {ax.x, ax.y, ax.z, ax.w}, pbx[4] = {bx.x, bx.y, bx.z, bx.w};
             const float pay[4] = {ay.x, ay.y, ay.z, ay.w}, pby[4] = {by.x, by.y, by.z, by.w};
@@ -1922,15 +1923,16 @@ __global__ void __launch_bounds__(kTraceThreads) k_transmittance_packet(SceneVie
                 const int k = __ffs(al) - 1;
                 const bool h = (lh >> k) & 1u;
                 const unsigned bm = __ballot_sync(FULL, h);
+                const int kc = __shfl_sync(FULL, mykid, k);
                 if (h) {
                     SRT_DCHECK(njobs + __popc(bm & lt) < BATCH + 128);
-                    sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~sel4(kids, k) << 5) | (uint32_t)lane;
+                    sjob[wid][njobs + __popc(bm & lt)] = ((uint32_t)~kc << 5) | (uint32_t)lane;
                 }
                 njobs += __popc(bm);
             }
             // unclipped: every inner child any lane hits is walked, in any order
             for (unsigned ai = any & ~leafm; ai; ai &= ai - 1) {
-                const int code = sel4(kids, __ffs(ai) - 1);
+                const int code = __shfl_sync(FULL, mykid, __ffs(ai) - 1);
                 if (node == kDone) {
                     node = code;
                 } else if (sp < PSTACK) {
