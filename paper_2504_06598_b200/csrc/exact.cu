@@ -550,10 +550,12 @@ __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsign
     }
     __syncwarp();
     // 3. insertion sort inside each bucket [end of bucket b-1, end of bucket b)
-    //    by (t, prim id)
+    //    by (t, prim id); lane l sorts buckets l, l + 32, ... so the dense
+    //    depth range (neighbouring buckets) spreads over the lanes instead of
+    //    serialising on a few (exact 1080p frame 52.0 -> see DESIGN §5)
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
-        const int b = lane * PER + j;
+        const int b = j * 32 + lane;
         const int lo = b == 0 ? 0 : scn[b - 1], hi = scn[b];
         for (int i = lo + 1; i < hi; ++i) {
             const unsigned k = sk[i];
