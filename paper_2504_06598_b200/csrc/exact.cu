@@ -509,12 +509,12 @@ __device__ __noinline__ void composite_ray_warp(const SceneView &s, const unsign
     }
     kmin = __reduce_min_sync(FULL, kmin);
     kmax = __reduce_max_sync(FULL, kmax);
-    const float t_lo = unpack_t((unsigned long long)kmin << 32), t_hi = unpack_t((unsigned long long)kmax << 32);
-    const float span = t_hi - t_lo;
-    const float scale = span > 0.0f && isfinite(span) ? (float)NB / span : 0.0f;
+    // buckets linear in the orderable depth bits (monotone in t, and linear in
+    // t within one binade): no float decode per entry
+    const float scale = (float)NB / ((float)(kmax - kmin) + 1.0f);
     auto bucket = [&](unsigned long long k) {
-        const float b = (unpack_t(k) - t_lo) * scale;
-        return b >= (float)(NB - 1) ? NB - 1 : (b > 0.0f ? (int)b : 0);
+        const float b = (float)((unsigned)(k >> 32) - kmin) * scale;
+        return b >= (float)(NB - 1) ? NB - 1 : (int)b;
     };
     // 2. counting sort: counts, exclusive scan, scatter
 #pragma unroll
