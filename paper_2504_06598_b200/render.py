@@ -188,8 +188,11 @@ def render_biased(asset, camera: CameraConfig, settings: RenderSettings, k: int,
     sc = prepare(asset, settings, bvh, device)
     cam = camera_tuple(camera, settings.width, settings.height)
     mode = 0 if settings.depth_mode == "mean" else 1
+    # pooled mapped page-locked output, as render(): 8.8 -> 5.6 ms for the 1080p
+    # k=4 frame against a fresh pageable array (profiles/r02m_resolve/)
     return sc.render_biased(cam, settings.width, settings.height, int(k), settings.passes, mode,
-                            settings.cutoff_s * settings.cutoff_s, settings.seed, settings.background, rng=rng)
+                            settings.cutoff_s * settings.cutoff_s, settings.seed, settings.background, rng=rng,
+                            out_rgb=_PINNED.array((settings.height, settings.width, 3)))
 
 
 def image_metrics(image: AccumBuffer, reference: AccumBuffer) -> dict:
